@@ -1,0 +1,34 @@
+"""CPU oracle for the randomized discrete sparse Fourier transform of
+Merhi, Zhang, Iwen, Christlieb, "A New Class of Fully Discrete Sparse Fourier
+Transforms" (arXiv 1706.02740; `/root/reference/PAPER.md`).
+
+TEST INFRASTRUCTURE ONLY.  Nothing in the product path may import this
+package: only `tests/`, `__graft_entry__.smoke()` and `bench.py`'s
+`cpu_baseline` / `--impl reference` legs call it.  It shares no code, tables
+or constants with the CUDA path (`paper_1706_02740_b200/`); the only module
+both sides use is the seeded input generator `dsft_synth/`, which holds none
+of the method's arithmetic.
+
+The oracle is plain numpy in float64 / complex128 and follows Algorithm 1
+ step by step, with the inner randomized SFT 𝒜 (line 9)
+given by the reading fixed in DESIGN.md §3 ("readings").  Every function cites
+the passage it implements.  Pins (tests/test_oracle_*.py, `-m "not gpu"`)
+check it against closed forms, brute force and the paper's bounds.
+
+Parity status per function (DESIGN.md §4 lists the pin for each):
+  conventions.*            pinned (brute-force F matrix)
+  filt.ghat / filt.g       pinned (Lemma 2 vs quadrature of eq. (4))
+  params.derive_plan       pinned (worked values, Lemma 3 exhaustive, coverage)
+  numtheory.*              pinned (brute-force CRT / sieve / SplitMix64 vectors)
+  dsft.filtered_samples    pinned (closed form within Theorem 4 bound)
+  dsft.alias_dft           pinned (brute-force DFT, aliasing identity)
+  dsft.identify / vote     pinned (brute-force CRT, planted isolated tones)
+  dsft.estimate / merge    pinned (planted exact inversion, brute-force sort)
+  dsft.dsft (end to end)   pinned (brute-force DFT on tiny N; Theorem 5 bound)
+  inner-SFT design constants (c_b, T, v_min, pool rule, residue rule):
+                           parity unpinned -- the paper prints no values for
+                           them; only invariants pin them.
+"""
+
+from .params import OracleParams, Plan, derive_plan  # noqa: F401
+from .dsft import dsft  # noqa: F401

@@ -1,0 +1,182 @@
+"""Parameter derivation for Algorithm 1 (test infrastructure only).
+
+Follows PAPER.md:
+  * Lemma 3: tau in (0, 1/sqrt(2 pi)), alpha in [1, N/sqrt(ln N)],
+    beta <= alpha*sqrt(ln(1/(tau sqrt(2 pi)))/2), c1 = beta sqrt(ln N)/N.
+  * Algorithm 1 line 2: c2 = alpha sqrt(ln N)/2; lines 3-4
+    (PAPER.md:233-234): q_j = -ceil(N/2) + 1 + (2j-1) ceil(N/(alpha sqrt(ln N))),
+    j = 1..ceil(c2).
+  * Theorem 4: beta = 6 sqrt(r),
+    kappa = ceil(6 r ln N/(sqrt(2) pi)) + 1  (preset THM4).
+  * Section 5: DMSFT-4 / DMSFT-6 use kappa = 4 / 6 (presets).
+  * Section 4: tau = 1/3 default; alpha from beta (reading R2).
+Readings R1..R12 are listed in DESIGN.md §3.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+from .numtheory import draw_distinct, largest_prime_factor, primes_below
+
+PRESET_DMSFT6 = "dmsft6"
+PRESET_DMSFT4 = "dmsft4"
+PRESET_THM4 = "thm4"
+
+# Largest prime factor allowed in P-1 for a bucket prime P (reading R6: every
+# bucket DFT is evaluated by the GPU as a Rader convolution over a mixed-radix
+# FFT of length P-1; the oracle mirrors only the pool rule, not the algorithm).
+RADER_SMOOTH = 13
+
+
+class ConfigError(ValueError):
+    """Invalid (N, s, params) combination (the C-ABI's DSFT_ERR_CONFIG)."""
+
+
+@dataclass
+class OracleParams:
+    preset: str = PRESET_DMSFT6
+    r: float = 1.0            # THM4 decay exponent
+    kappa: int = 0            # 0 = preset value
+    tau: float = 1.0 / 3.0
+    alpha_rule: str = "corrected"  # reading R2; "literal" = PAPER.md:597 as printed
+    bucket_factor: float = 4.0     # c_b (reading R6)
+    n_bucket_primes: int = 5       # T   (reading R6)
+    vote_min: int = 3              # v_min (reading R9: > T/2)
+    band_budget: int = 0           # 0 = s (reading R11)
+    seed: int = 0
+
+
+@dataclass
+class Plan:
+    N: int
+    s: int
+    preset: str
+    kappa: int
+    beta: float
+    c1: float
+    tau: float
+    alpha: float
+    w: int
+    J: int
+    q: list[int]
+    B_lo: int            # smallest element of B = (-ceil(N/2), floor(N/2)]
+    B_hi: int            # largest element of B
+    pool: list[int]
+    primes: list[int]    # P_t, t = 0..T-1, ascending
+    residues: list[list[int]] = field(default_factory=list)  # r_{t,i}
+    vote_min: int = 3
+    band_budget: int = 0
+    seed: int = 0
+
+    @property
+    def T(self) -> int:
+        return len(self.primes)
+
+    def grid_lengths(self, t: int) -> list[int]:
+        """Aliasing grid lengths L_{t,i} = P_t * r_{t,i} (s_j)."""
+        return [self.primes[t] * r for r in self.residues[t]]
+
+
+def odd_primes(count_hint: int = 64) -> list[int]:
+    return [p for p in primes_below(512) if p > 2][:count_hint]
+
+
+def bucket_pool(s: int, bucket_factor: float) -> list[int]:
+    """Reading R6: primes P in [ceil(c_b s), 2 ceil(c_b s)) whose P-1 has no
+    prime factor above 13.  PAPER.md:175-177 / 845-850 fix only that the
+    moduli are primes and that the randomized variant reads a random subset."""
+    lo = int(math.ceil(bucket_factor * s))
+    hi = 2 * lo
+    return [p for p in primes_below(hi) if p >= lo and largest_prime_factor(p - 1) <= RADER_SMOOTH]
+
+
+def passband_plan(N: int, alpha: float) -> tuple[int, int, list[int]]:
+    """Algorithm 1 lines 2-4: half-width
+    w = ceil(N/(alpha sqrt(ln N))), J = ceil(c2) = ceil(alpha sqrt(ln N)/2) bands,
+    centres q_j = -ceil(N/2) + 1 + (2j-1) w, j = 1..J."""
+    lnN = math.log(N)
+    w = int(math.ceil(N / (alpha * math.sqrt(lnN))))
+    J = int(math.ceil(alpha * math.sqrt(lnN) / 2.0))
+    halfN_up = (N + 1) // 2
+    q = [-halfN_up + 1 + (2 * j - 1) * w for j in range(1, J + 1)]
+    return w, J, q
+
+
+def derive_plan(N: int, s: int, params: OracleParams | None = None) -> Plan:
+    """Derive every parameter Algorithm 1 needs."""
+    p = params or OracleParams()
+    if N < 36:
+        raise ConfigError("N must be >= 36 (Theorem 4 needs N >= 36 r, PAPER.md:498)")
+    if not (2 <= s <= N):
+        raise ConfigError("s must lie in [2, N] (PAPER.md:40)")
+    if not (0.0 < p.tau < 1.0 / math.sqrt(2.0 * math.pi)):
+        raise ConfigError("tau must lie in (0, 1/sqrt(2 pi)) (Lemma 3, PAPER.md:149)")
+    lnN = math.log(N)
+
+    # beta and kappa (Theorem 4 / Section 5 presets; reading R4 for DMSFT).
+    if p.preset == PRESET_THM4:
+        if not (1.0 <= p.r <= N / 36.0):
+            raise ConfigError("r must lie in [1, N/36] (PAPER.md:498)")
+        beta = 6.0 * math.sqrt(p.r)
+        kappa = int(math.ceil(6.0 * p.r * lnN / (math.sqrt(2.0) * math.pi))) + 1
+    elif p.preset in (PRESET_DMSFT6, PRESET_DMSFT4):
+        kappa = 6 if p.preset == PRESET_DMSFT6 else 4
+        beta = None
+    else:
+        raise ConfigError(f"unknown preset {p.preset!r}")
+    if p.kappa > 0:
+        kappa = int(p.kappa)
+    if beta is None:
+        # R4: balance Lemma 10's truncation exponent 2 pi^2 kappa^2/(beta^2 ln N)
+        # against Lemma 9's aliasing exponent beta^2 ln N / 8.
+        beta = math.sqrt(4.0 * math.pi * kappa / lnN)
+    if 2 * kappa + 2 > N:
+        raise ConfigError("window 2 kappa + 2 must fit in N (SPEC.md:256)")
+
+    c1 = beta * math.sqrt(lnN) / N  # Algorithm 1 line 2
+    if not c1 < 0.5:
+        raise ConfigError("c1 >= 0.5: periodization images not negligible (reading R5)")
+
+    # alpha (Lemma 3 admissibility; reading R2 for the Section 4 typo).
+    lg = math.log(1.0 / (p.tau * math.sqrt(2.0 * math.pi)))
+    if p.alpha_rule == "corrected":
+        alpha = beta / math.sqrt(lg / 2.0)
+    elif p.alpha_rule == "literal":
+        alpha = beta * math.sqrt(2.0) / lg
+    else:
+        raise ConfigError(f"unknown alpha_rule {p.alpha_rule!r}")
+    alpha = min(max(alpha, 1.0), N / math.sqrt(lnN))
+
+    w, J, q = passband_plan(N, alpha)
+    B_lo = -((N + 1) // 2) + 1
+    B_hi = N // 2
+
+    # Inner SFT (reading R6-R8): bucket primes and residue primes.
+    T = int(p.n_bucket_primes)
+    if T < 1:
+        raise ConfigError("need at least one bucket prime")
+    pool = bucket_pool(s, p.bucket_factor)
+    if len(pool) < T:
+        raise ConfigError(f"bucket-prime pool has {len(pool)} < T={T} primes")
+    primes = draw_distinct(pool, T, p.seed)
+    rp = odd_primes()
+    residues = []
+    for P in primes:
+        rs = []
+        prod = P
+        while prod < N or not rs:          # R8: at least one residue prime
+            r = rp[len(rs)]
+            rs.append(r)
+            prod *= r
+        if rs[-1] >= P:
+            raise ConfigError("residue primes must be smaller than the bucket primes")
+        residues.append(rs)
+    if not (1 <= p.vote_min <= T):
+        raise ConfigError("vote_min must lie in [1, T]")
+    budget = int(p.band_budget) if p.band_budget > 0 else s
+
+    return Plan(N=N, s=s, preset=p.preset, kappa=kappa, beta=beta, c1=c1, tau=p.tau,
+                alpha=alpha, w=w, J=J, q=q, B_lo=B_lo, B_hi=B_hi, pool=pool, primes=primes,
+                residues=residues, vote_min=int(p.vote_min), band_budget=budget, seed=int(p.seed))
