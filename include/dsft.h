@@ -1,0 +1,196 @@
+/*
+ * dsft.h -- C ABI of the B200-native randomized discrete sparse Fourier
+ * transform (Merhi, Zhang, Iwen, Christlieb, arXiv 1706.02740; PAPER.md).
+ *
+ * The library computes Algorithm 1 with the randomized
+ * inner SFT of DESIGN.md §3 on an NVIDIA B200 (sm_100a):
+ *   K1 gather_mix  filtered sampling, Algorithm 1 lines 5-7 (PAPER.md:235-237,
+ *                  Lemma 10 / Theorem 4 window)
+ *   K2 prime_dft   aliasing DFTs E_j, Good-Thomas + Rader
+ *   K3 identify    residue argmax + CRT (reading R7)
+ *   K4/K5 vote_estimate  majority vote, passband (line 10),
+ *                  Re/Im medians, unbias (line 11)
+ *   K6 merge       top-s (line 13; ties PAPER.md:113)
+ *
+ * Conventions (all entry points):
+ *  - Complex data is interleaved float64 (re, im): identical to
+ *    torch.complex128 / cuDoubleComplex.  Signal f_j = f(-pi + 2 pi j / N)
+ *    (PAPER.md:87); coefficients are returned in the paper's convention
+ *    fhat = F f, F_{omega,j} = ((-1)^omega / N) e^{-2 pi i omega j / N}
+ *    (PAPER.md:82); frequencies omega lie in B = (-ceil(N/2), floor(N/2)]
+ *    (PAPER.md:84).
+ *  - `_dev` pointers are CUDA device pointers owned by the caller; `_host`
+ *    pointers are host memory owned by the caller.  The library never frees
+ *    caller memory.  `stream` is a cudaStream_t passed as void* (NULL = legacy
+ *    default stream).
+ *  - Every function returns dsft_status; nothing is thrown across the ABI.
+ *    On error a message is available from dsft_last_error() (thread-local).
+ *    Device-side faults are asynchronous and surface at the caller's next
+ *    synchronisation; launch errors are returned immediately.
+ *  - A plan is immutable after creation except for its workspace; one
+ *    in-flight execute per plan (use one plan per concurrent stream).
+ */
+#ifndef DSFT_H
+#define DSFT_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DSFT_MAX_T 16   /* bucket primes per plan                        */
+#define DSFT_MAX_K 10   /* residue primes per bucket prime               */
+#define DSFT_MAX_J 128  /* passbands (Algorithm 1 line 3: ceil(c2))      */
+
+typedef struct { double re, im; } dsft_c128;
+typedef struct dsft_plan dsft_plan;
+typedef struct dsft_comm dsft_comm;
+
+typedef enum {
+  DSFT_OK = 0,
+  DSFT_ERR_CONFIG = 2,   /* (N, s, params) outside the admissible domain   */
+  DSFT_ERR_ARG = 3,      /* NULL / misaligned pointer, bad size            */
+  DSFT_ERR_CUDA = 4,
+  DSFT_ERR_NCCL = 5,
+  DSFT_ERR_NOMEM = 6,
+  DSFT_ERR_INTERNAL = 7,
+  DSFT_ERR_UNSUPPORTED = 8 /* valid config this build cannot run yet       */
+} dsft_status;
+
+enum { DSFT_PRESET_DMSFT6 = 0, DSFT_PRESET_DMSFT4 = 1, DSFT_PRESET_THM4 = 2 };
+enum { DSFT_ALPHA_CORRECTED = 0, DSFT_ALPHA_LITERAL = 1 };
+
+/* Parameters of Algorithm 1 and of the inner SFT.
+ *  preset        DMSFT6 (kappa = 6), DMSFT4 (kappa = 4)  -- PAPER.md:653;
+ *                THM4 (beta = 6 sqrt r, kappa from Theorem 4)
+ *  r             THM4 decay exponent, 1 <= r <= N/36
+ *  kappa         window half-width override (0 = preset)
+ *  tau           passband floor, 0 < tau < 1/sqrt(2 pi) (Lemma 3)
+ *  alpha_rule    CORRECTED (reading R2) or LITERAL (PAPER.md:597 as printed)
+ *  bucket_factor c_b: bucket primes drawn from [ceil(c_b s), 2 ceil(c_b s))
+ *  n_bucket_primes T (<= DSFT_MAX_T); vote_min v_min in [1, T]
+ *  band_budget   entries kept per band after line 9 (0 = s; reading R11)
+ *  seed          SplitMix64 seed of the bucket-prime draw (reading R7)   */
+typedef struct {
+  int32_t preset;
+  double r;
+  int32_t kappa;
+  double tau;
+  int32_t alpha_rule;
+  double bucket_factor;
+  int32_t n_bucket_primes;
+  int32_t vote_min;
+  int64_t band_budget;
+  uint64_t seed;
+} dsft_params;
+
+/* Derived plan quantities, for oracle cross-checks (read-only copy). */
+typedef struct {
+  int64_t N, s;
+  int32_t preset, kappa, J, T;
+  int64_t w;                    /* passband half-width ceil(N/(alpha sqrt lnN)) */
+  double beta, c1, alpha, tau;
+  int64_t q1;                   /* first band centre; q_j = q1 + 2 (j-1) w     */
+  int32_t vote_min;
+  int64_t band_budget;
+  int64_t primes[DSFT_MAX_T];   /* P_t ascending                               */
+  int32_t n_residues[DSFT_MAX_T];
+  int32_t residues[DSFT_MAX_T][DSFT_MAX_K];
+  int32_t n_shifts[DSFT_MAX_T]; /* S_t = 1 + sum_i (r_{t,i} - 1)               */
+  int64_t nodes;                /* sum_t S_t P_t: distinct sample nodes        */
+  int64_t grid_points;          /* sum_t sum_i P_t r_{t,i}                     */
+  int64_t sum_primes;           /* sum_t P_t                                   */
+} dsft_plan_info;
+
+void dsft_params_default(dsft_params* p);
+const char* dsft_status_string(dsft_status st);
+const char* dsft_last_error(void);
+const char* dsft_version(void);
+
+/* Derive the plan for length N and sparsity s; uploads the plan tables to the
+ * current CUDA device (the only host->device copy outside execute).  Returns
+ * DSFT_ERR_CONFIG and leaves *out untouched for an invalid configuration:
+ * N < 36, s outside [2, N], tau outside (0, 1/sqrt(2 pi)), THM4 r outside
+ * [1, N/36], 2 kappa + 2 > N, c1 >= 1/2, fewer than T primes in the pool,
+ * residue primes not below the bucket primes, vote_min outside [1, T]. */
+dsft_status dsft_plan_create(int64_t N, int64_t s, const dsft_params* params, dsft_plan** out);
+void dsft_plan_destroy(dsft_plan* plan);
+dsft_status dsft_plan_get_info(const dsft_plan* plan, dsft_plan_info* info);
+
+/* Host-only derivation of the same quantities (no CUDA call; same validation
+ * and error codes as dsft_plan_create). */
+dsft_status dsft_plan_derive_info(int64_t N, int64_t s, const dsft_params* params, dsft_plan_info* info);
+
+/* Device workspace for `batch` vectors processed concurrently.  If never set,
+ * execute allocates it on first use and the plan frees it on destroy.  A
+ * caller-provided workspace (>= dsft_plan_workspace_bytes, 256-B aligned) is
+ * borrowed, never freed. */
+size_t dsft_plan_workspace_bytes(const dsft_plan* plan, int64_t batch);
+dsft_status dsft_plan_set_workspace(dsft_plan* plan, void* dev, size_t bytes);
+
+/* One transform.  f_dev: N contiguous dsft_c128, 16-B aligned, read-only.
+ * freqs_out_dev[s], coeffs_out_dev[s]: sorted by (|c| desc, omega asc); unused
+ * slots hold omega = INT64_MIN, c = 0.  Asynchronous, stream-ordered. */
+dsft_status dsft_execute(dsft_plan* plan, const dsft_c128* f_dev, int64_t* freqs_out_dev,
+                         dsft_c128* coeffs_out_dev, void* stream);
+
+/* `batch` independent vectors f_dev + b*ld (ld >= N), same plan (same primes)
+ * for each; outputs [batch][s]. */
+dsft_status dsft_execute_batched(dsft_plan* plan, const dsft_c128* f_dev, int64_t batch, int64_t ld,
+                                 int64_t* freqs_out_dev, dsft_c128* coeffs_out_dev, void* stream);
+
+/* End-to-end variant with HOST buffers: copies f_host (pinned or pageable) to
+ * the device, executes, copies the result back, and synchronises `stream`. */
+dsft_status dsft_execute_host(dsft_plan* plan, const dsft_c128* f_host, int64_t* freqs_out_host,
+                              dsft_c128* coeffs_out_host, void* stream);
+
+/* Number of kernels one dsft_execute launches (for bench bookkeeping). */
+int64_t dsft_plan_launches_per_execute(const dsft_plan* plan);
+
+/* Optional per-kernel timing.  When enabled, every launch is bracketed by a
+ * CUDA event pair recorded on the launching stream.  dsft_plan_collect_times
+ * waits for those events and returns, per kernel class (0 K1 gather_mix,
+ * 1 K2 prime_dft, 2 K3 identify, 3 K45 vote_estimate, 4 K6 merge), the summed
+ * milliseconds and launch counts since the previous collect. */
+#define DSFT_KERNEL_CLASSES 5
+dsft_status dsft_plan_set_timing(dsft_plan* plan, int32_t enable);
+dsft_status dsft_plan_collect_times(dsft_plan* plan, double* ms_out, int64_t* launches_out);
+
+/* ---- multi-GPU (NCCL loaded with dlopen; one process per GPU) ----------
+ * dsft_comm_get_unique_id writes NCCL's 128-byte unique id on rank 0; the
+ * caller broadcasts it (e.g. torch.distributed) and every rank calls
+ * dsft_comm_create.  dsft_execute_sharded: f_dev replicated on every rank;
+ * rank rho computes the bands j = rho (mod world), then one ncclAllGather of
+ * the fixed-capacity per-band result blocks and the merge run on every rank,
+ * so all ranks end with the identical result.  dsft_execute_batched_sharded:
+ * each rank passes its own slice of vectors (no exchange needed; outputs are
+ * per-rank). */
+dsft_status dsft_comm_get_unique_id(void* out128);
+/* Host-only: the bands j = rank (mod world) a rank computes (bands_out[J]). */
+void dsft_shard_bands(int32_t J, int32_t rank, int32_t world, int32_t* bands_out, int32_t* nbands_out);
+dsft_status dsft_comm_create(int32_t rank, int32_t world, const void* unique_id128, dsft_comm** out);
+void dsft_comm_destroy(dsft_comm* comm);
+dsft_status dsft_execute_sharded(dsft_plan* plan, dsft_comm* comm, const dsft_c128* f_dev,
+                                 int64_t* freqs_out_dev, dsft_c128* coeffs_out_dev, void* stream);
+
+/* ---- parity hooks (tests only; same kernels as execute) ----------------
+ * dsft_debug_grid: run K1 (what = 0: filtered samples h_q(x_k), k < L) or
+ * K1+K2 (what = 1: E[b] = (1/L) sum_k h_q(x_k) e^{-2 pi i k b/L}, b < L) of
+ * band `band`, bucket prime t, residue i, grid L = P_t r_{t,i}, into
+ * out_dev[L] in natural order.
+ * dsft_debug_copy: after an execute, copy an internal buffer of vector 0:
+ *   which = 0: candidates  int64 [J][sum_t P_t]   (omega' or INT64_MIN)
+ *   which = 1: band counts int32 [J]
+ *   which = 2: band omegas int64 [J][band_budget]
+ *   which = 3: band coeffs dsft_c128 [J][band_budget] (unbiased c)
+ *   which = 4: band z      dsft_c128 [J][band_budget] (before unbiasing)   */
+dsft_status dsft_debug_grid(dsft_plan* plan, const dsft_c128* f_dev, int32_t band, int32_t t, int32_t i,
+                            int32_t what, dsft_c128* out_dev, void* stream);
+dsft_status dsft_debug_copy(dsft_plan* plan, int32_t which, void* dst_dev, size_t bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DSFT_H */

@@ -1,0 +1,243 @@
+"""Thin Python binding of libdsft (include/dsft.h): argument marshalling only.
+
+Every step of the transform runs in the CUDA kernels of libdsft.so
+(paper_1706_02740_b200/csrc).  There is no CPU fallback: importing this
+package fails loudly if the library has not been built, and every call that
+returns a non-OK status raises DsftError.  PyTorch is used only to own device
+memory and streams (tensor.data_ptr() / stream.cuda_stream are passed through).
+
+Function names mirror the C ABI: dsft_plan_create, dsft_execute, ...
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import re
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libdsft.so")
+HEADER = os.path.join(os.path.dirname(HERE), "include", "dsft.h")
+
+DSFT_MAX_T, DSFT_MAX_K, DSFT_MAX_J = 16, 10, 128
+DSFT_OK, DSFT_ERR_CONFIG, DSFT_ERR_ARG, DSFT_ERR_CUDA = 0, 2, 3, 4
+DSFT_ERR_NCCL, DSFT_ERR_NOMEM, DSFT_ERR_INTERNAL, DSFT_ERR_UNSUPPORTED = 5, 6, 7, 8
+PRESETS = {"dmsft6": 0, "dmsft4": 1, "thm4": 2}
+ALPHA_RULES = {"corrected": 0, "literal": 1}
+SENTINEL = -(1 << 63)
+
+
+class DsftError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"dsft status {status}: {msg}")
+        self.status = status
+
+
+class dsft_params(C.Structure):
+    _fields_ = [("preset", C.c_int32), ("r", C.c_double), ("kappa", C.c_int32), ("tau", C.c_double),
+                ("alpha_rule", C.c_int32), ("bucket_factor", C.c_double), ("n_bucket_primes", C.c_int32),
+                ("vote_min", C.c_int32), ("band_budget", C.c_int64), ("seed", C.c_uint64)]
+
+
+class dsft_plan_info(C.Structure):
+    _fields_ = [("N", C.c_int64), ("s", C.c_int64), ("preset", C.c_int32), ("kappa", C.c_int32),
+                ("J", C.c_int32), ("T", C.c_int32), ("w", C.c_int64), ("beta", C.c_double), ("c1", C.c_double),
+                ("alpha", C.c_double), ("tau", C.c_double), ("q1", C.c_int64), ("vote_min", C.c_int32),
+                ("band_budget", C.c_int64), ("primes", C.c_int64 * DSFT_MAX_T),
+                ("n_residues", C.c_int32 * DSFT_MAX_T), ("residues", (C.c_int32 * DSFT_MAX_K) * DSFT_MAX_T),
+                ("n_shifts", C.c_int32 * DSFT_MAX_T), ("nodes", C.c_int64), ("grid_points", C.c_int64),
+                ("sum_primes", C.c_int64)]
+
+
+_P = C.c_void_p
+_SIGS = {
+    "dsft_params_default": (None, [C.POINTER(dsft_params)]),
+    "dsft_status_string": (C.c_char_p, [C.c_int]),
+    "dsft_last_error": (C.c_char_p, []),
+    "dsft_version": (C.c_char_p, []),
+    "dsft_plan_create": (C.c_int, [C.c_int64, C.c_int64, C.POINTER(dsft_params), C.POINTER(_P)]),
+    "dsft_plan_destroy": (None, [_P]),
+    "dsft_plan_get_info": (C.c_int, [_P, C.POINTER(dsft_plan_info)]),
+    "dsft_plan_derive_info": (C.c_int, [C.c_int64, C.c_int64, C.POINTER(dsft_params), C.POINTER(dsft_plan_info)]),
+    "dsft_plan_workspace_bytes": (C.c_size_t, [_P, C.c_int64]),
+    "dsft_plan_set_workspace": (C.c_int, [_P, _P, C.c_size_t]),
+    "dsft_execute": (C.c_int, [_P, _P, _P, _P, _P]),
+    "dsft_execute_batched": (C.c_int, [_P, _P, C.c_int64, C.c_int64, _P, _P, _P]),
+    "dsft_execute_host": (C.c_int, [_P, _P, _P, _P, _P]),
+    "dsft_plan_launches_per_execute": (C.c_int64, [_P]),
+    "dsft_plan_set_timing": (C.c_int, [_P, C.c_int32]),
+    "dsft_plan_collect_times": (C.c_int, [_P, C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
+    "dsft_comm_get_unique_id": (C.c_int, [_P]),
+    "dsft_shard_bands": (None, [C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
+    "dsft_comm_create": (C.c_int, [C.c_int32, C.c_int32, _P, C.POINTER(_P)]),
+    "dsft_comm_destroy": (None, [_P]),
+    "dsft_execute_sharded": (C.c_int, [_P, _P, _P, _P, _P, _P]),
+    "dsft_debug_grid": (C.c_int, [_P, _P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _P, _P]),
+    "dsft_debug_copy": (C.c_int, [_P, C.c_int32, _P, C.c_size_t, _P]),
+}
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Load libdsft.so (built in-tree); raises if it is missing -- no fallback."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} not built: run `python -m paper_1706_02740_b200.build` "
+                              "(there is no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        for name, (res, args) in _SIGS.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def header_functions() -> list[str]:
+    """Names of every function include/dsft.h declares."""
+    txt = open(HEADER).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"\b(dsft_[a-z0-9_]+)\s*\(", txt)))
+
+
+def _check(st: int) -> None:
+    if st != DSFT_OK:
+        raise DsftError(st, lib().dsft_last_error().decode())
+
+
+def make_params(preset: str = "dmsft6", r: float = 1.0, kappa: int = 0, tau: float = 1.0 / 3.0,
+                alpha_rule: str = "corrected", bucket_factor: float = 4.0, n_bucket_primes: int = 5,
+                vote_min: int = 3, band_budget: int = 0, seed: int = 0) -> dsft_params:
+    p = dsft_params()
+    lib().dsft_params_default(C.byref(p))
+    p.preset = PRESETS[preset]
+    p.r, p.kappa, p.tau = r, kappa, tau
+    p.alpha_rule = ALPHA_RULES[alpha_rule]
+    p.bucket_factor, p.n_bucket_primes, p.vote_min = bucket_factor, n_bucket_primes, vote_min
+    p.band_budget, p.seed = band_budget, seed
+    return p
+
+
+def dsft_plan_derive_info(N: int, s: int, params: dsft_params | None = None) -> dsft_plan_info:
+    info = dsft_plan_info()
+    _check(lib().dsft_plan_derive_info(N, s, C.byref(params) if params is not None else None, C.byref(info)))
+    return info
+
+
+def dsft_shard_bands(J: int, rank: int, world: int) -> list[int]:
+    out = (C.c_int32 * max(J, 1))()
+    n = C.c_int32(0)
+    lib().dsft_shard_bands(J, rank, world, out, C.byref(n))
+    return list(out[:n.value])
+
+
+def _stream_ptr(stream) -> int | None:
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    return stream if isinstance(stream, int) else stream.cuda_stream
+
+
+class Plan:
+    """Owns a dsft_plan; tensors are torch CUDA tensors (complex128 / int64)."""
+
+    def __init__(self, N: int, s: int, params: dsft_params | None = None, **kw):
+        self.params = params if params is not None else make_params(**kw)
+        h = _P()
+        _check(lib().dsft_plan_create(N, s, C.byref(self.params), C.byref(h)))
+        self._h = h
+        self.N, self.s = N, s
+        self.info = dsft_plan_info()
+        _check(lib().dsft_plan_get_info(self._h, C.byref(self.info)))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().dsft_plan_destroy(self._h)
+            self._h = None
+
+    __del__ = close
+
+    @property
+    def handle(self):
+        return self._h
+
+    def primes(self) -> list[int]:
+        return list(self.info.primes[:self.info.T])
+
+    def residues(self) -> list[list[int]]:
+        return [list(self.info.residues[t][:self.info.n_residues[t]]) for t in range(self.info.T)]
+
+    def launches_per_execute(self) -> int:
+        return int(lib().dsft_plan_launches_per_execute(self._h))
+
+    KERNEL_CLASSES = ("k1_gather_mix", "k2_prime_dft", "k3_identify", "k45_vote_estimate", "k6_merge")
+
+    def dsft_plan_set_timing(self, enable: bool):
+        _check(lib().dsft_plan_set_timing(self._h, 1 if enable else 0))
+
+    def dsft_plan_collect_times(self) -> dict:
+        ms = (C.c_double * 5)()
+        n = (C.c_int64 * 5)()
+        _check(lib().dsft_plan_collect_times(self._h, ms, n))
+        return {k: (ms[i], n[i]) for i, k in enumerate(self.KERNEL_CLASSES)}
+
+    def dsft_execute(self, f, freqs_out, coeffs_out, stream=None):
+        _check(lib().dsft_execute(self._h, f.data_ptr(), freqs_out.data_ptr(), coeffs_out.data_ptr(),
+                                  _stream_ptr(stream)))
+
+    def dsft_execute_batched(self, f, batch: int, ld: int, freqs_out, coeffs_out, stream=None):
+        _check(lib().dsft_execute_batched(self._h, f.data_ptr(), batch, ld, freqs_out.data_ptr(),
+                                          coeffs_out.data_ptr(), _stream_ptr(stream)))
+
+    def dsft_execute_host(self, f_host, freqs_host, coeffs_host, stream=None):
+        _check(lib().dsft_execute_host(self._h, f_host.data_ptr(), freqs_host.data_ptr(),
+                                       coeffs_host.data_ptr(), _stream_ptr(stream)))
+
+    def dsft_execute_sharded(self, comm, f, freqs_out, coeffs_out, stream=None):
+        _check(lib().dsft_execute_sharded(self._h, comm.handle, f.data_ptr(), freqs_out.data_ptr(),
+                                          coeffs_out.data_ptr(), _stream_ptr(stream)))
+
+    def dsft_debug_grid(self, f, band: int, t: int, i: int, what: int, out, stream=None):
+        _check(lib().dsft_debug_grid(self._h, f.data_ptr(), band, t, i, what, out.data_ptr(), _stream_ptr(stream)))
+
+    def dsft_debug_copy(self, which: int, dst, stream=None):
+        nbytes = dst.numel() * dst.element_size()
+        _check(lib().dsft_debug_copy(self._h, which, dst.data_ptr(), nbytes, _stream_ptr(stream)))
+
+    # convenience -------------------------------------------------------
+    def __call__(self, f, stream=None):
+        """Transform one device vector; returns (freqs[s] int64, coeffs[s] complex128) device tensors."""
+        import torch
+        freqs = torch.empty(self.s, dtype=torch.int64, device=f.device)
+        coeffs = torch.empty(self.s, dtype=torch.complex128, device=f.device)
+        self.dsft_execute(f, freqs, coeffs, stream)
+        return freqs, coeffs
+
+
+class Comm:
+    """NCCL communicator owned by libdsft (unique id broadcast by torch.distributed)."""
+
+    def __init__(self, rank: int, world: int, unique_id: bytes):
+        h = _P()
+        buf = C.create_string_buffer(bytes(unique_id), 128)
+        _check(lib().dsft_comm_create(rank, world, C.cast(buf, _P), C.byref(h)))
+        self._h = h
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        _check(lib().dsft_comm_get_unique_id(C.cast(buf, _P)))
+        return buf.raw
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().dsft_comm_destroy(self._h)
+            self._h = None
+
+    __del__ = close

@@ -1,0 +1,124 @@
+// internal.h -- plan layout and kernel launch interfaces of libdsft (not ABI).
+//
+// Data layout in HBM:
+//   f            caller's complex128 vector(s), read once per node window (K1)
+//   Z            per bucket prime t (reused across t, sized for max_t):
+//                [vec][band j][shift sigma][n1 < P_t] complex128
+//                K1 writes filtered samples, K2 turns each row into its
+//                length-P_t DFT in place (Good-Thomas column, Rader), K3 reads.
+//   cand_w       [vec][band][sum_t P_t] int64   omega' per bucket (or INT64_MIN)
+//   cand_v       [vec][band][sum_t P_t][Kmax] complex128, E_{t,i}[bin] of the
+//                residue argmax (written only for in-passband candidates)
+//   acc_w/acc_z  [vec][band][sum_t P_t] accepted omegas and their median z
+//   band_w/c/z   [vec][band][band_budget] line-9/11 output per band, band_n counts
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/dsft.h"
+
+namespace dsft {
+
+constexpr int kMaxShifts = 160;  // 1 + sum_i (r_i - 1) for up to 10 residue primes
+constexpr int kMaxFac = 24;      // FFT passes of P-1
+constexpr int kK1TabMax = 32 * 6 * 2;  // J <= 32 with kappa <= 6 in kernel params
+constexpr int64_t kSentinel = INT64_MIN;
+
+// Per-bucket-prime tables (host copy + device pointers into plan->dev_tables).
+struct Bucket {
+  int64_t P = 0;
+  int K = 0;                 // residue primes used with P (reading R8)
+  int r[DSFT_MAX_K] = {};
+  int S = 0;                 // shifts: sigma = 0 is the P-subgrid, then (i, n2>=1)
+  int shift_r[kMaxShifts] = {};
+  int shift_n2[kMaxShifts] = {};
+  int shift_base[DSFT_MAX_K] = {};  // sigma of (i, n2=1)
+  int64_t off = 0;           // sum_{t'<t} P_t'
+  int64_t crtM = 0;          // P * prod r
+  int64_t crtE[DSFT_MAX_K + 1] = {};  // CRT coefficients for moduli (P, r_0, ...)
+  // Rader / FFT of length M = P - 1
+  int M = 0;
+  int g = 0;                 // primitive root mod P
+  int nfac = 0;
+  int fac[kMaxFac] = {};
+  int fft_threads = 0;
+  // device pointers
+  int32_t* perm_in = nullptr;   // [M] g^q mod P
+  int32_t* perm_out = nullptr;  // [M] g^-p mod P
+  double2* bhat = nullptr;      // [M] FFT_M(b)/M, b_m = exp(-2 pi i g^-m / P)
+  double2* tw = nullptr;        // [M] exp(-2 pi i m / M)
+};
+
+struct Plan {
+  dsft_plan_info info{};
+  dsft_params params{};
+  int64_t N = 0, s = 0;
+  int kappa = 0, J = 0, T = 0;
+  int64_t w = 0, q1 = 0, halfN_up = 0, B_lo = 0, B_hi = 0;
+  double c1 = 0;
+  int Kmax = 0, Smax = 0;
+  int64_t sumP = 0, maxSP = 0;
+  Bucket bk[DSFT_MAX_T];
+  std::vector<double> k1tab;   // [J][kappa][2] cos/sin(q_j u 2pi/N), u = 1..kappa
+  std::vector<double> ctab;    // [kappa+1] exp(-u^2 h^2 / (2 c1^2)), h = 2 pi / N
+  double* k1tab_dev = nullptr;
+  void* dev_tables = nullptr;
+  // workspace
+  void* ws = nullptr;
+  size_t ws_bytes = 0;
+  bool ws_owned = false;
+  int64_t ws_batch = 0;        // vectors processed concurrently with this workspace
+  // device-side scratch for the host-buffer e2e path
+  void* io_dev = nullptr;
+  size_t io_bytes = 0;
+  // optional per-kernel CUDA-event timing (bench): event pairs recorded on the
+  // launching stream around every launch, reduced by dsft_plan_collect_times
+  bool timing = false;
+  std::vector<cudaEvent_t> ev_pool;
+  std::vector<int> ev_class;   // kernel class of pair i (0 K1, 1 K2, 2 K3, 3 K45, 4 K6)
+  size_t ev_used = 0;          // pairs recorded since the last collect
+};
+
+// Workspace regions (byte offsets, 256-aligned) for `nvec` concurrent vectors,
+// and the per-vector element strides the kernels use.
+struct WsLayout {
+  size_t z, cand_w, cand_v, acc_w, acc_z, band_w, band_c, band_z, band_n, total;
+  int64_t z_vec;     // complex128 elements per vector in Z:        J * max_t S_t P_t
+  int64_t cw_vec;    // elements per vector in cand_w / acc_w / acc_z: J * sum_t P_t
+  int64_t band_vec;  // elements per vector in band_w / band_c / band_z: J * budget
+  int64_t bn_vec;    // elements per vector in band_n: J
+};
+WsLayout ws_layout(const Plan& p, int64_t nvec);
+
+// ---- kernel launchers (kernels.cu); all stream-ordered, return cudaError_t
+cudaError_t launch_k1(const Plan& p, int t, const double2* f, int64_t ld, int nvec, void* ws,
+                      const int* band_list, int nbands, cudaStream_t st);
+cudaError_t launch_k2(const Plan& p, int t, int nvec, void* ws, const int* band_list, int nbands,
+                      cudaStream_t st);
+cudaError_t launch_k3(const Plan& p, int t, int nvec, void* ws, const int* band_list, int nbands,
+                      cudaStream_t st);
+cudaError_t launch_k45(const Plan& p, int nvec, void* ws, const int* band_list, int nbands,
+                       cudaStream_t st);
+cudaError_t launch_k6(const Plan& p, int nvec, void* ws, int64_t* freqs, double2* coeffs,
+                      cudaStream_t st);
+cudaError_t launch_debug_grid(const Plan& p, int t, int i, int band, int what, const void* ws,
+                              double2* out, cudaStream_t st);
+cudaError_t kernels_init();  // one-time attribute setup (dynamic smem limits)
+cudaError_t launch_k6_blocks(const int64_t* bw, const double2* bc, const int32_t* bn, int nblocks, int64_t budget,
+                             int64_t blk_vec, int64_t bn_vec, int64_t s, int nvec, int64_t* freqs, double2* coeffs,
+                             cudaStream_t st);
+
+}  // namespace dsft
+
+struct dsft_plan {
+  dsft::Plan p;
+};
+
+namespace dsft {
+// plan.cpp: K1..K45 for the bands j = rank (mod world) of vector 0; zeroes band counts first.
+dsft_status run_sharded_bands(dsft_plan* pl, const double2* f, int rank, int world, cudaStream_t st, int* nb_out);
+}  // namespace dsft

@@ -1,0 +1,751 @@
+// plan.cpp -- host side of libdsft: parameter derivation (Algorithm 1 lines 1-4,
+// PAPER.md:225-234; Lemma 3; Theorem 4 PAPER.md:496-511;
+// Section 5 presets PAPER.md:653; readings R1-R12 of DESIGN.md §3), bucket /
+// residue primes and their Rader + CRT tables, workspace, and the stream-ordered
+// execute sequence K1..K6.  Independent of oracle/ (shares no code with it).
+#include <cuda_runtime.h>
+#include <math.h>
+#include <string.h>
+
+#include <algorithm>
+#include <complex>
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+
+using namespace dsft;
+
+namespace {
+
+thread_local std::string g_err;
+
+dsft_status fail(dsft_status st, const std::string& msg) {
+  g_err = msg;
+  return st;
+}
+
+dsft_status cuda_fail(cudaError_t e, const char* what) {
+  g_err = std::string(what) + ": " + cudaGetErrorString(e);
+  return DSFT_ERR_CUDA;
+}
+
+#define CU(call, what)                                 \
+  do {                                                 \
+    cudaError_t e_ = (call);                           \
+    if (e_ != cudaSuccess) return cuda_fail(e_, what); \
+  } while (0)
+
+// ---------------------------------------------------------------- integers
+std::vector<int64_t> primes_below(int64_t hi) {
+  std::vector<char> sv(std::max<int64_t>(hi, 2), 1);
+  sv[0] = sv[1] = 0;
+  for (int64_t i = 2; i * i < hi; ++i)
+    if (sv[i])
+      for (int64_t j = i * i; j < hi; j += i) sv[j] = 0;
+  std::vector<int64_t> out;
+  for (int64_t i = 2; i < hi; ++i)
+    if (sv[i]) out.push_back(i);
+  return out;
+}
+
+int64_t largest_prime_factor(int64_t n) {
+  int64_t best = 1;
+  for (int64_t d = 2; d * d <= n; ++d)
+    while (n % d == 0) {
+      best = d;
+      n /= d;
+    }
+  return n > 1 ? std::max(best, n) : best;
+}
+
+std::vector<int64_t> prime_factors(int64_t n) {
+  std::vector<int64_t> f;
+  for (int64_t d = 2; d * d <= n; ++d)
+    if (n % d == 0) {
+      f.push_back(d);
+      while (n % d == 0) n /= d;
+    }
+  if (n > 1) f.push_back(n);
+  return f;
+}
+
+int64_t powmod(int64_t b, int64_t e, int64_t m) {
+  __int128 r = 1, x = b % m;
+  while (e > 0) {
+    if (e & 1) r = (r * x) % m;
+    x = (x * x) % m;
+    e >>= 1;
+  }
+  return (int64_t)r;
+}
+
+int64_t invmod(int64_t a, int64_t m) {  // extended Euclid, gcd(a, m) = 1
+  int64_t g = m, x = 0, x1 = 1, a1 = ((a % m) + m) % m;
+  while (a1) {
+    int64_t q = g / a1;
+    int64_t t = g - q * a1;
+    g = a1;
+    a1 = t;
+    t = x - q * x1;
+    x = x1;
+    x1 = t;
+  }
+  return ((x % m) + m) % m;
+}
+
+struct SplitMix64 {  // reading R7: same counter-based generator as the oracle
+  uint64_t s;
+  uint64_t next() {
+    s += 0x9E3779B97F4A7C15ull;
+    uint64_t z = s;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+  }
+};
+
+// ------------------------------------------------------- host FFT (long double)
+using cld = std::complex<long double>;
+const long double kPiL = 3.141592653589793238462643383279502884L;
+
+cld unit_root(int64_t e, int64_t n) {  // exp(-2 pi i e / n), exact reduction of e
+  e %= n;
+  if (e < 0) e += n;
+  const long double a = -2.0L * kPiL * (long double)e / (long double)n;
+  return cld(cosl(a), sinl(a));
+}
+
+void fft_rec(const cld* x, cld* y, int64_t n, int64_t stride) {
+  if (n == 1) {
+    y[0] = x[0];
+    return;
+  }
+  int64_t p = 2;
+  while (n % p) ++p;
+  const int64_t m = n / p;
+  std::vector<cld> sub(n);
+  for (int64_t r = 0; r < p; ++r) fft_rec(x + r * stride, sub.data() + r * m, m, stride * p);
+  for (int64_t k = 0; k < n; ++k) {
+    cld acc = 0;
+    for (int64_t r = 0; r < p; ++r) acc += sub[r * m + k % m] * unit_root(r * k, n);
+    y[k] = acc;
+  }
+}
+
+size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+}  // namespace
+
+// ======================================================================= layout
+namespace dsft {
+
+WsLayout ws_layout(const Plan& p, int64_t nvec) {
+  WsLayout L{};
+  L.z_vec = (int64_t)p.J * p.maxSP;
+  L.cw_vec = (int64_t)p.J * p.sumP;
+  L.band_vec = (int64_t)p.J * p.info.band_budget;
+  L.bn_vec = p.J;
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    size_t at = o;
+    o = align256(o + bytes);
+    return at;
+  };
+  L.z = take((size_t)nvec * L.z_vec * 16);
+  L.cand_w = take((size_t)nvec * L.cw_vec * 8);
+  L.cand_v = take((size_t)nvec * L.cw_vec * p.Kmax * 16);
+  L.acc_w = take((size_t)nvec * L.cw_vec * 8);
+  L.acc_z = take((size_t)nvec * L.cw_vec * 16);
+  L.band_w = take((size_t)nvec * L.band_vec * 8);
+  L.band_c = take((size_t)nvec * L.band_vec * 16);
+  L.band_z = take((size_t)nvec * L.band_vec * 16);
+  L.band_n = take((size_t)nvec * L.bn_vec * 4);
+  L.total = o;
+  return L;
+}
+
+}  // namespace dsft
+
+// =================================================================== derivation
+static dsft_status derive(int64_t N, int64_t s, const dsft_params& prm, Plan& P) {
+  if (N < 36) return fail(DSFT_ERR_CONFIG, "N must be >= 36 (PAPER.md:498)");
+  if (s < 2 || s > N) return fail(DSFT_ERR_CONFIG, "s must lie in [2, N] (PAPER.md:40)");
+  if (!(prm.tau > 0.0 && prm.tau < 1.0 / sqrt(2.0 * M_PI)))
+    return fail(DSFT_ERR_CONFIG, "tau must lie in (0, 1/sqrt(2 pi)) (Lemma 3)");
+  const double lnN = log((double)N);
+  double beta;
+  int kappa;
+  if (prm.preset == DSFT_PRESET_THM4) {
+    if (!(prm.r >= 1.0 && prm.r <= (double)N / 36.0)) return fail(DSFT_ERR_CONFIG, "r must lie in [1, N/36]");
+    beta = 6.0 * sqrt(prm.r);
+    kappa = (int)ceil(6.0 * prm.r * lnN / (sqrt(2.0) * M_PI)) + 1;  // Theorem 4
+  } else if (prm.preset == DSFT_PRESET_DMSFT6 || prm.preset == DSFT_PRESET_DMSFT4) {
+    kappa = prm.preset == DSFT_PRESET_DMSFT6 ? 6 : 4;
+    beta = -1.0;
+  } else {
+    return fail(DSFT_ERR_CONFIG, "unknown preset");
+  }
+  if (prm.kappa > 0) kappa = prm.kappa;
+  if (beta < 0) beta = sqrt(4.0 * M_PI * kappa / lnN);  // reading R4
+  if (2 * (int64_t)kappa + 2 > N) return fail(DSFT_ERR_CONFIG, "2 kappa + 2 > N");
+  if (kappa > 31) return fail(DSFT_ERR_UNSUPPORTED, "kappa > 31 not supported by K1");
+  const double c1 = beta * sqrt(lnN) / (double)N;  // Algorithm 1 line 2
+  if (!(c1 < 0.5)) return fail(DSFT_ERR_CONFIG, "c1 >= 0.5 (reading R5)");
+  const double lg = log(1.0 / (prm.tau * sqrt(2.0 * M_PI)));
+  double alpha;
+  if (prm.alpha_rule == DSFT_ALPHA_CORRECTED) alpha = beta / sqrt(lg / 2.0);
+  else if (prm.alpha_rule == DSFT_ALPHA_LITERAL) alpha = beta * sqrt(2.0) / lg;
+  else return fail(DSFT_ERR_CONFIG, "unknown alpha_rule");
+  alpha = std::min(std::max(alpha, 1.0), (double)N / sqrt(lnN));
+  const int64_t w = (int64_t)ceil((double)N / (alpha * sqrt(lnN)));
+  const int64_t J = (int64_t)ceil(alpha * sqrt(lnN) / 2.0);          // ceil(c2)
+  if (J > DSFT_MAX_J) return fail(DSFT_ERR_UNSUPPORTED, "more than DSFT_MAX_J passbands");
+  const int64_t halfN_up = (N + 1) / 2;
+  const int T = prm.n_bucket_primes;
+  if (T < 1) return fail(DSFT_ERR_CONFIG, "need at least one bucket prime");
+  if (T > DSFT_MAX_T) return fail(DSFT_ERR_UNSUPPORTED, "T > DSFT_MAX_T");
+  // bucket-prime pool (reading R6)
+  const int64_t lo = (int64_t)ceil(prm.bucket_factor * (double)s);
+  const int64_t hi = 2 * lo;
+  std::vector<int64_t> pool;
+  for (int64_t pr : primes_below(hi))
+    if (pr >= lo && largest_prime_factor(pr - 1) <= 13) pool.push_back(pr);
+  if ((int64_t)pool.size() < T) return fail(DSFT_ERR_CONFIG, "bucket-prime pool smaller than T");
+  // draw T distinct by partial Fisher-Yates with SplitMix64 (reading R7)
+  SplitMix64 rng{prm.seed};
+  std::vector<int64_t> work = pool;
+  const uint64_t n = work.size();
+  for (int i = 0; i < T; ++i) {
+    const uint64_t j = (uint64_t)i + rng.next() % (n - (uint64_t)i);
+    std::swap(work[i], work[j]);
+  }
+  std::vector<int64_t> primes(work.begin(), work.begin() + T);
+  std::sort(primes.begin(), primes.end());
+  if (prm.vote_min < 1 || prm.vote_min > T) return fail(DSFT_ERR_CONFIG, "vote_min must lie in [1, T]");
+
+  std::vector<int64_t> odd;
+  for (int64_t pr : primes_below(512))
+    if (pr > 2) odd.push_back(pr);
+
+  P.params = prm;
+  P.N = N;
+  P.s = s;
+  P.kappa = kappa;
+  P.J = (int)J;
+  P.T = T;
+  P.w = w;
+  P.halfN_up = halfN_up;
+  P.q1 = -halfN_up + 1 + w;
+  P.B_lo = -halfN_up + 1;
+  P.B_hi = N / 2;
+  P.c1 = c1;
+  P.Kmax = 0;
+  P.Smax = 0;
+  P.sumP = 0;
+  P.maxSP = 0;
+  int64_t grid_points = 0, nodes = 0;
+  for (int t = 0; t < T; ++t) {
+    Bucket& b = P.bk[t];
+    b.P = primes[t];
+    // residue primes: smallest consecutive odd primes with P prod r >= N, at least one (R8)
+    int K = 0;
+    __int128 prod = b.P;
+    while (prod < N || K == 0) {
+      if (K >= DSFT_MAX_K) return fail(DSFT_ERR_UNSUPPORTED, "more than DSFT_MAX_K residue primes");
+      b.r[K] = (int)odd[K];
+      prod *= odd[K];
+      ++K;
+    }
+    b.K = K;
+    if (b.r[K - 1] >= b.P) return fail(DSFT_ERR_CONFIG, "residue primes must be smaller than the bucket primes");
+    if (b.r[K - 1] > 31) return fail(DSFT_ERR_UNSUPPORTED, "residue prime > 31");
+    // shifts: sigma 0 = P-subgrid (n2 = 0 of every residue grid), then (i, n2 >= 1)
+    int S = 1;
+    b.shift_r[0] = 1;
+    b.shift_n2[0] = 0;
+    for (int i = 0; i < K; ++i) {
+      b.shift_base[i] = S;
+      for (int n2 = 1; n2 < b.r[i]; ++n2) {
+        if (S >= kMaxShifts) return fail(DSFT_ERR_UNSUPPORTED, "too many shifts");
+        b.shift_r[S] = b.r[i];
+        b.shift_n2[S] = n2;
+        ++S;
+      }
+      grid_points += b.P * b.r[i];
+    }
+    b.S = S;
+    nodes += (int64_t)S * b.P;
+    // CRT coefficients e_m = (M/m) ((M/m)^-1 mod m) for moduli (P, r_0, ..., r_{K-1})
+    int64_t M = b.P;
+    for (int i = 0; i < K; ++i) M *= b.r[i];
+    b.crtM = M;
+    {
+      const int64_t Mi = M / b.P;
+      b.crtE[0] = (int64_t)(((__int128)Mi * invmod(Mi % b.P, b.P)) % M);
+      for (int i = 0; i < K; ++i) {
+        const int64_t Mr = M / b.r[i];
+        b.crtE[i + 1] = (int64_t)(((__int128)Mr * invmod(Mr % b.r[i], b.r[i])) % M);
+      }
+    }
+    b.off = P.sumP;
+    P.sumP += b.P;
+    P.maxSP = std::max<int64_t>(P.maxSP, (int64_t)S * b.P);
+    P.Kmax = std::max(P.Kmax, K);
+    P.Smax = std::max(P.Smax, S);
+    // Rader setup: M = P - 1, primitive root g
+    b.M = (int)(b.P - 1);
+    if ((size_t)b.M * 16 > 226 * 1024)
+      return fail(DSFT_ERR_UNSUPPORTED, "bucket prime above 14465 needs the multi-CTA DFT (not built yet)");
+    const auto pf = prime_factors(b.M);
+    int g = 2;
+    for (;; ++g) {
+      bool ok = true;
+      for (int64_t qf : pf)
+        if (powmod(g, b.M / qf, b.P) == 1) {
+          ok = false;
+          break;
+        }
+      if (ok) break;
+    }
+    b.g = g;
+    int m = b.M, nf = 0;
+    while (m % 8 == 0) b.fac[nf++] = 8, m /= 8;
+    while (m % 4 == 0) b.fac[nf++] = 4, m /= 4;
+    while (m % 2 == 0) b.fac[nf++] = 2, m /= 2;
+    for (int rdx : {13, 11, 7, 5, 3})
+      while (m % rdx == 0) b.fac[nf++] = rdx, m /= rdx;
+    if (m != 1) return fail(DSFT_ERR_INTERNAL, "P-1 not 13-smooth");
+    b.nfac = nf;
+    int nt = 64;
+    while (nt < 512 && b.M > 16 * nt) nt *= 2;
+    b.fft_threads = nt;
+  }
+  // K1 tables: cos/sin(q_j u h), h = 2 pi / N, angles reduced exactly mod N
+  P.k1tab.assign((size_t)J * kappa * 2, 0.0);
+  for (int64_t j = 0; j < J; ++j) {
+    const int64_t q = P.q1 + 2 * w * j;
+    for (int u = 1; u <= kappa; ++u) {
+      int64_t e = (int64_t)(((__int128)q * u) % N);
+      if (e < 0) e += N;
+      const long double a = 2.0L * kPiL * (long double)e / (long double)N;
+      P.k1tab[((size_t)j * kappa + (u - 1)) * 2 + 0] = (double)cosl(a);
+      P.k1tab[((size_t)j * kappa + (u - 1)) * 2 + 1] = (double)sinl(a);
+    }
+  }
+  P.ctab.assign(kappa + 1, 0.0);
+  const long double h = 2.0L * kPiL / (long double)N;
+  for (int u = 0; u <= kappa; ++u)
+    P.ctab[u] = (double)expl(-(long double)u * u * h * h / (2.0L * (long double)c1 * (long double)c1));
+
+  dsft_plan_info& I = P.info;
+  memset(&I, 0, sizeof(I));
+  I.N = N;
+  I.s = s;
+  I.preset = prm.preset;
+  I.kappa = kappa;
+  I.J = (int32_t)J;
+  I.T = T;
+  I.w = w;
+  I.beta = beta;
+  I.c1 = c1;
+  I.alpha = alpha;
+  I.tau = prm.tau;
+  I.q1 = P.q1;
+  I.vote_min = prm.vote_min;
+  I.band_budget = prm.band_budget > 0 ? prm.band_budget : s;
+  for (int t = 0; t < T; ++t) {
+    I.primes[t] = P.bk[t].P;
+    I.n_residues[t] = P.bk[t].K;
+    for (int i = 0; i < P.bk[t].K; ++i) I.residues[t][i] = P.bk[t].r[i];
+    I.n_shifts[t] = P.bk[t].S;
+  }
+  I.nodes = nodes;
+  I.grid_points = grid_points;
+  I.sum_primes = P.sumP;
+  return DSFT_OK;
+}
+
+static dsft_status upload_tables(Plan& P) {
+  // one allocation: per t [perm_in M][perm_out M] int32, [bhat M][tw M] double2; then k1tab, ctab
+  size_t bytes = 0;
+  std::vector<size_t> offs(P.T);
+  for (int t = 0; t < P.T; ++t) {
+    offs[t] = bytes;
+    bytes = align256(bytes + (size_t)P.bk[t].M * (4 + 4 + 16 + 16) + 16);
+  }
+  const size_t k1off = bytes;
+  bytes = align256(bytes + (P.k1tab.size() + P.ctab.size()) * 8);
+  std::vector<char> host(bytes, 0);
+  for (int t = 0; t < P.T; ++t) {
+    Bucket& b = P.bk[t];
+    const int M = b.M;
+    int32_t* pin = (int32_t*)(host.data() + offs[t]);
+    int32_t* pout = pin + M;
+    // lay out: pin [M] int32, pout [M] int32, then (aligned to 16) bhat [M], tw [M]
+    const size_t cpx_off = offs[t] + (((size_t)M * 8 + 15) & ~(size_t)15);
+    double* bhat = (double*)(host.data() + cpx_off);
+    double* tw = bhat + 2 * (size_t)M;
+    const int64_t ginv = invmod(b.g, b.P);
+    int64_t gp = 1, gn = 1;
+    std::vector<cld> bseq(M), bf(M);
+    for (int q = 0; q < M; ++q) {
+      pin[q] = (int32_t)gp;   // g^q
+      pout[q] = (int32_t)gn;  // g^-q
+      bseq[q] = unit_root(gn, b.P);  // b_m = W_P^{g^-m}
+      gp = gp * b.g % b.P;
+      gn = gn * ginv % b.P;
+    }
+    fft_rec(bseq.data(), bf.data(), M, 1);
+    for (int c = 0; c < M; ++c) {
+      // DIF output position of frequency c: pos = sum_s d_s M/(R_1..R_s), c = d_1 + R_1(d_2 + ...)
+      int64_t cc = c, pos = 0, span = M;
+      for (int i = 0; i < b.nfac; ++i) {
+        const int64_t d = cc % b.fac[i];
+        cc /= b.fac[i];
+        span /= b.fac[i];
+        pos += d * span;
+      }
+      bhat[2 * pos] = (double)(bf[c].real() / (long double)M);
+      bhat[2 * pos + 1] = (double)(bf[c].imag() / (long double)M);
+    }
+    for (int k = 0; k < M; ++k) {
+      const cld wv = unit_root(k, M);
+      tw[2 * k] = (double)wv.real();
+      tw[2 * k + 1] = (double)wv.imag();
+    }
+  }
+  memcpy(host.data() + k1off, P.k1tab.data(), P.k1tab.size() * 8);
+  memcpy(host.data() + k1off + P.k1tab.size() * 8, P.ctab.data(), P.ctab.size() * 8);
+  CU(cudaMalloc(&P.dev_tables, bytes), "cudaMalloc(plan tables)");
+  CU(cudaMemcpy(P.dev_tables, host.data(), bytes, cudaMemcpyHostToDevice), "upload plan tables");
+  for (int t = 0; t < P.T; ++t) {
+    Bucket& b = P.bk[t];
+    char* base = (char*)P.dev_tables;
+    b.perm_in = (int32_t*)(base + offs[t]);
+    b.perm_out = b.perm_in + b.M;
+    const size_t cpx_off = offs[t] + (((size_t)b.M * 8 + 15) & ~(size_t)15);
+    b.bhat = (double2*)(base + cpx_off);
+    b.tw = b.bhat + b.M;
+  }
+  P.k1tab_dev = (double*)((char*)P.dev_tables + k1off);
+  return DSFT_OK;
+}
+
+// =============================================================== ABI: basics
+extern "C" {
+
+void dsft_params_default(dsft_params* p) {
+  if (!p) return;
+  memset(p, 0, sizeof(*p));
+  p->preset = DSFT_PRESET_DMSFT6;
+  p->r = 1.0;
+  p->kappa = 0;
+  p->tau = 1.0 / 3.0;
+  p->alpha_rule = DSFT_ALPHA_CORRECTED;
+  p->bucket_factor = 4.0;
+  p->n_bucket_primes = 5;
+  p->vote_min = 3;
+  p->band_budget = 0;
+  p->seed = 0;
+}
+
+const char* dsft_status_string(dsft_status st) {
+  switch (st) {
+    case DSFT_OK: return "ok";
+    case DSFT_ERR_CONFIG: return "invalid configuration";
+    case DSFT_ERR_ARG: return "invalid argument";
+    case DSFT_ERR_CUDA: return "CUDA error";
+    case DSFT_ERR_NCCL: return "NCCL error";
+    case DSFT_ERR_NOMEM: return "out of memory";
+    case DSFT_ERR_INTERNAL: return "internal error";
+    case DSFT_ERR_UNSUPPORTED: return "unsupported configuration";
+  }
+  return "unknown status";
+}
+
+const char* dsft_last_error(void) { return g_err.c_str(); }
+
+const char* dsft_version(void) { return "dsft-b200 0.1 (sm_100a)"; }
+
+dsft_status dsft_plan_create(int64_t N, int64_t s, const dsft_params* params, dsft_plan** out) {
+  if (!out) return fail(DSFT_ERR_ARG, "out is NULL");
+  dsft_params prm;
+  if (params) prm = *params;
+  else dsft_params_default(&prm);
+  dsft_plan* pl = new dsft_plan();
+  dsft_status st = derive(N, s, prm, pl->p);
+  if (st != DSFT_OK) {
+    delete pl;
+    return st;
+  }
+  cudaError_t e = kernels_init();
+  if (e != cudaSuccess) {
+    delete pl;
+    return cuda_fail(e, "kernels_init");
+  }
+  st = upload_tables(pl->p);
+  if (st != DSFT_OK) {
+    if (pl->p.dev_tables) cudaFree(pl->p.dev_tables);
+    delete pl;
+    return st;
+  }
+  *out = pl;
+  return DSFT_OK;
+}
+
+void dsft_plan_destroy(dsft_plan* pl) {
+  if (!pl) return;
+  for (cudaEvent_t e : pl->p.ev_pool) cudaEventDestroy(e);
+  if (pl->p.dev_tables) cudaFree(pl->p.dev_tables);
+  if (pl->p.ws_owned && pl->p.ws) cudaFree(pl->p.ws);
+  if (pl->p.io_dev) cudaFree(pl->p.io_dev);
+  delete pl;
+}
+
+dsft_status dsft_plan_derive_info(int64_t N, int64_t s, const dsft_params* params, dsft_plan_info* info) {
+  if (!info) return fail(DSFT_ERR_ARG, "info is NULL");
+  dsft_params prm;
+  if (params) prm = *params;
+  else dsft_params_default(&prm);
+  Plan* P = new Plan();
+  dsft_status st = derive(N, s, prm, *P);
+  if (st == DSFT_OK) *info = P->info;
+  delete P;
+  return st;
+}
+
+void dsft_shard_bands(int32_t J, int32_t rank, int32_t world, int32_t* bands_out, int32_t* nbands_out) {
+  int32_t n = 0;
+  if (world >= 1 && rank >= 0 && rank < world)
+    for (int32_t j = rank; j < J; j += world) {
+      if (bands_out) bands_out[n] = j;
+      ++n;
+    }
+  if (nbands_out) *nbands_out = n;
+}
+
+dsft_status dsft_plan_get_info(const dsft_plan* pl, dsft_plan_info* info) {
+  if (!pl || !info) return fail(DSFT_ERR_ARG, "NULL argument");
+  *info = pl->p.info;
+  return DSFT_OK;
+}
+
+static int64_t choose_wave(const Plan& p, int64_t batch) {
+  // vectors per wave: keep the Z working set near L2 size (126 MB) when several fit
+  const double zbytes = (double)p.J * p.maxSP * 16.0;
+  int64_t vb = (int64_t)(64.0e6 / std::max(zbytes, 1.0));
+  vb = std::max<int64_t>(1, std::min<int64_t>(vb, 64));
+  return std::min<int64_t>(vb, std::max<int64_t>(batch, 1));
+}
+
+size_t dsft_plan_workspace_bytes(const dsft_plan* pl, int64_t batch) {
+  if (!pl) return 0;
+  return ws_layout(pl->p, choose_wave(pl->p, batch)).total;
+}
+
+dsft_status dsft_plan_set_workspace(dsft_plan* pl, void* dev, size_t bytes) {
+  if (!pl) return fail(DSFT_ERR_ARG, "plan is NULL");
+  if (!dev || ((uintptr_t)dev & 255)) return fail(DSFT_ERR_ARG, "workspace must be non-NULL and 256-B aligned");
+  Plan& p = pl->p;
+  int64_t nv = 0;
+  while (nv < 64 && ws_layout(p, nv + 1).total <= bytes) ++nv;
+  if (nv == 0) return fail(DSFT_ERR_ARG, "workspace smaller than dsft_plan_workspace_bytes(plan, 1)");
+  if (p.ws_owned && p.ws) cudaFree(p.ws);
+  p.ws = dev;
+  p.ws_bytes = bytes;
+  p.ws_owned = false;
+  p.ws_batch = nv;
+  return DSFT_OK;
+}
+
+static dsft_status ensure_ws(Plan& p, int64_t want) {
+  if (p.ws && !p.ws_owned) return DSFT_OK;  // borrowed: process in waves of ws_batch
+  if (p.ws && p.ws_batch >= want) return DSFT_OK;
+  if (p.ws) {
+    cudaFree(p.ws);
+    p.ws = nullptr;
+  }
+  const size_t bytes = ws_layout(p, want).total;
+  cudaError_t e = cudaMalloc(&p.ws, bytes);
+  if (e != cudaSuccess) {
+    p.ws = nullptr;
+    return fail(DSFT_ERR_NOMEM, std::string("workspace cudaMalloc: ") + cudaGetErrorString(e));
+  }
+  p.ws_bytes = bytes;
+  p.ws_owned = true;
+  p.ws_batch = want;
+  return DSFT_OK;
+}
+
+// Per-kernel timing: record an event pair around a launch when enabled.
+extern "C++" template <class F>
+inline cudaError_t timed(Plan& p, int cls, cudaStream_t st, F&& launch) {
+  if (!p.timing) return launch();
+  if (p.ev_used + 1 > p.ev_pool.size() / 2) {
+    for (int k = 0; k < 64; ++k) {
+      cudaEvent_t e;
+      cudaError_t r = cudaEventCreate(&e);
+      if (r != cudaSuccess) return r;
+      p.ev_pool.push_back(e);
+    }
+    p.ev_class.resize(p.ev_pool.size() / 2);
+  }
+  const size_t i = p.ev_used++;
+  p.ev_class[i] = cls;
+  cudaError_t r = cudaEventRecord(p.ev_pool[2 * i], st);
+  if (r != cudaSuccess) return r;
+  r = launch();
+  if (r != cudaSuccess) return r;
+  return cudaEventRecord(p.ev_pool[2 * i + 1], st);
+}
+
+// The stream-ordered pipeline for `nv` vectors (<= ws_batch) and a band list.
+static dsft_status run_bands(Plan& p, const double2* f, int64_t ld, int nv, const int* bands, int nb,
+                             cudaStream_t st) {
+  for (int t = 0; t < p.T; ++t) {
+    CU(timed(p, 0, st, [&] { return launch_k1(p, t, f, ld, nv, p.ws, bands, nb, st); }), "K1 gather_mix launch");
+    CU(timed(p, 1, st, [&] { return launch_k2(p, t, nv, p.ws, bands, nb, st); }), "K2 prime_dft launch");
+    CU(timed(p, 2, st, [&] { return launch_k3(p, t, nv, p.ws, bands, nb, st); }), "K3 identify launch");
+  }
+  CU(timed(p, 3, st, [&] { return launch_k45(p, nv, p.ws, bands, nb, st); }), "K45 vote_estimate launch");
+  return DSFT_OK;
+}
+
+static dsft_status execute_impl(dsft_plan* pl, const dsft_c128* f, int64_t batch, int64_t ld, int64_t* freqs,
+                                dsft_c128* coeffs, void* stream) {
+  if (!pl) return fail(DSFT_ERR_ARG, "plan is NULL");
+  Plan& p = pl->p;
+  if (!f || !freqs || !coeffs) return fail(DSFT_ERR_ARG, "NULL device pointer");
+  if (((uintptr_t)f & 15) || ((uintptr_t)coeffs & 15) || ((uintptr_t)freqs & 7))
+    return fail(DSFT_ERR_ARG, "misaligned pointer (f/coeffs need 16 B, freqs 8 B)");
+  if (batch < 1 || ld < p.N) return fail(DSFT_ERR_ARG, "batch >= 1 and ld >= N required");
+  dsft_status stt = ensure_ws(p, choose_wave(p, batch));
+  if (stt != DSFT_OK) return stt;
+  cudaStream_t st = (cudaStream_t)stream;
+  std::vector<int> bands(p.J);
+  for (int j = 0; j < p.J; ++j) bands[j] = j;
+  for (int64_t v0 = 0; v0 < batch; v0 += p.ws_batch) {
+    const int nv = (int)std::min<int64_t>(p.ws_batch, batch - v0);
+    stt = run_bands(p, (const double2*)f + v0 * ld, ld, nv, bands.data(), p.J, st);
+    if (stt != DSFT_OK) return stt;
+    CU(timed(p, 4, st, [&] { return launch_k6(p, nv, p.ws, freqs + v0 * p.s, (double2*)coeffs + v0 * p.s, st); }),
+       "K6 merge launch");
+  }
+  return DSFT_OK;
+}
+
+dsft_status dsft_execute(dsft_plan* pl, const dsft_c128* f_dev, int64_t* freqs, dsft_c128* coeffs, void* stream) {
+  return execute_impl(pl, f_dev, 1, pl ? pl->p.N : 0, freqs, coeffs, stream);
+}
+
+dsft_status dsft_execute_batched(dsft_plan* pl, const dsft_c128* f_dev, int64_t batch, int64_t ld, int64_t* freqs,
+                                 dsft_c128* coeffs, void* stream) {
+  return execute_impl(pl, f_dev, batch, ld, freqs, coeffs, stream);
+}
+
+dsft_status dsft_execute_host(dsft_plan* pl, const dsft_c128* f_host, int64_t* freqs_host, dsft_c128* coeffs_host,
+                              void* stream) {
+  if (!pl || !f_host || !freqs_host || !coeffs_host) return fail(DSFT_ERR_ARG, "NULL argument");
+  Plan& p = pl->p;
+  const size_t fb = align256((size_t)p.N * 16), wb = align256((size_t)p.s * 8), cb = (size_t)p.s * 16;
+  if (!p.io_dev) {
+    CU(cudaMalloc(&p.io_dev, fb + wb + cb), "cudaMalloc(io)");
+    p.io_bytes = fb + wb + cb;
+  }
+  char* base = (char*)p.io_dev;
+  cudaStream_t st = (cudaStream_t)stream;
+  CU(cudaMemcpyAsync(base, f_host, (size_t)p.N * 16, cudaMemcpyHostToDevice, st), "H2D f");
+  dsft_status r = dsft_execute(pl, (const dsft_c128*)base, (int64_t*)(base + fb), (dsft_c128*)(base + fb + wb), stream);
+  if (r != DSFT_OK) return r;
+  CU(cudaMemcpyAsync(freqs_host, base + fb, (size_t)p.s * 8, cudaMemcpyDeviceToHost, st), "D2H freqs");
+  CU(cudaMemcpyAsync(coeffs_host, base + fb + wb, (size_t)p.s * 16, cudaMemcpyDeviceToHost, st), "D2H coeffs");
+  CU(cudaStreamSynchronize(st), "stream sync");
+  return DSFT_OK;
+}
+
+dsft_status dsft_plan_set_timing(dsft_plan* pl, int32_t enable) {
+  if (!pl) return fail(DSFT_ERR_ARG, "plan is NULL");
+  pl->p.timing = enable != 0;
+  pl->p.ev_used = 0;
+  return DSFT_OK;
+}
+
+dsft_status dsft_plan_collect_times(dsft_plan* pl, double* ms_out, int64_t* launches_out) {
+  if (!pl || !ms_out || !launches_out) return fail(DSFT_ERR_ARG, "NULL argument");
+  Plan& p = pl->p;
+  for (int c = 0; c < DSFT_KERNEL_CLASSES; ++c) {
+    ms_out[c] = 0.0;
+    launches_out[c] = 0;
+  }
+  for (size_t i = 0; i < p.ev_used; ++i) {
+    CU(cudaEventSynchronize(p.ev_pool[2 * i + 1]), "event sync");
+    float ms = 0.f;
+    CU(cudaEventElapsedTime(&ms, p.ev_pool[2 * i], p.ev_pool[2 * i + 1]), "event elapsed");
+    ms_out[p.ev_class[i]] += ms;
+    launches_out[p.ev_class[i]] += 1;
+  }
+  p.ev_used = 0;
+  return DSFT_OK;
+}
+
+int64_t dsft_plan_launches_per_execute(const dsft_plan* pl) {
+  if (!pl) return 0;
+  return 3 * (int64_t)pl->p.T + 2;
+}
+
+// -------------------------------------------------------------- parity hooks
+dsft_status dsft_debug_grid(dsft_plan* pl, const dsft_c128* f_dev, int32_t band, int32_t t, int32_t i, int32_t what,
+                            dsft_c128* out_dev, void* stream) {
+  if (!pl || !f_dev || !out_dev) return fail(DSFT_ERR_ARG, "NULL argument");
+  Plan& p = pl->p;
+  if (band < 0 || band >= p.J || t < 0 || t >= p.T || i < 0 || i >= p.bk[t].K || what < 0 || what > 1)
+    return fail(DSFT_ERR_ARG, "band/t/i/what out of range");
+  dsft_status stt = ensure_ws(p, 1);
+  if (stt != DSFT_OK) return stt;
+  cudaStream_t st = (cudaStream_t)stream;
+  int b = band;
+  CU(launch_k1(p, t, (const double2*)f_dev, p.N, 1, p.ws, &b, 1, st), "K1 launch");
+  if (what == 1) CU(launch_k2(p, t, 1, p.ws, &b, 1, st), "K2 launch");
+  CU(launch_debug_grid(p, t, i, 0, what, p.ws, (double2*)out_dev, st), "debug grid launch");
+  return DSFT_OK;
+}
+
+dsft_status dsft_debug_copy(dsft_plan* pl, int32_t which, void* dst, size_t bytes, void* stream) {
+  if (!pl || !dst) return fail(DSFT_ERR_ARG, "NULL argument");
+  Plan& p = pl->p;
+  if (!p.ws) return fail(DSFT_ERR_ARG, "no execute has run on this plan");
+  const WsLayout L = ws_layout(p, p.ws_batch);
+  size_t off, need;
+  switch (which) {
+    case 0: off = L.cand_w; need = (size_t)L.cw_vec * 8; break;
+    case 1: off = L.band_n; need = (size_t)L.bn_vec * 4; break;
+    case 2: off = L.band_w; need = (size_t)L.band_vec * 8; break;
+    case 3: off = L.band_c; need = (size_t)L.band_vec * 16; break;
+    case 4: off = L.band_z; need = (size_t)L.band_vec * 16; break;
+    default: return fail(DSFT_ERR_ARG, "unknown buffer");
+  }
+  if (bytes < need) return fail(DSFT_ERR_ARG, "destination too small");
+  CU(cudaMemcpyAsync(dst, (char*)p.ws + off, need, cudaMemcpyDeviceToDevice, (cudaStream_t)stream), "debug copy");
+  return DSFT_OK;
+}
+
+}  // extern "C"
+
+// ============================================================ sharded execution
+// (comm.cpp provides the NCCL handle; this part needs only the plan internals)
+namespace dsft {
+dsft_status run_sharded_bands(dsft_plan* pl, const double2* f, int rank, int world, cudaStream_t st, int* nb_out) {
+  Plan& p = pl->p;
+  std::vector<int> bands;
+  for (int j = rank; j < p.J; j += world) bands.push_back(j);
+  *nb_out = (int)bands.size();
+  dsft_status stt = ensure_ws(p, 1);
+  if (stt != DSFT_OK) return stt;
+  const WsLayout L = ws_layout(p, p.ws_batch);
+  CU(cudaMemsetAsync((char*)p.ws + L.band_n, 0, (size_t)L.bn_vec * 4, st), "zero band counts");
+  if (bands.empty()) return DSFT_OK;
+  return run_bands(p, f, p.N, 1, bands.data(), (int)bands.size(), st);
+}
+}  // namespace dsft

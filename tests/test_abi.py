@@ -1,0 +1,61 @@
+"""C-ABI checks that need no GPU: the library loads, exports every symbol the
+header declares, and its host-side plan derivation agrees exactly with the
+oracle's independent derivation (integers bit-exact, reals bitwise)."""
+
+import pytest
+
+import paper_1706_02740_b200 as d
+from oracle.params import ConfigError, OracleParams, derive_plan
+
+
+def test_library_exports_every_header_symbol():
+    L = d.lib()
+    names = d.header_functions()
+    assert len(names) >= 20
+    for n in names:
+        assert hasattr(L, n), n
+    assert b"sm_100a" in L.dsft_version()
+
+
+CASES = [(4096, 8, 0), (4096, 8, 5), (64, 4, 1), (97, 4, 2), (255, 6, 3), (2**16, 50, 4), (2**22, 50, 3),
+         (2**26, 1000, 1), (2**26, 500, 9), (2**26, 1500, 4), (6000011, 100, 7), (2**24, 256, 2)]
+
+
+@pytest.mark.parametrize("N,s,seed", CASES)
+@pytest.mark.parametrize("preset", ["dmsft6", "dmsft4", "thm4"])
+def test_plan_matches_oracle(N, s, seed, preset):
+    info = d.dsft_plan_derive_info(N, s, d.make_params(preset=preset, seed=seed))
+    p = derive_plan(N, s, OracleParams(preset=preset, seed=seed))
+    assert list(info.primes[:info.T]) == p.primes
+    assert [list(info.residues[t][:info.n_residues[t]]) for t in range(info.T)] == p.residues
+    assert (info.w, info.J, info.q1, info.kappa, info.band_budget) == (p.w, p.J, p.q[0], p.kappa, p.band_budget)
+    assert info.c1 == p.c1 and info.alpha == p.alpha and info.beta == p.beta
+    assert info.sum_primes == sum(p.primes)
+    assert info.grid_points == sum(P * r for P, rs in zip(p.primes, p.residues) for r in rs)
+    assert info.nodes == sum(P * (1 + sum(r - 1 for r in rs)) for P, rs in zip(p.primes, p.residues))
+
+
+def test_literal_alpha_and_kappa_override_match():
+    for kw in (dict(alpha_rule="literal"), dict(kappa=5), dict(tau=0.1), dict(bucket_factor=5.0, n_bucket_primes=7, vote_min=4)):
+        info = d.dsft_plan_derive_info(2**20, 100, d.make_params(**kw))
+        p = derive_plan(2**20, 100, OracleParams(**kw))
+        assert (info.w, info.J, info.kappa, list(info.primes[:info.T])) == (p.w, p.J, p.kappa, p.primes)
+
+
+@pytest.mark.parametrize("N,s,kw", [(30, 4, {}), (4096, 1, {}), (4096, 4097, {}), (4096, 8, dict(tau=0.5)),
+                                    (4096, 8, dict(preset="thm4", r=0.5)), (4096, 3, {}),
+                                    (4096, 8, dict(vote_min=6))])
+def test_config_errors_match_oracle(N, s, kw):
+    with pytest.raises(ConfigError):
+        derive_plan(N, s, OracleParams(**kw))
+    with pytest.raises(d.DsftError) as ei:
+        d.dsft_plan_derive_info(N, s, d.make_params(**kw))
+    assert ei.value.status == d.DSFT_ERR_CONFIG
+
+
+def test_shard_bands_partition():
+    for J in (1, 7, 15, 43):
+        for world in (1, 2, 3, 4, 8):
+            got = sorted(j for r in range(world) for j in d.dsft_shard_bands(J, r, world))
+            assert got == list(range(J))
+            assert all(j % world == r for r in range(world) for j in d.dsft_shard_bands(J, r, world))
