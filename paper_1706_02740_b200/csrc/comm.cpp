@@ -108,8 +108,11 @@ dsft_status dsft_execute_sharded(dsft_plan* pl, dsft_comm* c, const dsft_c128* f
   if (s != DSFT_OK) return s;
   const int nbmax = (p.J + c->world - 1) / c->world;
   const int64_t budget = p.info.band_budget;
-  const size_t wbytes = (size_t)nbmax * budget * 8, cbytes = (size_t)nbmax * budget * 16, nbytes = (size_t)nbmax * 4;
-  const size_t need = (wbytes + cbytes + nbytes) * c->world + 1024;
+  // per rank: the first nbmax band blocks (omega, c, key) and the non-zero counts
+  const size_t wb = (size_t)nbmax * budget * 8, cb = (size_t)nbmax * budget * 16, mb = (size_t)nbmax * budget * 8,
+               nbz = (size_t)nbmax * 4;
+  auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+  const size_t need = al(wb * c->world) + al(cb * c->world) + al(mb * c->world) + al(nbz * c->world);
   if (c->gbytes < need) {
     if (c->gbuf) cudaFree(c->gbuf);
     if (cudaMalloc(&c->gbuf, need) != cudaSuccess) {
@@ -122,17 +125,21 @@ dsft_status dsft_execute_sharded(dsft_plan* pl, dsft_comm* c, const dsft_c128* f
   const dsft::WsLayout L = dsft::ws_layout(p, p.ws_batch);
   char* ws = (char*)p.ws;
   char* gw = (char*)c->gbuf;
-  char* gc = gw + ((wbytes * c->world + 255) & ~(size_t)255);
-  char* gn = gc + ((cbytes * c->world + 255) & ~(size_t)255);
+  char* gc = gw + al(wb * c->world);
+  char* gm = gc + al(cb * c->world);
+  char* gz = gm + al(mb * c->world);
   g_nccl.GroupStart();
-  ncclResult_t r1 = g_nccl.AllGather(ws + L.band_w, gw, wbytes, ncclInt8, c->comm, st);
-  ncclResult_t r2 = g_nccl.AllGather(ws + L.band_c, gc, cbytes, ncclInt8, c->comm, st);
-  ncclResult_t r3 = g_nccl.AllGather(ws + L.band_n, gn, nbytes, ncclInt8, c->comm, st);
-  ncclResult_t r4 = g_nccl.GroupEnd();
-  if (r1 != ncclSuccess || r2 != ncclSuccess || r3 != ncclSuccess || r4 != ncclSuccess) return DSFT_ERR_NCCL;
-  // gathered layout: [world][nbmax][budget]; one "vector" of world*nbmax blocks
-  cudaError_t e = dsft::launch_k6_blocks((const int64_t*)gw, (const double2*)gc, (const int32_t*)gn,
-                                         c->world * nbmax, budget, 0, 0, p.s, 1, freqs, (double2*)coeffs, st);
+  ncclResult_t r1 = g_nccl.AllGather(ws + L.band_w, gw, wb, ncclInt8, c->comm, st);
+  ncclResult_t r2 = g_nccl.AllGather(ws + L.band_c, gc, cb, ncclInt8, c->comm, st);
+  ncclResult_t r3 = g_nccl.AllGather(ws + L.band_m, gm, mb, ncclInt8, c->comm, st);
+  ncclResult_t r4 = g_nccl.AllGather(ws + L.band_nz, gz, nbz, ncclInt8, c->comm, st);
+  ncclResult_t r5 = g_nccl.GroupEnd();
+  if (r1 != ncclSuccess || r2 != ncclSuccess || r3 != ncclSuccess || r4 != ncclSuccess || r5 != ncclSuccess)
+    return DSFT_ERR_NCCL;
+  // gathered layout: [world][nbmax][budget] -- one "vector" of world*nbmax sorted blocks
+  cudaError_t e = dsft::launch_k6_blocks((const int64_t*)gw, (const double2*)gc, (const double*)gm,
+                                         (const int32_t*)gz, c->world * nbmax, budget, 0, 0, p.s, 1, freqs,
+                                         (double2*)coeffs, st);
   return e == cudaSuccess ? DSFT_OK : DSFT_ERR_CUDA;
 }
 

@@ -9,8 +9,9 @@
 //   cand_w       [vec][band][sum_t P_t] int64   omega' per bucket (or INT64_MIN)
 //   cand_v       [vec][band][sum_t P_t][Kmax] complex128, E_{t,i}[bin] of the
 //                residue argmax (written only for in-passband candidates)
-//   acc_w/acc_z  [vec][band][sum_t P_t] accepted omegas and their median z
-//   band_w/c/z   [vec][band][band_budget] line-9/11 output per band, band_n counts
+//   acc_w/acc_z/acc_r [vec][band][sum_t P_t] accepted omegas, median z, |z| rank; acc_n [vec][band]
+//   band_w/c/z/m [vec][band][band_budget] line-9/11 output per band sorted by the
+//                merge key m = |c|^2 (-1 for exact zeros); band_n / band_nz counts
 #pragma once
 
 #include <cuda_runtime.h>
@@ -27,6 +28,7 @@ constexpr int kMaxShifts = 160;  // 1 + sum_i (r_i - 1) for up to 10 residue pri
 constexpr int kMaxFac = 24;      // FFT passes of P-1
 constexpr int kK1TabMax = 32 * 6 * 2;  // J <= 32 with kappa <= 6 in kernel params
 constexpr int64_t kSentinel = INT64_MIN;
+constexpr int kMaxRadix = 16;    // largest in-register FFT stage radix in K2
 
 // Per-bucket-prime tables (host copy + device pointers into plan->dev_tables).
 struct Bucket {
@@ -46,11 +48,12 @@ struct Bucket {
   int nfac = 0;
   int fac[kMaxFac] = {};
   int fft_threads = 0;
+  int nt1 = 0;                  // M/64 + 1 coarse twiddles
   // device pointers
-  int32_t* perm_in = nullptr;   // [M] g^q mod P
-  int32_t* perm_out = nullptr;  // [M] g^-p mod P
-  double2* bhat = nullptr;      // [M] FFT_M(b)/M, b_m = exp(-2 pi i g^-m / P)
-  double2* tw = nullptr;        // [M] exp(-2 pi i m / M)
+  uint16_t* dlog = nullptr;     // [P] discrete log base g (dlog[0] unused)
+  double2* bhat = nullptr;      // [M] FFT_M(b)/M in DIF output order, b_m = exp(-2 pi i g^-m / P)
+  double2* tw1 = nullptr;       // [nt1] exp(-2 pi i 64 e / M)
+  double2* tw2 = nullptr;       // [64]  exp(-2 pi i e / M)
 };
 
 struct Plan {
@@ -60,7 +63,7 @@ struct Plan {
   int kappa = 0, J = 0, T = 0;
   int64_t w = 0, q1 = 0, halfN_up = 0, B_lo = 0, B_hi = 0;
   double c1 = 0;
-  int Kmax = 0, Smax = 0;
+  int Kmax = 0, Smax = 0, Rmax = 0;  // Rmax: largest residue prime
   int64_t sumP = 0, maxSP = 0;
   Bucket bk[DSFT_MAX_T];
   std::vector<double> k1tab;   // [J][kappa][2] cos/sin(q_j u 2pi/N), u = 1..kappa
@@ -86,7 +89,8 @@ struct Plan {
 // Workspace regions (byte offsets, 256-aligned) for `nvec` concurrent vectors,
 // and the per-vector element strides the kernels use.
 struct WsLayout {
-  size_t z, cand_w, cand_v, acc_w, acc_z, band_w, band_c, band_z, band_n, total;
+  size_t z, cand_w, cand_v, acc_w, acc_z, acc_r, acc_mask, acc_n, work_n, work, band_w, band_c, band_z, band_m, band_n,
+      band_nz, total;
   int64_t z_vec;     // complex128 elements per vector in Z:        J * max_t S_t P_t
   int64_t cw_vec;    // elements per vector in cand_w / acc_w / acc_z: J * sum_t P_t
   int64_t band_vec;  // elements per vector in band_w / band_c / band_z: J * budget
@@ -108,9 +112,9 @@ cudaError_t launch_k6(const Plan& p, int nvec, void* ws, int64_t* freqs, double2
 cudaError_t launch_debug_grid(const Plan& p, int t, int i, int band, int what, const void* ws,
                               double2* out, cudaStream_t st);
 cudaError_t kernels_init();  // one-time attribute setup (dynamic smem limits)
-cudaError_t launch_k6_blocks(const int64_t* bw, const double2* bc, const int32_t* bn, int nblocks, int64_t budget,
-                             int64_t blk_vec, int64_t bn_vec, int64_t s, int nvec, int64_t* freqs, double2* coeffs,
-                             cudaStream_t st);
+cudaError_t launch_k6_blocks(const int64_t* bw, const double2* bc, const double* bm, const int32_t* bnz, int nblocks,
+                             int64_t budget, int64_t blk_vec, int64_t bn_vec, int64_t s, int nvec, int64_t* freqs,
+                             double2* coeffs, cudaStream_t st);
 
 }  // namespace dsft
 

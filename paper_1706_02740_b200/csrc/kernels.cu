@@ -18,6 +18,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
+
 #include "internal.h"
 #include "radix_consts.h"
 
@@ -36,6 +38,30 @@ __device__ __forceinline__ double2 cscale(double2 a, double s) { return make_dou
 __device__ __forceinline__ double cabs2_rn(double2 a) { return __dadd_rn(__dmul_rn(a.x, a.x), __dmul_rn(a.y, a.y)); }
 
 __device__ __forceinline__ double2 ldg2(const double2* p) { return __ldg(p); }
+
+// L2 eviction-priority policy (createpolicy) for Z, the per-prime working set
+// K1 -> K2 -> K3 keeps in L2 (evict_last); f windows bypass L1 allocation.
+// (An evict_first policy on f was measured to lose the L2 hits between
+// neighbouring windows: +30% DRAM reads, profiles/r1c.)
+__device__ __forceinline__ uint64_t l2_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ double2 ld_stream(const double2* ptr) {
+  double2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(ptr));
+  return v;
+}
+__device__ __forceinline__ void st_keep(double2* ptr, double2 v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(ptr), "d"(v.x), "d"(v.y), "l"(pol)
+               : "memory");
+}
 
 // ------------------------------------------------------------ in-register DFTs
 // Forward DFT (W = e^{-2 pi i / R}) of R values in registers.
@@ -83,8 +109,65 @@ __device__ __forceinline__ void dft4(double2& a, double2& b, double2& c, double2
 }
 
 template <int R>
+__device__ __forceinline__ void dft(double2 (&x)[R]);
+
+__host__ __device__ constexpr bool is_odd_prime(int r) {
+  if (r < 3 || r % 2 == 0) return false;
+  for (int d = 3; d * d <= r; d += 2)
+    if (r % d == 0) return false;
+  return true;
+}
+__host__ __device__ constexpr int first_factor(int r) {
+  if (r % 8 == 0) return 8;
+  if (r % 4 == 0) return 4;
+  if (r % 2 == 0) return 2;
+  for (int d = 3; d <= r; d += 2)
+    if (r % d == 0) return d;
+  return r;
+}
+
+// Composite R = A * B (Cooley-Tukey inside registers): n = B n1 + n2,
+// k = k1 + A k2; column DFTs of length A, twiddle W_R^{n2 k1}, row DFTs of
+// length B.  All indices are compile-time, so the arrays stay in registers and
+// the final transposition is a register renaming.
+template <int A, int B>
+__device__ __forceinline__ void dft_composite(double2 (&x)[A * B]) {
+  constexpr int R = A * B;
+#pragma unroll
+  for (int n2 = 0; n2 < B; ++n2) {
+    double2 col[A];
+#pragma unroll
+    for (int n1 = 0; n1 < A; ++n1) col[n1] = x[B * n1 + n2];
+    dft<A>(col);
+#pragma unroll
+    for (int k1 = 0; k1 < A; ++k1) {
+      const int e = (n2 * k1) % R;
+      double2 v = col[k1];
+      if (e != 0) {
+        const double c = RadixTab<R>::c(e), sn = RadixTab<R>::s(e);  // W_R^e = c - i sn
+        v = make_double2(fma(v.x, c, v.y * sn), fma(v.y, c, -v.x * sn));
+      }
+      x[B * k1 + n2] = v;
+    }
+  }
+  double2 out[R];
+#pragma unroll
+  for (int k1 = 0; k1 < A; ++k1) {
+    double2 row[B];
+#pragma unroll
+    for (int n2 = 0; n2 < B; ++n2) row[n2] = x[B * k1 + n2];
+    dft<B>(row);
+#pragma unroll
+    for (int k2 = 0; k2 < B; ++k2) out[k1 + A * k2] = row[k2];
+  }
+#pragma unroll
+  for (int i = 0; i < R; ++i) x[i] = out[i];
+}
+
+template <int R>
 __device__ __forceinline__ void dft(double2 (&x)[R]) {
-  if constexpr (R == 2) {
+  if constexpr (R == 1) {
+  } else if constexpr (R == 2) {
     const double2 a = x[0], b = x[1];
     x[0] = cadd(a, b);
     x[1] = csub(a, b);
@@ -107,8 +190,11 @@ __device__ __forceinline__ void dft(double2 (&x)[R]) {
     x[6] = csub(e2, t2);
     x[3] = cadd(e3, t3);
     x[7] = csub(e3, t3);
-  } else {
+  } else if constexpr (is_odd_prime(R)) {
     dft_odd<R>(x);
+  } else {
+    constexpr int A = first_factor(R);
+    dft_composite<A, R / A>(x);
   }
 }
 
@@ -134,6 +220,116 @@ struct K1Params {
   double ctab[8];
   double tab[kK1TabMax];     // [nb][kappa][2] cos/sin(q_j u 2 pi / N) (fast path)
 };
+
+// Node geometry shared by both K1 variants: node (sigma, n1) of bucket prime P
+// is x = -pi + 2 pi k / L, L = P r_sigma, k = (r n1 + P n2) mod L (Good's
+// mapping of the residue grid; sigma = 0 is the P-subgrid).
+struct NodeGeo {
+  int64_t jp;   // j' = round(kN/L)
+  double d0;    // x - y_j'
+};
+
+__device__ __forceinline__ NodeGeo node_geo(const K1Params& p, int sigma, int64_t n1) {
+  const int64_t r = p.shift_r[sigma];
+  const int64_t L = p.P * r;
+  int64_t k = r * n1 + p.P * (int64_t)p.shift_n2[sigma];
+  if (k >= L) k -= L;
+  // j' = round(kN / L): L is odd, so 2kN + L is never an exact multiple tie (R3).
+  const int64_t jp = (2 * k * p.N + L) / (2 * L);
+  const int64_t num0 = k * p.N - jp * L;  // (x - y_j') N L / (2 pi), exact
+  return NodeGeo{jp, (double)num0 * p.shift_scale[sigma]};
+}
+
+// Fast path (KAPPA in {4, 6}): each warp stages the 32 windows of its nodes in
+// shared memory with coalesced 16-lane loads (one 208-B window per half-warp
+// instruction instead of 32 scattered 16-B requests), then every lane runs the
+// band mix for its own node from shared memory.
+constexpr int kK1FastThreads = 128;
+
+template <int KAPPA>
+__global__ void __launch_bounds__(kK1FastThreads) k1_gather_mix_fast(const __grid_constant__ K1Params p) {
+  constexpr int W = 2 * KAPPA + 1;
+  __shared__ double2 s_win[kK1FastThreads / 32][32][W];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t nodes = (int64_t)p.S * p.P;
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool active = gid < nodes;
+  const int v = blockIdx.y;
+  const int sigma = active ? (int)(gid / p.P) : 0;
+  const int64_t n1 = active ? gid - (int64_t)sigma * p.P : 0;
+  const NodeGeo g = active ? node_geo(p, sigma, n1) : NodeGeo{0, 0.0};
+  const double2* fv = p.f + (int64_t)v * p.ld;
+  const int64_t N = p.N;
+  // ---- cooperative window loads: half-warp h of instruction i loads node 2i+h.
+  // All 16 loads are issued before the first shared store (16 in flight per lane).
+  {
+    const int h = lane >> 4, u = lane & 15;
+    double2 buf[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int m = 2 * i + h;
+      const int64_t jpm = __shfl_sync(0xffffffffu, g.jp, m);
+      const int64_t gm = __shfl_sync(0xffffffffu, gid, m);
+      if (u < W && gm < nodes) {
+        int64_t idx = jpm - KAPPA + u;
+        if (idx < 0) idx += N;
+        else if (idx >= N) idx -= N;
+        buf[i] = ld_stream(fv + idx);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int m = 2 * i + h;
+      if (u < W) s_win[warp][m][u] = buf[i];
+    }
+  }
+  __syncwarp();
+  if (!active) return;
+  double2 fw[W];
+#pragma unroll
+  for (int u = 0; u < W; ++u) fw[u] = s_win[warp][lane][u];
+
+  // Gaussian taps g(d_u)/N, d_u = d0 - u h, via G_u = G_0 E^u C_u (DESIGN.md §6 K1)
+  const double d0 = g.d0;
+  const double G0 = exp(d0 * d0 * p.neg_half_inv_c1sq) * p.inv_c1N;
+  const double E = exp(d0 * p.h_over_c1sq);
+  const double Ei = 1.0 / E;
+  const double2 P0 = cscale(fw[KAPPA], G0);
+  double2 A[KAPPA], D[KAPPA];
+  double ep = G0, em = G0;
+#pragma unroll
+  for (int u = 1; u <= KAPPA; ++u) {
+    ep *= E;
+    em *= Ei;
+    const double cu = p.ctab[u];
+    const double2 pp = cscale(fw[KAPPA + u], ep * cu);
+    const double2 pm = cscale(fw[KAPPA - u], em * cu);
+    A[u - 1] = cadd(pp, pm);
+    D[u - 1] = csub(pp, pm);
+  }
+  double sn, cs;
+  sincos(p.qfirst * d0, &sn, &cs);
+  double2 ph = make_double2(cs, sn);
+  sincos(p.qstep * d0, &sn, &cs);
+  const double2 step = make_double2(cs, sn);
+  const uint64_t pol_z = l2_evict_last();
+  double2* zo = p.Z + (int64_t)v * p.z_vec_stride + (int64_t)sigma * p.P + n1;
+  const int64_t band_stride = (int64_t)p.S * p.P;
+  for (int j = 0; j < p.nb; ++j) {
+    double re = P0.x, im = P0.y;
+    const double* tb = p.tab + j * KAPPA * 2;
+#pragma unroll
+    for (int u = 0; u < KAPPA; ++u) {
+      const double c = tb[2 * u], sgn = tb[2 * u + 1];
+      re = fma(A[u].x, c, re);
+      re = fma(D[u].y, sgn, re);
+      im = fma(A[u].y, c, im);
+      im = fma(-D[u].x, sgn, im);
+    }
+    st_keep(zo + j * band_stride, cmul(make_double2(re, im), ph), pol_z);
+    ph = cmul(ph, step);
+  }
+}
 
 // KAPPA > 0: compile-time window, table in kernel parameters (constant bank).
 // KAPPA == 0: runtime kappa (THM4 presets), tables in global memory.
@@ -229,13 +425,18 @@ __global__ void __launch_bounds__(256) k1_gather_mix(const __grid_constant__ K1P
 struct K2Params {
   double2* Z;
   int64_t z_vec_stride;
-  int P, M, nfac, pad_;
+  int P, M, nfac, nt1;
   int fac[kMaxFac];
-  const int32_t* perm_in;
-  const int32_t* perm_out;
-  const double2* bhat;  // FFT_M(b)/M stored in DIF output (digit-reversed) order
-  const double2* tw;
+  const uint16_t* dlog;  // [P]: dlog[n] = q with g^q = n (n >= 1)
+  const double2* bhat;   // FFT_M(b)/M stored in DIF output (digit-reversed) order
+  const double2* tw1;    // [nt1] W_M^{64 e1}
+  const double2* tw2;    // [64]  W_M^{e2}
 };
+
+// W_M^e from the two-level table in shared memory (e < M)
+__device__ __forceinline__ double2 tw_lookup(const double2* t1, const double2* t2, int e) {
+  return cmul(t1[e >> 6], t2[e & 63]);
+}
 
 // In-place mixed-radix FFT stages over s[0..M) (one butterfly's values live in
 // registers at a time).  DIF (span n shrinking) leaves the spectrum in digit-
@@ -244,7 +445,7 @@ struct K2Params {
 // convolution runs DIF -> pointwise (table pre-permuted) -> DIT, so no explicit
 // digit-reversal pass is needed.  Twiddle W_n^{ck} = tw[c k M/n].
 template <int NT, int R>
-__device__ __forceinline__ void dif_stage(double2* s, int M, int n, const double2* __restrict__ tw) {
+__device__ __forceinline__ void dif_stage(double2* s, int M, int n, const double2* t1, const double2* t2) {
   const int m = n / R;
   const int nbf = M / R;
   const int tws = M / n;
@@ -257,14 +458,24 @@ __device__ __forceinline__ void dif_stage(double2* s, int M, int n, const double
     for (int r = 0; r < R; ++r) v[r] = s[base + r * m];
     dft<R>(v);
     s[base] = v[0];
+    if (k == 0) {
 #pragma unroll
-    for (int c = 1; c < R; ++c) s[base + c * m] = (k == 0) ? v[c] : cmul(v[c], ldg2(tw + c * k * tws));
+      for (int c = 1; c < R; ++c) s[base + c * m] = v[c];
+    } else {
+      const double2 w1 = tw_lookup(t1, t2, k * tws);  // W_n^k; W_n^{ck} by recurrence
+      double2 w = w1;
+#pragma unroll
+      for (int c = 1; c < R; ++c) {
+        s[base + c * m] = cmul(v[c], w);
+        if (c + 1 < R) w = cmul(w, w1);
+      }
+    }
   }
   __syncthreads();
 }
 
 template <int NT, int R>
-__device__ __forceinline__ void dit_stage(double2* s, int M, int n, const double2* __restrict__ tw) {
+__device__ __forceinline__ void dit_stage(double2* s, int M, int n, const double2* t1, const double2* t2) {
   const int m = n / R;
   const int nbf = M / R;
   const int tws = M / n;
@@ -274,10 +485,17 @@ __device__ __forceinline__ void dit_stage(double2* s, int M, int n, const double
     const int base = blk * n + k;
     double2 v[R];
     v[0] = s[base];
+    if (k == 0) {
 #pragma unroll
-    for (int r = 1; r < R; ++r) {
-      const double2 x = s[base + r * m];
-      v[r] = (k == 0) ? x : cmul(x, ldg2(tw + r * k * tws));
+      for (int r = 1; r < R; ++r) v[r] = s[base + r * m];
+    } else {
+      const double2 w1 = tw_lookup(t1, t2, k * tws);
+      double2 w = w1;
+#pragma unroll
+      for (int r = 1; r < R; ++r) {
+        v[r] = cmul(s[base + r * m], w);
+        if (r + 1 < R) w = cmul(w, w1);
+      }
     }
     dft<R>(v);
 #pragma unroll
@@ -287,46 +505,54 @@ __device__ __forceinline__ void dit_stage(double2* s, int M, int n, const double
 }
 
 template <int NT, bool DIF>
-__device__ __forceinline__ void stage(double2* s, int R, int M, int n, const double2* tw) {
+__device__ __forceinline__ void stage(double2* s, int R, int M, int n, const double2* t1, const double2* t2) {
   switch (R) {
 #define DSFT_STAGE(RR) \
-  case RR: DIF ? dif_stage<NT, RR>(s, M, n, tw) : dit_stage<NT, RR>(s, M, n, tw); break;
-    DSFT_STAGE(2) DSFT_STAGE(3) DSFT_STAGE(4) DSFT_STAGE(5) DSFT_STAGE(7) DSFT_STAGE(8) DSFT_STAGE(11) DSFT_STAGE(13)
+  case RR: DIF ? dif_stage<NT, RR>(s, M, n, t1, t2) : dit_stage<NT, RR>(s, M, n, t1, t2); break;
+    DSFT_STAGE(2) DSFT_STAGE(3) DSFT_STAGE(4) DSFT_STAGE(5) DSFT_STAGE(6) DSFT_STAGE(7) DSFT_STAGE(8)
+    DSFT_STAGE(9) DSFT_STAGE(10) DSFT_STAGE(11) DSFT_STAGE(12) DSFT_STAGE(13) DSFT_STAGE(14) DSFT_STAGE(15)
+    DSFT_STAGE(16)
 #undef DSFT_STAGE
     default: break;
   }
 }
 
 template <int NT>
-__device__ void fft_dif(double2* s, const K2Params& p) {
+__device__ void fft_dif(double2* s, const K2Params& p, const double2* t1, const double2* t2) {
   int n = p.M;
   for (int i = 0; i < p.nfac; ++i) {
-    stage<NT, true>(s, p.fac[i], p.M, n, p.tw);
+    stage<NT, true>(s, p.fac[i], p.M, n, t1, t2);
     n /= p.fac[i];
   }
 }
 
 template <int NT>
-__device__ void fft_dit(double2* s, const K2Params& p) {
+__device__ void fft_dit(double2* s, const K2Params& p, const double2* t1, const double2* t2) {
   int n = 1;
   for (int i = p.nfac - 1; i >= 0; --i) {
     n *= p.fac[i];
-    stage<NT, false>(s, p.fac[i], p.M, n, p.tw);
+    stage<NT, false>(s, p.fac[i], p.M, n, t1, t2);
   }
 }
 
 // X[0] = sum x; X[g^-p] = x[0] + (a (*) b)[p], a_q = x[g^q], b_m = W_P^{g^-m}.
+// Row I/O is coalesced: x[n] lands in smem at q = dlog[n]; the output X[n] is
+// read back from p = -dlog[n] mod M.
 template <int NT>
-__global__ void __launch_bounds__(NT) k2_prime_dft(const __grid_constant__ K2Params p) {
+__global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 2) k2_prime_dft(const __grid_constant__ K2Params p) {
   extern __shared__ double2 sm[];
   __shared__ double2 red[NT / 32];
-  double2* row = p.Z + (int64_t)blockIdx.y * p.z_vec_stride + (int64_t)blockIdx.x * p.P;
   const int M = p.M;
+  double2* t1 = sm + M;
+  double2* t2 = t1 + p.nt1;
+  for (int i = threadIdx.x; i < p.nt1; i += NT) t1[i] = ldg2(p.tw1 + i);
+  for (int i = threadIdx.x; i < 64; i += NT) t2[i] = ldg2(p.tw2 + i);
+  double2* row = p.Z + (int64_t)blockIdx.y * p.z_vec_stride + (int64_t)blockIdx.x * p.P;
   const double2 x0 = row[0];
   double2 acc = make_double2(0.0, 0.0);
-  for (int q = threadIdx.x; q < M; q += NT) {
-    const double2 val = row[__ldg(p.perm_in + q)];
-    sm[q] = val;
+  for (int n = 1 + threadIdx.x; n < p.P; n += NT) {
+    const double2 val = row[n];
+    sm[__ldg(p.dlog + n)] = val;
     acc = cadd(acc, val);
   }
 #pragma unroll
@@ -336,11 +562,14 @@ __global__ void __launch_bounds__(NT) k2_prime_dft(const __grid_constant__ K2Par
   }
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
   __syncthreads();
-  fft_dif<NT>(sm, p);
+  fft_dif<NT>(sm, p, t1, t2);
   for (int k = threadIdx.x; k < M; k += NT) sm[k] = cconj(cmul(sm[k], ldg2(p.bhat + k)));
   __syncthreads();
-  fft_dit<NT>(sm, p);
-  for (int q = threadIdx.x; q < M; q += NT) row[__ldg(p.perm_out + q)] = cadd(x0, cconj(sm[q]));
+  fft_dit<NT>(sm, p, t1, t2);
+  for (int n = 1 + threadIdx.x; n < p.P; n += NT) {
+    const int d = __ldg(p.dlog + n);
+    row[n] = cadd(x0, cconj(sm[d == 0 ? 0 : M - d]));
+  }
   if (threadIdx.x == 0) {
     double2 X0 = x0;
     for (int w = 0; w < NT / 32; ++w) X0 = cadd(X0, red[w]);
@@ -391,6 +620,7 @@ __device__ __forceinline__ void residue_argmax(const double2* __restrict__ col, 
   yv = cscale(y, invL);
 }
 
+template <int RMAX>
 __global__ void __launch_bounds__(256) k3_identify(const __grid_constant__ K3Params p) {
   const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (gid >= (int64_t)p.nb * p.P) return;
@@ -405,16 +635,13 @@ __global__ void __launch_bounds__(256) k3_identify(const __grid_constant__ K3Par
     double2 y = make_double2(0.0, 0.0);
     const int sb = p.shift_base[i];
     switch (p.r[i]) {
-      case 3: residue_argmax<3>(col, p.P, sb, p.invL[i], b, y); break;
-      case 5: residue_argmax<5>(col, p.P, sb, p.invL[i], b, y); break;
-      case 7: residue_argmax<7>(col, p.P, sb, p.invL[i], b, y); break;
-      case 11: residue_argmax<11>(col, p.P, sb, p.invL[i], b, y); break;
-      case 13: residue_argmax<13>(col, p.P, sb, p.invL[i], b, y); break;
-      case 17: residue_argmax<17>(col, p.P, sb, p.invL[i], b, y); break;
-      case 19: residue_argmax<19>(col, p.P, sb, p.invL[i], b, y); break;
-      case 23: residue_argmax<23>(col, p.P, sb, p.invL[i], b, y); break;
-      case 29: residue_argmax<29>(col, p.P, sb, p.invL[i], b, y); break;
-      case 31: residue_argmax<31>(col, p.P, sb, p.invL[i], b, y); break;
+#define DSFT_RES(RR) \
+  case RR:           \
+    if constexpr (RR <= RMAX) residue_argmax<RR>(col, p.P, sb, p.invL[i], b, y); \
+    break;
+      DSFT_RES(3) DSFT_RES(5) DSFT_RES(7) DSFT_RES(11) DSFT_RES(13) DSFT_RES(17) DSFT_RES(19) DSFT_RES(23)
+      DSFT_RES(29) DSFT_RES(31)
+#undef DSFT_RES
       default: break;
     }
     R += (int64_t)b * p.crtE[i + 1];
@@ -435,31 +662,79 @@ __global__ void __launch_bounds__(256) k3_identify(const __grid_constant__ K3Par
   }
 }
 
-// ========================================================= K4/K5 vote_estimate
-struct K45Params {
+// ================================================================ K4 vote
+// Reading R9: omega is accepted in its band when at least v_min distinct bucket
+// primes produced it.  The owner slot (smallest such t) appends (omega, voter
+// mask) to the band's list and (band, position) to one global worklist, with
+// atomic counters.  List order is arbitrary; everything downstream is rank-
+// based on a total order, so results are deterministic.
+struct K4Params {
   const int64_t* cand_w;
-  const double2* cand_v;
   int64_t cw_vec_stride, sumP;
-  int T, Kmax, vote_min, nb;
+  int T, vote_min, nb, pad_;
   int64_t P[DSFT_MAX_T];
   int64_t off[DSFT_MAX_T];
-  int K[DSFT_MAX_T];
-  int64_t qfirst, qstep;
-  double c1;
-  int64_t budget;
-  int64_t band_vec, bn_vec;
   int64_t* acc_w;
-  double2* acc_z;
-  int64_t* band_w;
-  double2* band_c;
-  double2* band_z;
-  int32_t* band_n;
+  int32_t* acc_mask;
+  int32_t* acc_n;    // [vec][band]
+  int64_t bn_vec;
+  int64_t* work;     // [vec][band * sumP] packed (band << 32 | pos)
+  int32_t* work_n;   // [vec]
 };
 
 __device__ __forceinline__ int64_t pmod(int64_t x, int64_t m) {
   int64_t r = x % m;
   return r < 0 ? r + m : r;
 }
+
+__global__ void __launch_bounds__(256) k4_vote(const __grid_constant__ K4Params p) {
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= (int64_t)p.nb * p.sumP) return;
+  const int v = blockIdx.y;
+  const int j = (int)(gid / p.sumP);
+  const int64_t idx = gid - (int64_t)j * p.sumP;
+  const int64_t base = (int64_t)v * p.cw_vec_stride + (int64_t)j * p.sumP;
+  const int64_t* cw = p.cand_w + base;
+  const int64_t om = cw[idx];
+  if (om == kSentinel) return;
+  int t = 0;
+  while (t + 1 < p.T && idx >= p.off[t + 1]) ++t;
+  int votes = 0;
+  int32_t mask = 0;
+  for (int t2 = 0; t2 < p.T; ++t2) {
+    if (t2 == t || __ldg(cw + p.off[t2] + pmod(om, p.P[t2])) == om) {
+      if (t2 < t) return;  // not the owner
+      ++votes;
+      mask |= 1 << t2;
+    }
+  }
+  if (votes < p.vote_min) return;
+  const int pos = atomicAdd(p.acc_n + (int64_t)v * p.bn_vec + j, 1);
+  p.acc_w[base + pos] = om;
+  p.acc_mask[base + pos] = mask;
+  const int gpos = atomicAdd(p.work_n + v, 1);
+  p.work[(int64_t)v * p.cw_vec_stride + gpos] = ((int64_t)j << 32) | (int64_t)pos;
+}
+
+// =========================================================== K5a medians
+// Reading R10: z = median Re + i median Im of (-1)^omega E_{t,i}[omega mod L]
+// over the voting primes t (mask from K4) and all residues i (PAPER.md:167,
+// 872-874).  One warp per accepted omega anywhere on the GPU, one value per lane.
+struct K5aParams {
+  const double2* cand_v;
+  int64_t cw_vec_stride, sumP;
+  int T, Kmax;
+  int64_t P[DSFT_MAX_T];
+  int64_t off[DSFT_MAX_T];
+  int K[DSFT_MAX_T];
+  const int64_t* acc_w;
+  const int32_t* acc_mask;
+  double2* acc_z;
+  const int64_t* work;
+  const int32_t* work_n;
+};
+
+constexpr int kMaxVals = DSFT_MAX_T * DSFT_MAX_K;
 
 __device__ void sort_small(double* a, int n) {
   for (int i = 1; i < n; ++i) {
@@ -473,179 +748,301 @@ __device__ void sort_small(double* a, int n) {
   }
 }
 
-constexpr int kK45Threads = 256;
-constexpr int kMaxVals = DSFT_MAX_T * DSFT_MAX_K;
+// Median of up to 32 values held one per lane (pad +inf): bitonic sort by
+// shuffles, then the middle order statistic(s) (mean of the two middle ones for
+// even counts, as numpy's median).
+__device__ __forceinline__ double warp_median(double v, int cnt, int lane) {
+#pragma unroll
+  for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      const double o = __shfl_xor_sync(0xffffffffu, v, j);
+      const bool up = (lane & k) == 0;
+      const bool lower = (lane & j) == 0;
+      v = (lower == up) ? fmin(v, o) : fmax(v, o);
+    }
+  }
+  const double a = __shfl_sync(0xffffffffu, v, (cnt - 1) >> 1);
+  const double b = __shfl_sync(0xffffffffu, v, cnt >> 1);
+  return (cnt & 1) ? b : 0.5 * (a + b);
+}
 
-__global__ void __launch_bounds__(kK45Threads) k45_vote_estimate(const __grid_constant__ K45Params p) {
-  const int j = blockIdx.x, v = blockIdx.y;
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int64_t cw_base = (int64_t)v * p.cw_vec_stride + (int64_t)j * p.sumP;
-  const int64_t* cw = p.cand_w + cw_base;
-  int64_t* accw = p.acc_w + cw_base;
-  double2* accz = p.acc_z + cw_base;
-  __shared__ int wsum[kK45Threads / 32];
-  __shared__ int s_base;
-  if (tid == 0) s_base = 0;
-  __syncthreads();
-  // ---- vote (R9): owner = smallest t producing omega; accept at >= v_min primes
-  for (int64_t c0 = 0; c0 < p.sumP; c0 += kK45Threads) {
-    const int64_t idx = c0 + tid;
-    int flag = 0;
-    int64_t om = kSentinel;
-    if (idx < p.sumP) {
-      om = cw[idx];
-      if (om != kSentinel) {
-        int t = 0;
-        while (t + 1 < p.T && idx >= p.off[t + 1]) ++t;
-        int votes = 1;
-        bool owner = true;
-        for (int t2 = 0; t2 < p.T; ++t2) {
-          if (t2 == t) continue;
-          if (cw[p.off[t2] + pmod(om, p.P[t2])] == om) {
-            ++votes;
-            if (t2 < t) owner = false;
+__global__ void __launch_bounds__(256) k5a_medians(const __grid_constant__ K5aParams p) {
+  const int v = blockIdx.y;
+  const int lane = threadIdx.x & 31;
+  const int nwarps = gridDim.x * (blockDim.x >> 5);
+  const int total = p.work_n[v];
+  for (int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w < total; w += nwarps) {
+    const int64_t packed = p.work[(int64_t)v * p.cw_vec_stride + w];
+    const int j = (int)(packed >> 32);
+    const int pos = (int)(packed & 0xffffffff);
+    const int64_t base = (int64_t)v * p.cw_vec_stride + (int64_t)j * p.sumP;
+    const int64_t om = p.acc_w[base + pos];
+    const int32_t mask = p.acc_mask[base + pos];
+    const double sgn = (om & 1) ? -1.0 : 1.0;
+    // lane -> (t, i) over the voting primes in ascending t
+    int cnt = 0, my_t = -1, my_i = 0;
+    for (int t = 0; t < p.T; ++t) {
+      if (mask & (1 << t)) {
+        if (lane >= cnt && lane < cnt + p.K[t]) {
+          my_t = t;
+          my_i = lane - cnt;
+        }
+        cnt += p.K[t];
+      }
+    }
+    double2 z = make_double2(0.0, 0.0);
+    if (cnt <= 32) {
+      double re = INFINITY, im = INFINITY;
+      if (my_t >= 0) {
+        const int64_t slot = p.off[my_t] + pmod(om, p.P[my_t]);
+        const double2 y = p.cand_v[(base + slot) * p.Kmax + my_i];
+        re = sgn * y.x;
+        im = sgn * y.y;
+      }
+      z.x = warp_median(re, cnt, lane);
+      z.y = warp_median(im, cnt, lane);
+    } else if (lane == 0) {  // more than 32 voting grids (T*K > 32): serial fallback
+      double rv[kMaxVals], iv[kMaxVals];
+      int c = 0;
+      for (int t = 0; t < p.T; ++t)
+        if (mask & (1 << t)) {
+          const int64_t slot = p.off[t] + pmod(om, p.P[t]);
+          for (int i = 0; i < p.K[t]; ++i) {
+            const double2 y = p.cand_v[(base + slot) * p.Kmax + i];
+            rv[c] = sgn * y.x;
+            iv[c] = sgn * y.y;
+            ++c;
           }
         }
-        flag = (owner && votes >= p.vote_min) ? 1 : 0;
-      }
+      sort_small(rv, c);
+      sort_small(iv, c);
+      z = (c & 1) ? make_double2(rv[c / 2], iv[c / 2])
+                  : make_double2(0.5 * (rv[c / 2 - 1] + rv[c / 2]), 0.5 * (iv[c / 2 - 1] + iv[c / 2]));
     }
-    const unsigned bal = __ballot_sync(0xffffffffu, flag);
-    if (lane == 0) wsum[wid] = __popc(bal);
-    __syncthreads();
-    int pre = 0, tot = 0;
-    for (int w = 0; w < kK45Threads / 32; ++w) {
-      if (w < wid) pre += wsum[w];
-      tot += wsum[w];
-    }
-    pre += __popc(bal & ((1u << lane) - 1u));
-    if (flag) accw[s_base + pre] = om;
-    __syncthreads();
-    if (tid == 0) s_base += tot;
-    __syncthreads();
+    if (lane == 0) p.acc_z[base + pos] = z;
   }
-  const int n = s_base;
+}
+
+// ============================================================ K5b select
+// R11: keep the band_budget largest |z|^2 (ties -> smaller omega); line 11
+// (PAPER.md:242): c = z / ghat_{omega-q}; kept entries are written sorted by
+// the merge key m = |c|^2 desc (exact zeros last with m = -1), omega asc.
+// One CTA per band; the band's list is staged in shared memory tiles.
+struct K5bParams {
+  int64_t cw_vec_stride, sumP;
+  int nb, pad_;
+  int64_t qfirst, qstep;
+  double c1;
+  int64_t budget;
+  int64_t band_vec, bn_vec;
+  const int64_t* acc_w;
+  const double2* acc_z;
+  int32_t* acc_r;
+  const int32_t* acc_n;
+  int64_t* band_w;
+  double2* band_c;
+  double2* band_z;
+  double* band_m;
+  int32_t* band_n;
+  int32_t* band_nz;
+};
+
+constexpr int kK5Threads = 256;
+constexpr int kRankTile = 2048;
+
+__device__ __forceinline__ double ghat_dev(double c1, int64_t dq) {
+  const double d = (double)dq;
+  return exp(-(c1 * c1) * d * d / 2.0) / 2.5066282746310002;  // Lemma 2
+}
+
+__global__ void __launch_bounds__(kK5Threads) k5b_select(const __grid_constant__ K5bParams p) {
+  const int j = blockIdx.x, v = blockIdx.y, tid = threadIdx.x;
+  const int64_t base = (int64_t)v * p.cw_vec_stride + (int64_t)j * p.sumP;
+  const int64_t* accw = p.acc_w + base;
+  const double2* accz = p.acc_z + base;
+  int32_t* accr = p.acc_r + base;
+  const int n = p.acc_n[(int64_t)v * p.bn_vec + j];
   const int64_t q = p.qfirst + (int64_t)j * p.qstep;
-  // ---- estimate (R10): separate Re/Im medians of (-1)^omega E over voting grids
-  for (int e = tid; e < n; e += kK45Threads) {
-    const int64_t om = accw[e];
-    double re[kMaxVals], im[kMaxVals];
-    int cnt = 0;
-    const double sgn = (om & 1) ? -1.0 : 1.0;
-    for (int t = 0; t < p.T; ++t) {
-      const int64_t slot = p.off[t] + pmod(om, p.P[t]);
-      if (cw[slot] == om) {
-        const double2* cv = p.cand_v + (cw_base + slot) * p.Kmax;
-        for (int i = 0; i < p.K[t]; ++i) {
-          const double2 y = cv[i];
-          re[cnt] = sgn * y.x;
-          im[cnt] = sgn * y.y;
-          ++cnt;
-        }
+  __shared__ double sm_m[kRankTile];
+  __shared__ int64_t sm_w[kRankTile];
+  __shared__ int s_nz;
+  if (tid == 0) s_nz = 0;
+  // ---- rank 1: (|z|^2 desc, omega asc); keep rank < budget
+  for (int e0 = 0; e0 < n; e0 += kK5Threads) {
+    const int e = e0 + tid;
+    double my_m = 0.0;
+    int64_t my_w = 0;
+    if (e < n) {
+      my_m = cabs2_rn(accz[e]);
+      my_w = accw[e];
+    }
+    int rank = 0;
+    for (int t0 = 0; t0 < n; t0 += kRankTile) {
+      const int len = min(kRankTile, n - t0);
+      __syncthreads();
+      for (int i = tid; i < len; i += kK5Threads) {
+        sm_m[i] = cabs2_rn(accz[t0 + i]);
+        sm_w[i] = accw[t0 + i];
       }
+      __syncthreads();
+      if (e < n)
+        for (int i = 0; i < len; ++i) rank += (sm_m[i] > my_m || (sm_m[i] == my_m && sm_w[i] < my_w)) ? 1 : 0;
     }
-    sort_small(re, cnt);
-    sort_small(im, cnt);
-    double2 z;
-    if (cnt & 1) {
-      z = make_double2(re[cnt / 2], im[cnt / 2]);
-    } else {
-      z = make_double2(0.5 * (re[cnt / 2 - 1] + re[cnt / 2]), 0.5 * (im[cnt / 2 - 1] + im[cnt / 2]));
-    }
-    accz[e] = z;
+    if (e < n) accr[e] = rank;
   }
   __syncthreads();
-  // ---- band top-budget by (|z|^2 desc, omega asc) (R11), unbias (line 11)
-  const int64_t bbase = (int64_t)v * p.band_vec + (int64_t)j * p.budget;
-  for (int e = tid; e < n; e += kK45Threads) {
-    const int64_t om = accw[e];
-    const double2 z = accz[e];
-    const double m = cabs2_rn(z);
-    int64_t rank = 0;
-    for (int e2 = 0; e2 < n; ++e2) {
-      const double m2 = cabs2_rn(accz[e2]);
-      if (m2 > m || (m2 == m && accw[e2] < om)) ++rank;
+  // ---- rank 2 among kept -> output slot
+  for (int e0 = 0; e0 < n; e0 += kK5Threads) {
+    const int e = e0 + tid;
+    bool keep = false;
+    double my_m = 0.0;
+    int64_t my_w = 0;
+    double2 my_z = make_double2(0.0, 0.0), my_c = my_z;
+    if (e < n && accr[e] < p.budget) {
+      keep = true;
+      my_w = accw[e];
+      my_z = accz[e];
+      const double gh = ghat_dev(p.c1, my_w - q);
+      my_c = make_double2(my_z.x / gh, my_z.y / gh);
+      my_m = (my_c.x == 0.0 && my_c.y == 0.0) ? -1.0 : cabs2_rn(my_c);
     }
-    if (rank < p.budget) {
-      const double dq = (double)(om - q);
-      const double gh = exp(-(p.c1 * p.c1) * dq * dq / 2.0) / 2.5066282746310002;
-      p.band_w[bbase + rank] = om;
-      p.band_z[bbase + rank] = z;
-      p.band_c[bbase + rank] = make_double2(z.x / gh, z.y / gh);
+    int rank = 0;
+    for (int t0 = 0; t0 < n; t0 += kRankTile) {
+      const int len = min(kRankTile, n - t0);
+      __syncthreads();
+      for (int i = tid; i < len; i += kK5Threads) {
+        if (accr[t0 + i] < p.budget) {
+          const int64_t w2 = accw[t0 + i];
+          const double2 z2 = accz[t0 + i];
+          const double gh = ghat_dev(p.c1, w2 - q);
+          const double2 c2 = make_double2(z2.x / gh, z2.y / gh);
+          sm_m[i] = (c2.x == 0.0 && c2.y == 0.0) ? -1.0 : cabs2_rn(c2);
+          sm_w[i] = w2;
+        } else {
+          sm_m[i] = -2.0;  // not kept: never ranks ahead
+          sm_w[i] = 0;
+        }
+      }
+      __syncthreads();
+      if (keep)
+        for (int i = 0; i < len; ++i) rank += (sm_m[i] > my_m || (sm_m[i] == my_m && sm_w[i] < my_w)) ? 1 : 0;
+    }
+    if (keep) {
+      const int64_t o = (int64_t)v * p.band_vec + (int64_t)j * p.budget + rank;
+      p.band_w[o] = my_w;
+      p.band_z[o] = my_z;
+      p.band_c[o] = my_c;
+      p.band_m[o] = my_m;
+      if (my_m >= 0.0) atomicAdd(&s_nz, 1);
     }
   }
-  if (tid == 0) p.band_n[(int64_t)v * p.bn_vec + j] = (int32_t)(n < p.budget ? n : p.budget);
+  __syncthreads();
+  if (tid == 0) {
+    p.band_n[(int64_t)v * p.bn_vec + j] = (int32_t)(n < p.budget ? n : p.budget);
+    p.band_nz[(int64_t)v * p.bn_vec + j] = s_nz;
+  }
 }
 
 // ================================================================= K6 merge
+// Line 13: the s largest |c| over all band blocks, ties ->
+// smaller omega; exact zeros dropped (R12).  Every block is
+// sorted by the key (|c|^2 desc, omega asc) with its non-zero entries first
+// (K5b).  The non-zero prefixes are staged contiguously in shared memory; the
+// global rank of entry i of block b is i + the number of entries of every other
+// block ahead of it (binary search).  O(n log n), one thread per entry.
 struct K6Params {
   const int64_t* band_w;
   const double2* band_c;
-  const int32_t* band_n;
-  int nb;            // band blocks per vector
-  int64_t budget;    // capacity per block
-  int64_t blk_vec, bn_vec;  // per-vector strides of band_w/band_c and band_n
+  const double* band_m;
+  const int32_t* band_nz;
+  int nb;                    // band blocks per vector
+  int64_t budget;            // capacity per block
+  int64_t blk_vec, bn_vec;   // per-vector strides of the block arrays and of the counts
   int64_t s;
   int64_t* out_w;
   double2* out_c;
 };
 
-constexpr int kK6Threads = 1024;
+constexpr int kK6Threads = 256;
 constexpr int kK6MaxBlocks = 512;
+constexpr int kK6Stage = 4096;  // entries staged in shared memory (48 KB dynamic)
+
+__device__ __forceinline__ bool key_ahead(double m2, int64_t w2, double m, int64_t w) {
+  return m2 > m || (m2 == m && w2 < w);
+}
 
 __global__ void __launch_bounds__(kK6Threads) k6_merge(const __grid_constant__ K6Params p) {
-  const int v = blockIdx.x;
-  const int tid = threadIdx.x;
-  __shared__ int64_t pre[kK6MaxBlocks + 1];
-  __shared__ int s_elig;
-  const int32_t* bn = p.band_n + (int64_t)v * p.bn_vec;
-  if (tid == 0) {
+  const int v = blockIdx.y;
+  extern __shared__ unsigned char k6_smem[];
+  double* sm_m = (double*)k6_smem;
+  int64_t* sm_w = (int64_t*)(sm_m + kK6Stage);
+  __shared__ int32_t pre[kK6MaxBlocks + 1];
+  const int32_t* bz = p.band_nz + (int64_t)v * p.bn_vec;
+  if (threadIdx.x == 0) {
     pre[0] = 0;
-    for (int b = 0; b < p.nb; ++b) pre[b + 1] = pre[b] + bn[b];
-    s_elig = 0;
+    for (int b = 0; b < p.nb; ++b) pre[b + 1] = pre[b] + bz[b];
   }
   __syncthreads();
-  const int64_t n = pre[p.nb];
+  const int64_t n = pre[p.nb];  // eligible (non-zero) entries
   const int64_t* bw = p.band_w + (int64_t)v * p.blk_vec;
+  const double* bm = p.band_m + (int64_t)v * p.blk_vec;
   const double2* bc = p.band_c + (int64_t)v * p.blk_vec;
-  auto slot_of = [&](int64_t e) -> int64_t {
-    int b = 0;
-    while (pre[b + 1] <= e) ++b;
-    return (int64_t)b * p.budget + (e - pre[b]);
-  };
-  int local = 0;
-  for (int64_t e = tid; e < n; e += kK6Threads) {
-    const double2 c = bc[slot_of(e)];
-    if (!(c.x == 0.0 && c.y == 0.0)) ++local;
-  }
-  atomicAdd(&s_elig, local);
-  __syncthreads();
-  const int64_t elig = s_elig;
   int64_t* ow = p.out_w + (int64_t)v * p.s;
   double2* oc = p.out_c + (int64_t)v * p.s;
-  for (int64_t e = tid; e < n; e += kK6Threads) {
-    const int64_t sl = slot_of(e);
-    const double2 c = bc[sl];
-    if (c.x == 0.0 && c.y == 0.0) continue;
-    const int64_t om = bw[sl];
-    const double m = cabs2_rn(c);
-    int64_t rank = 0;
-    for (int b = 0; b < p.nb; ++b) {
-      for (int64_t k = 0; k < bn[b]; ++k) {
-        const int64_t sl2 = (int64_t)b * p.budget + k;
-        const double2 c2 = bc[sl2];
-        if (c2.x == 0.0 && c2.y == 0.0) continue;
-        const double m2 = cabs2_rn(c2);
-        if (m2 > m || (m2 == m && bw[sl2] < om)) ++rank;
+  const int64_t e = (int64_t)blockIdx.x * kK6Threads + threadIdx.x;  // flat eligible index
+  const int64_t e0 = (int64_t)blockIdx.x * kK6Threads;
+  if (e0 < n) {  // CTA-uniform
+    const bool staged = n <= kK6Stage;
+    if (staged) {
+      for (int64_t i = threadIdx.x; i < n; i += kK6Threads) {
+        int lo = 0, hi = p.nb;  // block of flat entry i: largest b with pre[b] <= i
+        while (hi - lo > 1) {
+          const int mid = (lo + hi) >> 1;
+          if (pre[mid] <= i) lo = mid;
+          else hi = mid;
+        }
+        const int64_t sl = (int64_t)lo * p.budget + (i - pre[lo]);
+        sm_m[i] = bm[sl];
+        sm_w[i] = bw[sl];
+      }
+      __syncthreads();
+    }
+    if (e < n) {
+      int lo = 0, hi = p.nb;
+      while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (pre[mid] <= e) lo = mid;
+        else hi = mid;
+      }
+      const int b = lo;
+      const int64_t i = e - pre[b];
+      const int64_t sl = (int64_t)b * p.budget + i;
+      const double m = staged ? sm_m[e] : bm[sl];
+      const int64_t w = staged ? sm_w[e] : bw[sl];
+      int64_t rank = i;
+      for (int b2 = 0; b2 < p.nb; ++b2) {
+        if (b2 == b) continue;
+        int l2 = 0, h2 = pre[b2 + 1] - pre[b2];  // first entry of b2 not ahead of (m, w)
+        const int64_t f2 = pre[b2], o2 = (int64_t)b2 * p.budget;
+        while (l2 < h2) {
+          const int mid = (l2 + h2) >> 1;
+          const bool ahead = staged ? key_ahead(sm_m[f2 + mid], sm_w[f2 + mid], m, w)
+                                    : key_ahead(bm[o2 + mid], bw[o2 + mid], m, w);
+          if (ahead) l2 = mid + 1;
+          else h2 = mid;
+        }
+        rank += l2;
+      }
+      if (rank < p.s) {
+        ow[rank] = w;
+        oc[rank] = bc[sl];
       }
     }
-    if (rank < p.s) {
-      ow[rank] = om;
-      oc[rank] = c;
-    }
   }
-  for (int64_t g = elig + tid; g < p.s; g += kK6Threads) {
-    ow[g] = kSentinel;
-    oc[g] = make_double2(0.0, 0.0);
+  if (e >= n && e < p.s) {  // unused output slots
+    ow[e] = kSentinel;
+    oc[e] = make_double2(0.0, 0.0);
   }
 }
 
@@ -688,7 +1085,7 @@ cudaError_t kernels_init() {
   cudaError_t e;
   const int maxsm = 227 * 1024 - 1024;  // leave room for the static reduction buffer
   if ((e = cudaFuncSetAttribute(k2_prime_dft<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm))) return e;
-  if ((e = cudaFuncSetAttribute(k2_prime_dft<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm))) return e;
+  if ((e = cudaFuncSetAttribute(k6_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, kK6Stage * 16))) return e;
   if ((e = cudaFuncSetAttribute(k2_prime_dft<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm))) return e;
   if ((e = cudaFuncSetAttribute(k2_prime_dft<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm))) return e;
   done = true;
@@ -735,10 +1132,12 @@ cudaError_t launch_k1(const Plan& p, int t, const double2* f, int64_t ld, int nv
         for (int c = 0; c < 2; ++c) k.tab[(jj * p.kappa + u) * 2 + c] = p.k1tab[((size_t)bands[jj] * p.kappa + u) * 2 + c];
   }
   const int64_t nodes = (int64_t)b.S * b.P;
-  dim3 grid(cdiv(nodes, 256), nvec);
-  if (fast && p.kappa == 6) k1_gather_mix<6><<<grid, 256, 0, st>>>(k);
-  else if (fast && p.kappa == 4) k1_gather_mix<4><<<grid, 256, 0, st>>>(k);
-  else k1_gather_mix<0><<<grid, 256, 0, st>>>(k);
+  if (fast && p.kappa == 6)
+    k1_gather_mix_fast<6><<<dim3(cdiv(nodes, kK1FastThreads), nvec), kK1FastThreads, 0, st>>>(k);
+  else if (fast && p.kappa == 4)
+    k1_gather_mix_fast<4><<<dim3(cdiv(nodes, kK1FastThreads), nvec), kK1FastThreads, 0, st>>>(k);
+  else
+    k1_gather_mix<0><<<dim3(cdiv(nodes, 256), nvec), 256, 0, st>>>(k);
   return cudaGetLastError();
 }
 
@@ -752,18 +1151,16 @@ cudaError_t launch_k2(const Plan& p, int t, int nvec, void* ws, const int* /*ban
   k.M = b.M;
   k.nfac = b.nfac;
   for (int i = 0; i < b.nfac; ++i) k.fac[i] = b.fac[i];
-  k.perm_in = b.perm_in;
-  k.perm_out = b.perm_out;
+  k.dlog = b.dlog;
   k.bhat = b.bhat;
-  k.tw = b.tw;
+  k.tw1 = b.tw1;
+  k.tw2 = b.tw2;
+  k.nt1 = b.nt1;
   dim3 grid((unsigned)(nbands * b.S), nvec);
-  const size_t smem = (size_t)b.M * sizeof(double2);
-  switch (b.fft_threads) {
-    case 64: k2_prime_dft<64><<<grid, 64, smem, st>>>(k); break;
-    case 128: k2_prime_dft<128><<<grid, 128, smem, st>>>(k); break;
-    case 256: k2_prime_dft<256><<<grid, 256, smem, st>>>(k); break;
-    default: k2_prime_dft<512><<<grid, 512, smem, st>>>(k); break;
-  }
+  const size_t smem = (size_t)(b.M + b.nt1 + 64) * sizeof(double2);
+  if (b.fft_threads <= 64) k2_prime_dft<64><<<grid, 64, smem, st>>>(k);
+  else if (b.fft_threads <= 256) k2_prime_dft<256><<<grid, 256, smem, st>>>(k);
+  else k2_prime_dft<512><<<grid, 512, smem, st>>>(k);
   return cudaGetLastError();
 }
 
@@ -799,68 +1196,108 @@ cudaError_t launch_k3(const Plan& p, int t, int nvec, void* ws, const int* bands
   k.sumP = p.sumP;
   k.off = b.off;
   dim3 grid(cdiv((int64_t)nbands * b.P, 256), nvec);
-  k3_identify<<<grid, 256, 0, st>>>(k);
+  if (p.Rmax <= 7) k3_identify<7><<<grid, 256, 0, st>>>(k);
+  else if (p.Rmax <= 13) k3_identify<13><<<grid, 256, 0, st>>>(k);
+  else if (p.Rmax <= 17) k3_identify<17><<<grid, 256, 0, st>>>(k);
+  else k3_identify<31><<<grid, 256, 0, st>>>(k);
   return cudaGetLastError();
 }
 
 cudaError_t launch_k45(const Plan& p, int nvec, void* ws, const int* bands, int nbands, cudaStream_t st) {
   const WsLayout L = ws_layout(p, p.ws_batch);
-  K45Params k{};
-  k.cand_w = (const int64_t*)((char*)ws + L.cand_w);
-  k.cand_v = (const double2*)((char*)ws + L.cand_v);
-  k.cw_vec_stride = L.cw_vec;
-  k.band_vec = L.band_vec;
-  k.bn_vec = L.bn_vec;
-  k.sumP = p.sumP;
-  k.T = p.T;
-  k.Kmax = p.Kmax;
-  k.vote_min = p.params.vote_min;
-  k.nb = nbands;
+  // zero the per-band and worklist counters (contiguous region)
+  cudaError_t e = cudaMemsetAsync((char*)ws + L.acc_n, 0, L.work - L.acc_n, st);
+  if (e != cudaSuccess) return e;
+  K4Params k4{};
+  k4.cand_w = (const int64_t*)((char*)ws + L.cand_w);
+  k4.cw_vec_stride = L.cw_vec;
+  k4.sumP = p.sumP;
+  k4.T = p.T;
+  k4.vote_min = p.params.vote_min;
+  k4.nb = nbands;
   for (int t = 0; t < p.T; ++t) {
-    k.P[t] = p.bk[t].P;
-    k.off[t] = p.bk[t].off;
-    k.K[t] = p.bk[t].K;
+    k4.P[t] = p.bk[t].P;
+    k4.off[t] = p.bk[t].off;
   }
+  k4.acc_w = (int64_t*)((char*)ws + L.acc_w);
+  k4.acc_mask = (int32_t*)((char*)ws + L.acc_mask);
+  k4.acc_n = (int32_t*)((char*)ws + L.acc_n);
+  k4.bn_vec = L.bn_vec;
+  k4.work = (int64_t*)((char*)ws + L.work);
+  k4.work_n = (int32_t*)((char*)ws + L.work_n);
+  k4_vote<<<dim3(cdiv((int64_t)nbands * p.sumP, 256), nvec), 256, 0, st>>>(k4);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+
+  K5aParams ka{};
+  ka.cand_v = (const double2*)((char*)ws + L.cand_v);
+  ka.cw_vec_stride = L.cw_vec;
+  ka.sumP = p.sumP;
+  ka.T = p.T;
+  ka.Kmax = p.Kmax;
+  for (int t = 0; t < p.T; ++t) {
+    ka.P[t] = p.bk[t].P;
+    ka.off[t] = p.bk[t].off;
+    ka.K[t] = p.bk[t].K;
+  }
+  ka.acc_w = k4.acc_w;
+  ka.acc_mask = k4.acc_mask;
+  ka.acc_z = (double2*)((char*)ws + L.acc_z);
+  ka.work = k4.work;
+  ka.work_n = k4.work_n;
+  k5a_medians<<<dim3(2 * 148, nvec), 256, 0, st>>>(ka);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+
+  K5bParams k{};
+  k.cw_vec_stride = L.cw_vec;
+  k.sumP = p.sumP;
+  k.nb = nbands;
   const int stride = nbands > 1 ? bands[1] - bands[0] : 1;
   k.qfirst = band_q(p, bands[0]);
   k.qstep = 2 * p.w * (int64_t)stride;
   k.c1 = p.c1;
   k.budget = p.info.band_budget;
-  k.acc_w = (int64_t*)((char*)ws + L.acc_w);
-  k.acc_z = (double2*)((char*)ws + L.acc_z);
+  k.band_vec = L.band_vec;
+  k.bn_vec = L.bn_vec;
+  k.acc_w = k4.acc_w;
+  k.acc_z = ka.acc_z;
+  k.acc_r = (int32_t*)((char*)ws + L.acc_r);
+  k.acc_n = k4.acc_n;
   k.band_w = (int64_t*)((char*)ws + L.band_w);
   k.band_c = (double2*)((char*)ws + L.band_c);
   k.band_z = (double2*)((char*)ws + L.band_z);
+  k.band_m = (double*)((char*)ws + L.band_m);
   k.band_n = (int32_t*)((char*)ws + L.band_n);
-  dim3 grid(nbands, nvec);
-  k45_vote_estimate<<<grid, kK45Threads, 0, st>>>(k);
+  k.band_nz = (int32_t*)((char*)ws + L.band_nz);
+  k5b_select<<<dim3(nbands, nvec), kK5Threads, 0, st>>>(k);
   return cudaGetLastError();
 }
 
-cudaError_t launch_k6_blocks(const int64_t* bw, const double2* bc, const int32_t* bn, int nblocks, int64_t budget,
-                             int64_t blk_vec, int64_t bn_vec, int64_t s, int nvec, int64_t* freqs, double2* coeffs,
-                             cudaStream_t st) {
+cudaError_t launch_k6_blocks(const int64_t* bw, const double2* bc, const double* bm, const int32_t* bnz, int nblocks,
+                             int64_t budget, int64_t blk_vec, int64_t bn_vec, int64_t s, int nvec, int64_t* freqs,
+                             double2* coeffs, cudaStream_t st) {
   if (nblocks > kK6MaxBlocks) return cudaErrorInvalidValue;
   K6Params k{};
-  k.blk_vec = blk_vec;
-  k.bn_vec = bn_vec;
   k.band_w = bw;
   k.band_c = bc;
-  k.band_n = bn;
+  k.band_m = bm;
+  k.band_nz = bnz;
   k.nb = nblocks;
   k.budget = budget;
+  k.blk_vec = blk_vec;
+  k.bn_vec = bn_vec;
   k.s = s;
   k.out_w = freqs;
   k.out_c = coeffs;
-  k6_merge<<<nvec, kK6Threads, 0, st>>>(k);
+  const int64_t cap = std::max<int64_t>((int64_t)nblocks * budget, s);
+  k6_merge<<<dim3(cdiv(cap, kK6Threads), nvec), kK6Threads, kK6Stage * 16, st>>>(k);
   return cudaGetLastError();
 }
 
 cudaError_t launch_k6(const Plan& p, int nvec, void* ws, int64_t* freqs, double2* coeffs, cudaStream_t st) {
   const WsLayout L = ws_layout(p, p.ws_batch);
   return launch_k6_blocks((const int64_t*)((char*)ws + L.band_w), (const double2*)((char*)ws + L.band_c),
-                          (const int32_t*)((char*)ws + L.band_n), p.J, p.info.band_budget, L.band_vec, L.bn_vec,
-                          p.s, nvec, freqs, coeffs, st);
+                          (const double*)((char*)ws + L.band_m), (const int32_t*)((char*)ws + L.band_nz), p.J,
+                          p.info.band_budget, L.band_vec, L.bn_vec, p.s, nvec, freqs, coeffs, st);
 }
 
 static int64_t modinv(int64_t a, int64_t m) {

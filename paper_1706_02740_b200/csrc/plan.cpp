@@ -158,10 +158,18 @@ WsLayout ws_layout(const Plan& p, int64_t nvec) {
   L.cand_v = take((size_t)nvec * L.cw_vec * p.Kmax * 16);
   L.acc_w = take((size_t)nvec * L.cw_vec * 8);
   L.acc_z = take((size_t)nvec * L.cw_vec * 16);
+  L.acc_r = take((size_t)nvec * L.cw_vec * 4);
+  L.acc_mask = take((size_t)nvec * L.cw_vec * 4);
+  // counters acc_n and work_n are contiguous (zeroed by one memset before K4)
+  L.acc_n = take((size_t)nvec * L.bn_vec * 4);
+  L.work_n = take((size_t)nvec * 4);
+  L.work = take((size_t)nvec * L.cw_vec * 8);
   L.band_w = take((size_t)nvec * L.band_vec * 8);
   L.band_c = take((size_t)nvec * L.band_vec * 16);
   L.band_z = take((size_t)nvec * L.band_vec * 16);
+  L.band_m = take((size_t)nvec * L.band_vec * 8);
   L.band_n = take((size_t)nvec * L.bn_vec * 4);
+  L.band_nz = take((size_t)nvec * L.bn_vec * 4);
   L.total = o;
   return L;
 }
@@ -293,11 +301,13 @@ static dsft_status derive(int64_t N, int64_t s, const dsft_params& prm, Plan& P)
     P.sumP += b.P;
     P.maxSP = std::max<int64_t>(P.maxSP, (int64_t)S * b.P);
     P.Kmax = std::max(P.Kmax, K);
+    P.Rmax = std::max(P.Rmax, b.r[K - 1]);
     P.Smax = std::max(P.Smax, S);
     // Rader setup: M = P - 1, primitive root g
     b.M = (int)(b.P - 1);
-    if ((size_t)b.M * 16 > 226 * 1024)
-      return fail(DSFT_ERR_UNSUPPORTED, "bucket prime above 14465 needs the multi-CTA DFT (not built yet)");
+    b.nt1 = b.M / 64 + 1;
+    if ((size_t)(b.M + b.nt1 + 64) * 16 > 226 * 1024)
+      return fail(DSFT_ERR_UNSUPPORTED, "bucket prime above ~14200 needs the multi-CTA DFT (not built yet)");
     const auto pf = prime_factors(b.M);
     int g = 2;
     for (;; ++g) {
@@ -310,17 +320,37 @@ static dsft_status derive(int64_t N, int64_t s, const dsft_params& prm, Plan& P)
       if (ok) break;
     }
     b.g = g;
+    // stage radices <= kMaxRadix (few smem passes at <= 128 registers): pack 2s,
+    // 3s, merge the smallest leftovers; radices with a factor 2 first (DIF
+    // stages with long contiguous runs), odd radices last.
     int m = b.M, nf = 0;
-    while (m % 8 == 0) b.fac[nf++] = 8, m /= 8;
-    while (m % 4 == 0) b.fac[nf++] = 4, m /= 4;
-    while (m % 2 == 0) b.fac[nf++] = 2, m /= 2;
-    for (int rdx : {13, 11, 7, 5, 3})
-      while (m % rdx == 0) b.fac[nf++] = rdx, m /= rdx;
+    std::vector<int> rad;
+    int c2 = 0, c3 = 0, c5 = 0;
+    while (m % 2 == 0) ++c2, m /= 2;
+    while (m % 3 == 0) ++c3, m /= 3;
+    while (m % 5 == 0) ++c5, m /= 5;
+    for (; c2 >= 4; c2 -= 4) rad.push_back(16);
+    if (c2) rad.push_back(1 << c2);
+    for (; c3 >= 2; c3 -= 2) rad.push_back(9);
+    if (c3) rad.push_back(3);
+    for (; c5 >= 1; c5 -= 1) rad.push_back(5);
+    for (int pr : {7, 11, 13})
+      while (m % pr == 0) rad.push_back(pr), m /= pr;
     if (m != 1) return fail(DSFT_ERR_INTERNAL, "P-1 not 13-smooth");
+    for (;;) {  // merge the two smallest radices while the product stays <= kMaxRadix
+      std::sort(rad.begin(), rad.end());
+      if (rad.size() < 2 || rad[0] * rad[1] > kMaxRadix) break;
+      const int merged = rad[0] * rad[1];
+      rad.erase(rad.begin(), rad.begin() + 2);
+      rad.push_back(merged);
+    }
+    std::stable_sort(rad.begin(), rad.end(), [](int x, int y) { return (x % 2 == 0) > (y % 2 == 0); });
+    for (int r : rad) {
+      if (nf >= kMaxFac) return fail(DSFT_ERR_INTERNAL, "too many FFT stages");
+      b.fac[nf++] = r;
+    }
     b.nfac = nf;
-    int nt = 64;
-    while (nt < 512 && b.M > 16 * nt) nt *= 2;
-    b.fft_threads = nt;
+    b.fft_threads = b.M <= 1024 ? 64 : (b.M <= 3072 ? 256 : 512);
   }
   // K1 tables: cos/sin(q_j u h), h = 2 pi / N, angles reduced exactly mod N
   P.k1tab.assign((size_t)J * kappa * 2, 0.0);
@@ -368,12 +398,15 @@ static dsft_status derive(int64_t N, int64_t s, const dsft_params& prm, Plan& P)
 }
 
 static dsft_status upload_tables(Plan& P) {
-  // one allocation: per t [perm_in M][perm_out M] int32, [bhat M][tw M] double2; then k1tab, ctab
+  // one allocation; per t: dlog [P] uint16 | bhat [M] | tw1 [nt1] | tw2 [64] (double2, 16-B aligned);
+  // then the K1 tables k1tab [J][kappa][2], ctab [kappa+1]
   size_t bytes = 0;
-  std::vector<size_t> offs(P.T);
+  std::vector<size_t> offs(P.T), cpx(P.T);
   for (int t = 0; t < P.T; ++t) {
+    const Bucket& b = P.bk[t];
     offs[t] = bytes;
-    bytes = align256(bytes + (size_t)P.bk[t].M * (4 + 4 + 16 + 16) + 16);
+    cpx[t] = align256(bytes + (size_t)b.P * 2);
+    bytes = align256(cpx[t] + (size_t)(b.M + b.nt1 + 64) * 16);
   }
   const size_t k1off = bytes;
   bytes = align256(bytes + (P.k1tab.size() + P.ctab.size()) * 8);
@@ -381,18 +414,15 @@ static dsft_status upload_tables(Plan& P) {
   for (int t = 0; t < P.T; ++t) {
     Bucket& b = P.bk[t];
     const int M = b.M;
-    int32_t* pin = (int32_t*)(host.data() + offs[t]);
-    int32_t* pout = pin + M;
-    // lay out: pin [M] int32, pout [M] int32, then (aligned to 16) bhat [M], tw [M]
-    const size_t cpx_off = offs[t] + (((size_t)M * 8 + 15) & ~(size_t)15);
-    double* bhat = (double*)(host.data() + cpx_off);
-    double* tw = bhat + 2 * (size_t)M;
+    uint16_t* dlog = (uint16_t*)(host.data() + offs[t]);
+    double* bhat = (double*)(host.data() + cpx[t]);
+    double* tw1 = bhat + 2 * (size_t)M;
+    double* tw2 = tw1 + 2 * (size_t)b.nt1;
     const int64_t ginv = invmod(b.g, b.P);
     int64_t gp = 1, gn = 1;
     std::vector<cld> bseq(M), bf(M);
     for (int q = 0; q < M; ++q) {
-      pin[q] = (int32_t)gp;   // g^q
-      pout[q] = (int32_t)gn;  // g^-q
+      dlog[gp] = (uint16_t)q;        // g^q = gp
       bseq[q] = unit_root(gn, b.P);  // b_m = W_P^{g^-m}
       gp = gp * b.g % b.P;
       gn = gn * ginv % b.P;
@@ -410,26 +440,30 @@ static dsft_status upload_tables(Plan& P) {
       bhat[2 * pos] = (double)(bf[c].real() / (long double)M);
       bhat[2 * pos + 1] = (double)(bf[c].imag() / (long double)M);
     }
-    for (int k = 0; k < M; ++k) {
-      const cld wv = unit_root(k, M);
-      tw[2 * k] = (double)wv.real();
-      tw[2 * k + 1] = (double)wv.imag();
+    for (int e = 0; e < b.nt1; ++e) {
+      const cld wv = unit_root((int64_t)64 * e, M);
+      tw1[2 * e] = (double)wv.real();
+      tw1[2 * e + 1] = (double)wv.imag();
+    }
+    for (int e = 0; e < 64; ++e) {
+      const cld wv = unit_root(e, M);
+      tw2[2 * e] = (double)wv.real();
+      tw2[2 * e + 1] = (double)wv.imag();
     }
   }
   memcpy(host.data() + k1off, P.k1tab.data(), P.k1tab.size() * 8);
   memcpy(host.data() + k1off + P.k1tab.size() * 8, P.ctab.data(), P.ctab.size() * 8);
   CU(cudaMalloc(&P.dev_tables, bytes), "cudaMalloc(plan tables)");
   CU(cudaMemcpy(P.dev_tables, host.data(), bytes, cudaMemcpyHostToDevice), "upload plan tables");
+  char* base = (char*)P.dev_tables;
   for (int t = 0; t < P.T; ++t) {
     Bucket& b = P.bk[t];
-    char* base = (char*)P.dev_tables;
-    b.perm_in = (int32_t*)(base + offs[t]);
-    b.perm_out = b.perm_in + b.M;
-    const size_t cpx_off = offs[t] + (((size_t)b.M * 8 + 15) & ~(size_t)15);
-    b.bhat = (double2*)(base + cpx_off);
-    b.tw = b.bhat + b.M;
+    b.dlog = (uint16_t*)(base + offs[t]);
+    b.bhat = (double2*)(base + cpx[t]);
+    b.tw1 = b.bhat + b.M;
+    b.tw2 = b.tw1 + b.nt1;
   }
-  P.k1tab_dev = (double*)((char*)P.dev_tables + k1off);
+  P.k1tab_dev = (double*)(base + k1off);
   return DSFT_OK;
 }
 
@@ -692,7 +726,7 @@ dsft_status dsft_plan_collect_times(dsft_plan* pl, double* ms_out, int64_t* laun
 
 int64_t dsft_plan_launches_per_execute(const dsft_plan* pl) {
   if (!pl) return 0;
-  return 3 * (int64_t)pl->p.T + 2;
+  return 3 * (int64_t)pl->p.T + 3;  // K1..K3 per bucket prime, K4, K5, K6
 }
 
 // -------------------------------------------------------------- parity hooks
@@ -745,6 +779,7 @@ dsft_status run_sharded_bands(dsft_plan* pl, const double2* f, int rank, int wor
   if (stt != DSFT_OK) return stt;
   const WsLayout L = ws_layout(p, p.ws_batch);
   CU(cudaMemsetAsync((char*)p.ws + L.band_n, 0, (size_t)L.bn_vec * 4, st), "zero band counts");
+  CU(cudaMemsetAsync((char*)p.ws + L.band_nz, 0, (size_t)L.bn_vec * 4, st), "zero band counts");
   if (bands.empty()) return DSFT_OK;
   return run_bands(p, f, p.N, 1, bands.data(), (int)bands.size(), st);
 }
