@@ -241,47 +241,72 @@ __device__ __forceinline__ NodeGeo node_geo(const K1Params& p, int sigma, int64_
 }
 
 // Fast path (KAPPA in {4, 6}): each warp stages the 32 windows of its nodes in
-// shared memory with coalesced 16-lane loads (one 208-B window per half-warp
-// instruction instead of 32 scattered 16-B requests), then every lane runs the
-// band mix for its own node from shared memory.
+// shared memory with coalesced half-warp loads (one 208-B window per half-warp
+// request instead of 32 scattered 16-B requests), then every lane runs the band
+// mix for its own node.  Index math is 32-bit (N < 2^31): the window start is
+// broadcast with one shuffle and only windows that wrap take the mod-N path.
 constexpr int kK1FastThreads = 128;
+
+// j' = round(kN/L) from a double estimate, corrected exactly in integers so
+// that |kN - j'L| <= L/2 (no ties: L odd, R3); returns (j', d0 = x - y_j').
+__device__ __forceinline__ NodeGeo node_geo_fast(const K1Params& p, int sigma, int n1) {
+  const int r = p.shift_r[sigma];
+  const int64_t L = p.P * (int64_t)r;
+  int64_t k = (int64_t)r * n1 + p.P * (int64_t)p.shift_n2[sigma];
+  if (k >= L) k -= L;
+  const int64_t kN = k * p.N;
+  int64_t jp = (int64_t)rint((double)kN / (double)L);
+  int64_t num0 = kN - jp * L;
+  if (2 * num0 > L) {
+    ++jp;
+    num0 -= L;
+  } else if (2 * num0 < -L) {
+    --jp;
+    num0 += L;
+  }
+  return NodeGeo{jp, (double)num0 * p.shift_scale[sigma]};
+}
 
 template <int KAPPA>
 __global__ void __launch_bounds__(kK1FastThreads) k1_gather_mix_fast(const __grid_constant__ K1Params p) {
   constexpr int W = 2 * KAPPA + 1;
   __shared__ double2 s_win[kK1FastThreads / 32][32][W];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t nodes = (int64_t)p.S * p.P;
-  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int nodes = p.S * (int)p.P;
+  const int gid = blockIdx.x * kK1FastThreads + threadIdx.x;
   const bool active = gid < nodes;
   const int v = blockIdx.y;
-  const int sigma = active ? (int)(gid / p.P) : 0;
-  const int64_t n1 = active ? gid - (int64_t)sigma * p.P : 0;
-  const NodeGeo g = active ? node_geo(p, sigma, n1) : NodeGeo{0, 0.0};
+  const int sigma = active ? gid / (int)p.P : 0;
+  const int n1 = active ? gid - sigma * (int)p.P : 0;
+  const NodeGeo g = active ? node_geo_fast(p, sigma, n1) : NodeGeo{0, 0.0};
+  const int N = (int)p.N;
+  // window start j' - kappa, or -1 - start for windows that wrap mod N
+  int st = (int)g.jp - KAPPA;
+  if (st < 0 || st + W > N) st = -1 - ((st % N) + N) % N;
   const double2* fv = p.f + (int64_t)v * p.ld;
-  const int64_t N = p.N;
-  // ---- cooperative window loads: half-warp h of instruction i loads node 2i+h.
-  // All 16 loads are issued before the first shared store (16 in flight per lane).
   {
     const int h = lane >> 4, u = lane & 15;
+    const bool lane_on = u < W;
+    const int first = (blockIdx.x * kK1FastThreads + warp * 32);
     double2 buf[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
       const int m = 2 * i + h;
-      const int64_t jpm = __shfl_sync(0xffffffffu, g.jp, m);
-      const int64_t gm = __shfl_sync(0xffffffffu, gid, m);
-      if (u < W && gm < nodes) {
-        int64_t idx = jpm - KAPPA + u;
-        if (idx < 0) idx += N;
-        else if (idx >= N) idx -= N;
+      const int stm = __shfl_sync(0xffffffffu, st, m);
+      if (lane_on && first + m < nodes) {
+        int idx;
+        if (stm >= 0) {
+          idx = stm + u;
+        } else {
+          idx = -1 - stm + u;
+          if (idx >= N) idx -= N;
+        }
         buf[i] = ld_stream(fv + idx);
       }
     }
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      const int m = 2 * i + h;
-      if (u < W) s_win[warp][m][u] = buf[i];
-    }
+    for (int i = 0; i < 16; ++i)
+      if (lane_on) s_win[warp][2 * i + h][u] = buf[i];
   }
   __syncwarp();
   if (!active) return;
@@ -315,19 +340,46 @@ __global__ void __launch_bounds__(kK1FastThreads) k1_gather_mix_fast(const __gri
   const uint64_t pol_z = l2_evict_last();
   double2* zo = p.Z + (int64_t)v * p.z_vec_stride + (int64_t)sigma * p.P + n1;
   const int64_t band_stride = (int64_t)p.S * p.P;
-  for (int j = 0; j < p.nb; ++j) {
-    double re = P0.x, im = P0.y;
+  // two bands per iteration, cos and sin parts in separate accumulators:
+  // 8 independent DFMA chains instead of 2 (the FP64 latency, not its
+  // throughput, bounded the single-chain loop)
+  const double2 step2 = cmul(step, step);
+  double2 ph1 = cmul(ph, step);
+  int j = 0;
+  for (; j + 1 < p.nb; j += 2) {
+    double rc0 = P0.x, rs0 = 0.0, ic0 = P0.y, is0 = 0.0;
+    double rc1 = P0.x, rs1 = 0.0, ic1 = P0.y, is1 = 0.0;
     const double* tb = p.tab + j * KAPPA * 2;
 #pragma unroll
     for (int u = 0; u < KAPPA; ++u) {
-      const double c = tb[2 * u], sgn = tb[2 * u + 1];
-      re = fma(A[u].x, c, re);
-      re = fma(D[u].y, sgn, re);
-      im = fma(A[u].y, c, im);
-      im = fma(-D[u].x, sgn, im);
+      const double c0 = tb[2 * u], s0 = tb[2 * u + 1];
+      const double c1 = tb[2 * KAPPA + 2 * u], s1 = tb[2 * KAPPA + 2 * u + 1];
+      rc0 = fma(A[u].x, c0, rc0);
+      rs0 = fma(D[u].y, s0, rs0);
+      ic0 = fma(A[u].y, c0, ic0);
+      is0 = fma(D[u].x, s0, is0);
+      rc1 = fma(A[u].x, c1, rc1);
+      rs1 = fma(D[u].y, s1, rs1);
+      ic1 = fma(A[u].y, c1, ic1);
+      is1 = fma(D[u].x, s1, is1);
     }
-    st_keep(zo + j * band_stride, cmul(make_double2(re, im), ph), pol_z);
-    ph = cmul(ph, step);
+    st_keep(zo + j * band_stride, cmul(make_double2(rc0 + rs0, ic0 - is0), ph), pol_z);
+    st_keep(zo + (j + 1) * band_stride, cmul(make_double2(rc1 + rs1, ic1 - is1), ph1), pol_z);
+    ph = cmul(ph, step2);
+    ph1 = cmul(ph1, step2);
+  }
+  if (j < p.nb) {
+    double rc = P0.x, rs = 0.0, ic = P0.y, is = 0.0;
+    const double* tb = p.tab + j * KAPPA * 2;
+#pragma unroll
+    for (int u = 0; u < KAPPA; ++u) {
+      const double c = tb[2 * u], sg = tb[2 * u + 1];
+      rc = fma(A[u].x, c, rc);
+      rs = fma(D[u].y, sg, rs);
+      ic = fma(A[u].y, c, ic);
+      is = fma(D[u].x, sg, is);
+    }
+    st_keep(zo + j * band_stride, cmul(make_double2(rc + rs, ic - is), ph), pol_z);
   }
 }
 
@@ -427,8 +479,8 @@ struct K2Params {
   int64_t z_vec_stride;
   int P, M, nfac, nt1;
   int fac[kMaxFac];
-  const uint16_t* dlog;  // [P]: dlog[n] = q with g^q = n (n >= 1)
-  const double2* bhat;   // FFT_M(b)/M stored in DIF output (digit-reversed) order
+  const uint16_t* dlog;  // [P] dlog[n] = q with g^q = n (n >= 1)
+  const double2* bhat;   // [M] FFT_M(b)/M in DIF output (digit-reversed) order
   const double2* tw1;    // [nt1] W_M^{64 e1}
   const double2* tw2;    // [64]  W_M^{e2}
 };
@@ -438,37 +490,34 @@ __device__ __forceinline__ double2 tw_lookup(const double2* t1, const double2* t
   return cmul(t1[e >> 6], t2[e & 63]);
 }
 
-// In-place mixed-radix FFT stages over s[0..M) (one butterfly's values live in
-// registers at a time).  DIF (span n shrinking) leaves the spectrum in digit-
-// reversed order pos(c) = sum_s c_s M/(R_1..R_s), c = c_1 + R_1(c_2 + R_2(..));
-// DIT (span growing) consumes that order and yields natural order.  Rader's
-// convolution runs DIF -> pointwise (table pre-permuted) -> DIT, so no explicit
-// digit-reversal pass is needed.  Twiddle W_n^{ck} = tw[c k M/n].
+// In-place mixed-radix FFT over s[0..M) in shared memory.  DIF stages (span n
+// shrinking) leave the spectrum in digit-reversed order; DIT stages (span
+// growing) consume it and produce natural order.  Rader's cyclic convolution is
+// DIF -> pointwise * bhat (table pre-permuted) -> DIT, where the last DIF stage
+// and the first DIT stage share their butterfly groups (span R, k = 0) and run
+// as one register-resident "turn" pass.  Twiddles: W_n^k from the smem table,
+// W_n^{ck} by recurrence (no k == 0 special case: uniform control flow).
 template <int NT, int R>
 __device__ __forceinline__ void dif_stage(double2* s, int M, int n, const double2* t1, const double2* t2) {
   const int m = n / R;
   const int nbf = M / R;
   const int tws = M / n;
+  const unsigned magic = 0xffffffffu / (unsigned)m + 1u;  // beta / m == umulhi(beta, magic) for beta*m < 2^32
   for (int beta = threadIdx.x; beta < nbf; beta += NT) {
-    const int blk = beta / m;
+    const int blk = m == 1 ? beta : (int)__umulhi((unsigned)beta, magic);
     const int k = beta - blk * m;
     const int base = blk * n + k;
     double2 v[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) v[r] = s[base + r * m];
     dft<R>(v);
+    const double2 w1 = tw_lookup(t1, t2, k * tws);
+    double2 w = w1;
     s[base] = v[0];
-    if (k == 0) {
 #pragma unroll
-      for (int c = 1; c < R; ++c) s[base + c * m] = v[c];
-    } else {
-      const double2 w1 = tw_lookup(t1, t2, k * tws);  // W_n^k; W_n^{ck} by recurrence
-      double2 w = w1;
-#pragma unroll
-      for (int c = 1; c < R; ++c) {
-        s[base + c * m] = cmul(v[c], w);
-        if (c + 1 < R) w = cmul(w, w1);
-      }
+    for (int c = 1; c < R; ++c) {
+      s[base + c * m] = cmul(v[c], w);
+      if (c + 1 < R) w = cmul(w, w1);
     }
   }
   __syncthreads();
@@ -479,23 +528,19 @@ __device__ __forceinline__ void dit_stage(double2* s, int M, int n, const double
   const int m = n / R;
   const int nbf = M / R;
   const int tws = M / n;
+  const unsigned magic = 0xffffffffu / (unsigned)m + 1u;
   for (int beta = threadIdx.x; beta < nbf; beta += NT) {
-    const int blk = beta / m;
+    const int blk = m == 1 ? beta : (int)__umulhi((unsigned)beta, magic);
     const int k = beta - blk * m;
     const int base = blk * n + k;
     double2 v[R];
+    const double2 w1 = tw_lookup(t1, t2, k * tws);
+    double2 w = w1;
     v[0] = s[base];
-    if (k == 0) {
 #pragma unroll
-      for (int r = 1; r < R; ++r) v[r] = s[base + r * m];
-    } else {
-      const double2 w1 = tw_lookup(t1, t2, k * tws);
-      double2 w = w1;
-#pragma unroll
-      for (int r = 1; r < R; ++r) {
-        v[r] = cmul(s[base + r * m], w);
-        if (r + 1 < R) w = cmul(w, w1);
-      }
+    for (int r = 1; r < R; ++r) {
+      v[r] = cmul(s[base + r * m], w);
+      if (r + 1 < R) w = cmul(w, w1);
     }
     dft<R>(v);
 #pragma unroll
@@ -504,40 +549,63 @@ __device__ __forceinline__ void dit_stage(double2* s, int M, int n, const double
   __syncthreads();
 }
 
-template <int NT, bool DIF>
-__device__ __forceinline__ void stage(double2* s, int R, int M, int n, const double2* t1, const double2* t2) {
+// last DIF stage + pointwise * bhat + conj + first DIT stage (span R, k = 0)
+template <int NT, int R>
+__device__ __forceinline__ void turn_stage(double2* s, int M, const double2* __restrict__ bhat) {
+  const int nbf = M / R;
+  for (int blk = threadIdx.x; blk < nbf; blk += NT) {
+    const int base = blk * R;
+    double2 v[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[r] = s[base + r];
+    dft<R>(v);
+#pragma unroll
+    for (int c = 0; c < R; ++c) v[c] = cconj(cmul(v[c], ldg2(bhat + base + c)));
+    dft<R>(v);
+#pragma unroll
+    for (int c = 0; c < R; ++c) s[base + c] = v[c];
+  }
+  __syncthreads();
+}
+
+#define DSFT_RADICES(X) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13) X(14) X(15) X(16)
+
+template <int NT>
+__device__ __forceinline__ void run_dif(int R, double2* s, int M, int n, const double2* t1, const double2* t2) {
   switch (R) {
-#define DSFT_STAGE(RR) \
-  case RR: DIF ? dif_stage<NT, RR>(s, M, n, t1, t2) : dit_stage<NT, RR>(s, M, n, t1, t2); break;
-    DSFT_STAGE(2) DSFT_STAGE(3) DSFT_STAGE(4) DSFT_STAGE(5) DSFT_STAGE(6) DSFT_STAGE(7) DSFT_STAGE(8)
-    DSFT_STAGE(9) DSFT_STAGE(10) DSFT_STAGE(11) DSFT_STAGE(12) DSFT_STAGE(13) DSFT_STAGE(14) DSFT_STAGE(15)
-    DSFT_STAGE(16)
-#undef DSFT_STAGE
+#define DSFT_C(RR) \
+  case RR: dif_stage<NT, RR>(s, M, n, t1, t2); break;
+    DSFT_RADICES(DSFT_C)
+#undef DSFT_C
     default: break;
   }
 }
 
 template <int NT>
-__device__ void fft_dif(double2* s, const K2Params& p, const double2* t1, const double2* t2) {
-  int n = p.M;
-  for (int i = 0; i < p.nfac; ++i) {
-    stage<NT, true>(s, p.fac[i], p.M, n, t1, t2);
-    n /= p.fac[i];
+__device__ __forceinline__ void run_dit(int R, double2* s, int M, int n, const double2* t1, const double2* t2) {
+  switch (R) {
+#define DSFT_C(RR) \
+  case RR: dit_stage<NT, RR>(s, M, n, t1, t2); break;
+    DSFT_RADICES(DSFT_C)
+#undef DSFT_C
+    default: break;
   }
 }
 
 template <int NT>
-__device__ void fft_dit(double2* s, const K2Params& p, const double2* t1, const double2* t2) {
-  int n = 1;
-  for (int i = p.nfac - 1; i >= 0; --i) {
-    n *= p.fac[i];
-    stage<NT, false>(s, p.fac[i], p.M, n, t1, t2);
+__device__ __forceinline__ void run_turn(int R, double2* s, int M, const double2* bhat) {
+  switch (R) {
+#define DSFT_C(RR) \
+  case RR: turn_stage<NT, RR>(s, M, bhat); break;
+    DSFT_RADICES(DSFT_C)
+#undef DSFT_C
+    default: break;
   }
 }
 
 // X[0] = sum x; X[g^-p] = x[0] + (a (*) b)[p], a_q = x[g^q], b_m = W_P^{g^-m}.
-// Row I/O is coalesced: x[n] lands in smem at q = dlog[n]; the output X[n] is
-// read back from p = -dlog[n] mod M.
+// Row I/O is coalesced: x[n] is scattered into smem at q = dlog[n]; X[n] is
+// gathered back from p = -dlog[n] mod M.
 template <int NT>
 __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 2) k2_prime_dft(const __grid_constant__ K2Params p) {
   extern __shared__ double2 sm[];
@@ -562,13 +630,21 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 2) k2_prime_dft(const __gr
   }
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
   __syncthreads();
-  fft_dif<NT>(sm, p, t1, t2);
-  for (int k = threadIdx.x; k < M; k += NT) sm[k] = cconj(cmul(sm[k], ldg2(p.bhat + k)));
-  __syncthreads();
-  fft_dit<NT>(sm, p, t1, t2);
-  for (int n = 1 + threadIdx.x; n < p.P; n += NT) {
-    const int d = __ldg(p.dlog + n);
-    row[n] = cadd(x0, cconj(sm[d == 0 ? 0 : M - d]));
+  const int last = p.nfac - 1;
+  int n = M;
+  for (int i = 0; i < last; ++i) {
+    run_dif<NT>(p.fac[i], sm, M, n, t1, t2);
+    n /= p.fac[i];
+  }
+  run_turn<NT>(p.fac[last], sm, M, p.bhat);
+  n = p.fac[last];
+  for (int i = last - 1; i >= 0; --i) {
+    n *= p.fac[i];
+    run_dit<NT>(p.fac[i], sm, M, n, t1, t2);
+  }
+  for (int n1 = 1 + threadIdx.x; n1 < p.P; n1 += NT) {
+    const int d = __ldg(p.dlog + n1);
+    row[n1] = cadd(x0, cconj(sm[d == 0 ? 0 : M - d]));
   }
   if (threadIdx.x == 0) {
     double2 X0 = x0;
@@ -1086,6 +1162,7 @@ cudaError_t kernels_init() {
   const int maxsm = 227 * 1024 - 1024;  // leave room for the static reduction buffer
   if ((e = cudaFuncSetAttribute(k2_prime_dft<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm))) return e;
   if ((e = cudaFuncSetAttribute(k6_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, kK6Stage * 16))) return e;
+
   if ((e = cudaFuncSetAttribute(k2_prime_dft<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm))) return e;
   if ((e = cudaFuncSetAttribute(k2_prime_dft<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm))) return e;
   done = true;

@@ -5,6 +5,7 @@
 // execute sequence K1..K6.  Independent of oracle/ (shares no code with it).
 #include <cuda_runtime.h>
 #include <math.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -350,7 +351,8 @@ static dsft_status derive(int64_t N, int64_t s, const dsft_params& prm, Plan& P)
       b.fac[nf++] = r;
     }
     b.nfac = nf;
-    b.fft_threads = b.M <= 1024 ? 64 : (b.M <= 3072 ? 256 : 512);
+    // 256 threads (2 CTAs / SM) while two CTAs' shared memory fits, else 512 (1 CTA / SM)
+    b.fft_threads = b.M <= 1024 ? 64 : ((size_t)(b.M + b.nt1 + 64) * 16 * 2 <= 226 * 1024 ? 256 : 512);
   }
   // K1 tables: cos/sin(q_j u h), h = 2 pi / N, angles reduced exactly mod N
   P.k1tab.assign((size_t)J * kappa * 2, 0.0);
@@ -398,7 +400,7 @@ static dsft_status derive(int64_t N, int64_t s, const dsft_params& prm, Plan& P)
 }
 
 static dsft_status upload_tables(Plan& P) {
-  // one allocation; per t: dlog [P] uint16 | bhat [M] | tw1 [nt1] | tw2 [64] (double2, 16-B aligned);
+  // one allocation; per t: dlog [P] uint16 | bhat [M] | tw1 [nt1] | tw2 [64] (double2);
   // then the K1 tables k1tab [J][kappa][2], ctab [kappa+1]
   size_t bytes = 0;
   std::vector<size_t> offs(P.T), cpx(P.T);
@@ -519,6 +521,7 @@ dsft_status dsft_plan_create(int64_t N, int64_t s, const dsft_params* params, ds
     delete pl;
     return cuda_fail(e, "kernels_init");
   }
+
   st = upload_tables(pl->p);
   if (st != DSFT_OK) {
     if (pl->p.dev_tables) cudaFree(pl->p.dev_tables);
