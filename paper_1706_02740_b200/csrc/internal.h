@@ -3,9 +3,11 @@
 // Data layout in HBM:
 //   f            caller's complex128 vector(s), read once per node window (K1)
 //   Z            per bucket prime t (reused across t, sized for max_t):
-//                [vec][band j][shift sigma][n1 < P_t] complex128
-//                K1 writes filtered samples, K2 turns each row into its
-//                length-P_t DFT in place (Good-Thomas column, Rader), K3 reads.
+//                [vec][band j][shift sigma][P_t] complex128, each row in Rader
+//                order: K1 writes the sample of node n1 = g^q at position q < M
+//                (M = P_t - 1) and node 0 at position M; K2 turns the row into
+//                its length-P_t DFT in place (Good-Thomas column, Rader), leaving
+//                bin a = g^-p at position p < M and bin 0 at M; K3 reads.
 //   cand_w       [vec][band][sum_t P_t] int64   omega' per bucket (or INT64_MIN)
 //   cand_v       [vec][band][sum_t P_t][Kmax] complex128, E_{t,i}[bin] of the
 //                residue argmax (written only for in-passband candidates)
@@ -48,12 +50,14 @@ struct Bucket {
   int nfac = 0;
   int fac[kMaxFac] = {};
   int fft_threads = 0;
-  int nt1 = 0;                  // M/64 + 1 coarse twiddles
+  int toff[kMaxFac] = {};       // offset of stage s's twiddle base table in tw
+  int ntw = 0;                  // entries in tw: sum over DIF stages of n_s / R_s
   // device pointers
-  uint16_t* dlog = nullptr;     // [P] discrete log base g (dlog[0] unused)
-  double2* bhat = nullptr;      // [M] FFT_M(b)/M in DIF output order, b_m = exp(-2 pi i g^-m / P)
-  double2* tw1 = nullptr;       // [nt1] exp(-2 pi i 64 e / M)
-  double2* tw2 = nullptr;       // [64]  exp(-2 pi i e / M)
+  uint16_t* dlog = nullptr;     // [P] discrete log base g (dlog[0] unused; parity hooks)
+  uint16_t* gpow = nullptr;     // [M] g^q mod P: node / bin of Rader position q
+  double2* bhat = nullptr;      // [R_last][M/R_last] FFT_M(b)/M, DIF output position blk*R_last + c stored
+                                // at c*(M/R_last) + blk; b_m = exp(-2 pi i g^-m / P)
+  double2* tw = nullptr;        // [ntw] per DIF stage s (span n_s, m_s = n_s/R_s): exp(-2 pi i k / n_s), k < m_s
 };
 
 struct Plan {

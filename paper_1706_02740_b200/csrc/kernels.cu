@@ -207,6 +207,7 @@ struct K1Params {
   int64_t z_vec_stride;  // elements per vector in Z
   int64_t P;
   int S, nb, kappa, pad_;
+  const uint16_t* gpow;      // [P-1] node n1 = g^q of Rader position q (position P-1: node 0)
   double neg_half_inv_c1sq;  // -1 / (2 c1^2)
   double inv_c1N;            // 1 / (c1 N)
   double h_over_c1sq;        // (2 pi / N) / c1^2
@@ -223,7 +224,12 @@ struct K1Params {
 
 // Node geometry shared by both K1 variants: node (sigma, n1) of bucket prime P
 // is x = -pi + 2 pi k / L, L = P r_sigma, k = (r n1 + P n2) mod L (Good's
-// mapping of the residue grid; sigma = 0 is the P-subgrid).
+// mapping of the residue grid; sigma = 0 is the P-subgrid).  Thread q of a row
+// computes node n1 = g^q (q < P-1) or n1 = 0 (q = P-1) and stores at q: the row
+// is then already in the Rader order K2 consumes.
+__device__ __forceinline__ int rader_node(const K1Params& p, int q) {
+  return q < (int)p.P - 1 ? (int)__ldg(p.gpow + q) : 0;
+}
 struct NodeGeo {
   int64_t jp;   // j' = round(kN/L)
   double d0;    // x - y_j'
@@ -277,8 +283,8 @@ __global__ void __launch_bounds__(kK1FastThreads) k1_gather_mix_fast(const __gri
   const bool active = gid < nodes;
   const int v = blockIdx.y;
   const int sigma = active ? gid / (int)p.P : 0;
-  const int n1 = active ? gid - sigma * (int)p.P : 0;
-  const NodeGeo g = active ? node_geo_fast(p, sigma, n1) : NodeGeo{0, 0.0};
+  const int q = active ? gid - sigma * (int)p.P : 0;
+  const NodeGeo g = active ? node_geo_fast(p, sigma, rader_node(p, q)) : NodeGeo{0, 0.0};
   const int N = (int)p.N;
   // window start j' - kappa, or -1 - start for windows that wrap mod N
   int st = (int)g.jp - KAPPA;
@@ -338,7 +344,7 @@ __global__ void __launch_bounds__(kK1FastThreads) k1_gather_mix_fast(const __gri
   sincos(p.qstep * d0, &sn, &cs);
   const double2 step = make_double2(cs, sn);
   const uint64_t pol_z = l2_evict_last();
-  double2* zo = p.Z + (int64_t)v * p.z_vec_stride + (int64_t)sigma * p.P + n1;
+  double2* zo = p.Z + (int64_t)v * p.z_vec_stride + (int64_t)sigma * p.P + q;
   const int64_t band_stride = (int64_t)p.S * p.P;
   // two bands per iteration, cos and sin parts in separate accumulators:
   // 8 independent DFMA chains instead of 2 (the FP64 latency, not its
@@ -394,7 +400,8 @@ __global__ void __launch_bounds__(256) k1_gather_mix(const __grid_constant__ K1P
   if (gid >= nodes) return;
   const int v = blockIdx.y;
   const int sigma = (int)(gid / p.P);
-  const int64_t n1 = gid - (int64_t)sigma * p.P;
+  const int64_t q = gid - (int64_t)sigma * p.P;
+  const int64_t n1 = rader_node(p, (int)q);
   const int64_t r = p.shift_r[sigma];
   const int64_t L = p.P * r;
   int64_t k = r * n1 + p.P * (int64_t)p.shift_n2[sigma];
@@ -451,7 +458,7 @@ __global__ void __launch_bounds__(256) k1_gather_mix(const __grid_constant__ K1P
   sincos(p.qstep * d0, &sn, &cs);
   const double2 step = make_double2(cs, sn);
 
-  double2* zo = p.Z + (int64_t)v * p.z_vec_stride + (int64_t)sigma * p.P + n1;
+  double2* zo = p.Z + (int64_t)v * p.z_vec_stride + (int64_t)sigma * p.P + q;
   const int64_t band_stride = (int64_t)p.S * p.P;
   for (int j = 0; j < p.nb; ++j) {
     double re = P0.x, im = P0.y;
@@ -474,44 +481,43 @@ __global__ void __launch_bounds__(256) k1_gather_mix(const __grid_constant__ K1P
 }
 
 // ============================================================== K2 prime_dft
+// One CTA per (band, shift) row of length P = M + 1, in Rader order (K1 wrote the
+// sample of node g^q at position q, node 0 at M).  X[0] = x0 + sum_q a_q and
+// X[g^-p] = x0 + (a (*) b)[p] with a_q = x[g^q], b_m = W_P^{g^-m}: the cyclic
+// convolution is DIF FFT_M -> pointwise * bhat -> conj -> DIT FFT_M -> conj.
+// Passes (radices R_0..R_{F-1}, plan.cpp choose_radices):
+//   DIF 0   global (L2) -> registers -> smem   (no separate load pass)
+//   DIF 1..F-2 in shared memory
+//   turn    last DIF stage, * bhat, conj, first DIT stage (span R_{F-1}, k = 0)
+//   DIT F-2..1 in shared memory
+//   DIT 0   smem -> registers -> global, + x0 (no separate store pass)
+// Twiddles: W_n^k from the stage's base table (coalesced __ldg, L1-resident),
+// W_n^{ck} by recurrence.  The output stays in Rader order (bin g^-p at p).
 struct K2Params {
   double2* Z;
   int64_t z_vec_stride;
-  int P, M, nfac, nt1;
+  int P, M, nfac, pad_;
   int fac[kMaxFac];
-  const uint16_t* dlog;  // [P] dlog[n] = q with g^q = n (n >= 1)
-  const double2* bhat;   // [M] FFT_M(b)/M in DIF output (digit-reversed) order
-  const double2* tw1;    // [nt1] W_M^{64 e1}
-  const double2* tw2;    // [64]  W_M^{e2}
+  int toff[kMaxFac];
+  const double2* bhat;   // [R_last][M/R_last] (see internal.h)
+  const double2* tw;     // per-stage twiddle base tables
 };
 
-// W_M^e from the two-level table in shared memory (e < M)
-__device__ __forceinline__ double2 tw_lookup(const double2* t1, const double2* t2, int e) {
-  return cmul(t1[e >> 6], t2[e & 63]);
-}
-
-// In-place mixed-radix FFT over s[0..M) in shared memory.  DIF stages (span n
-// shrinking) leave the spectrum in digit-reversed order; DIT stages (span
-// growing) consume it and produce natural order.  Rader's cyclic convolution is
-// DIF -> pointwise * bhat (table pre-permuted) -> DIT, where the last DIF stage
-// and the first DIT stage share their butterfly groups (span R, k = 0) and run
-// as one register-resident "turn" pass.  Twiddles: W_n^k from the smem table,
-// W_n^{ck} by recurrence (no k == 0 special case: uniform control flow).
-template <int NT, int R>
-__device__ __forceinline__ void dif_stage(double2* s, int M, int n, const double2* t1, const double2* t2) {
+template <int NT, int R, bool GSRC>
+__device__ __forceinline__ void dif_stage(const double2* __restrict__ src, double2* s, int M, int n,
+                                          const double2* __restrict__ tw) {
   const int m = n / R;
   const int nbf = M / R;
-  const int tws = M / n;
   const unsigned magic = 0xffffffffu / (unsigned)m + 1u;  // beta / m == umulhi(beta, magic) for beta*m < 2^32
   for (int beta = threadIdx.x; beta < nbf; beta += NT) {
-    const int blk = m == 1 ? beta : (int)__umulhi((unsigned)beta, magic);
+    const int blk = GSRC ? 0 : (m == 1 ? beta : (int)__umulhi((unsigned)beta, magic));
     const int k = beta - blk * m;
     const int base = blk * n + k;
+    const double2 w1 = ldg2(tw + k);
     double2 v[R];
 #pragma unroll
-    for (int r = 0; r < R; ++r) v[r] = s[base + r * m];
+    for (int r = 0; r < R; ++r) v[r] = GSRC ? __ldcg(src + base + r * m) : s[base + r * m];
     dft<R>(v);
-    const double2 w1 = tw_lookup(t1, t2, k * tws);
     double2 w = w1;
     s[base] = v[0];
 #pragma unroll
@@ -520,23 +526,23 @@ __device__ __forceinline__ void dif_stage(double2* s, int M, int n, const double
       if (c + 1 < R) w = cmul(w, w1);
     }
   }
-  __syncthreads();
 }
 
-template <int NT, int R>
-__device__ __forceinline__ void dit_stage(double2* s, int M, int n, const double2* t1, const double2* t2) {
+template <int NT, int R, bool GDST>
+__device__ __forceinline__ void dit_stage(double2* s, double2* __restrict__ dst, int M, int n,
+                                          const double2* __restrict__ tw, double2 x0) {
   const int m = n / R;
   const int nbf = M / R;
-  const int tws = M / n;
   const unsigned magic = 0xffffffffu / (unsigned)m + 1u;
+  const uint64_t pol = l2_evict_last();
   for (int beta = threadIdx.x; beta < nbf; beta += NT) {
-    const int blk = m == 1 ? beta : (int)__umulhi((unsigned)beta, magic);
+    const int blk = GDST ? 0 : (m == 1 ? beta : (int)__umulhi((unsigned)beta, magic));
     const int k = beta - blk * m;
     const int base = blk * n + k;
+    const double2 w1 = ldg2(tw + k);
     double2 v[R];
-    const double2 w1 = tw_lookup(t1, t2, k * tws);
-    double2 w = w1;
     v[0] = s[base];
+    double2 w = w1;
 #pragma unroll
     for (int r = 1; r < R; ++r) {
       v[r] = cmul(s[base + r * m], w);
@@ -544,37 +550,51 @@ __device__ __forceinline__ void dit_stage(double2* s, int M, int n, const double
     }
     dft<R>(v);
 #pragma unroll
-    for (int c = 0; c < R; ++c) s[base + c * m] = v[c];
+    for (int c = 0; c < R; ++c) {
+      if (GDST) st_keep(dst + base + c * m, cadd(x0, cconj(v[c])), pol);
+      else s[base + c * m] = v[c];
+    }
   }
-  __syncthreads();
 }
 
-// last DIF stage + pointwise * bhat + conj + first DIT stage (span R, k = 0)
+// last DIF stage + pointwise * bhat + conj + first DIT stage (span R, k = 0);
+// the DC bin A[0] (position 0) is kept for X[0] = x0 + A[0].
 template <int NT, int R>
-__device__ __forceinline__ void turn_stage(double2* s, int M, const double2* __restrict__ bhat) {
-  const int nbf = M / R;
-  for (int blk = threadIdx.x; blk < nbf; blk += NT) {
+__device__ __forceinline__ void turn_stage(double2* s, int M, const double2* __restrict__ bhat, double2* sX0) {
+  const int nblk = M / R;
+  for (int blk = threadIdx.x; blk < nblk; blk += NT) {
     const int base = blk * R;
     double2 v[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) v[r] = s[base + r];
     dft<R>(v);
+    if (blk == 0) *sX0 = v[0];
 #pragma unroll
-    for (int c = 0; c < R; ++c) v[c] = cconj(cmul(v[c], ldg2(bhat + base + c)));
+    for (int c = 0; c < R; ++c) v[c] = cconj(cmul(v[c], ldg2(bhat + c * nblk + blk)));
     dft<R>(v);
 #pragma unroll
     for (int c = 0; c < R; ++c) s[base + c] = v[c];
   }
-  __syncthreads();
 }
 
 #define DSFT_RADICES(X) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13) X(14) X(15) X(16)
 
-template <int NT>
-__device__ __forceinline__ void run_dif(int R, double2* s, int M, int n, const double2* t1, const double2* t2) {
+template <int NT, bool G>
+__device__ __forceinline__ void run_dif(int R, const double2* src, double2* s, int M, int n, const double2* tw) {
   switch (R) {
 #define DSFT_C(RR) \
-  case RR: dif_stage<NT, RR>(s, M, n, t1, t2); break;
+  case RR: dif_stage<NT, RR, G>(src, s, M, n, tw); break;
+    DSFT_RADICES(DSFT_C)
+#undef DSFT_C
+    default: break;
+  }
+}
+
+template <int NT, bool G>
+__device__ __forceinline__ void run_dit(int R, double2* s, double2* dst, int M, int n, const double2* tw, double2 x0) {
+  switch (R) {
+#define DSFT_C(RR) \
+  case RR: dit_stage<NT, RR, G>(s, dst, M, n, tw, x0); break;
     DSFT_RADICES(DSFT_C)
 #undef DSFT_C
     default: break;
@@ -582,75 +602,52 @@ __device__ __forceinline__ void run_dif(int R, double2* s, int M, int n, const d
 }
 
 template <int NT>
-__device__ __forceinline__ void run_dit(int R, double2* s, int M, int n, const double2* t1, const double2* t2) {
+__device__ __forceinline__ void run_turn(int R, double2* s, int M, const double2* bhat, double2* sX0) {
   switch (R) {
 #define DSFT_C(RR) \
-  case RR: dit_stage<NT, RR>(s, M, n, t1, t2); break;
+  case RR: turn_stage<NT, RR>(s, M, bhat, sX0); break;
     DSFT_RADICES(DSFT_C)
 #undef DSFT_C
     default: break;
   }
 }
 
-template <int NT>
-__device__ __forceinline__ void run_turn(int R, double2* s, int M, const double2* bhat) {
-  switch (R) {
-#define DSFT_C(RR) \
-  case RR: turn_stage<NT, RR>(s, M, bhat); break;
-    DSFT_RADICES(DSFT_C)
-#undef DSFT_C
-    default: break;
-  }
-}
-
-// X[0] = sum x; X[g^-p] = x[0] + (a (*) b)[p], a_q = x[g^q], b_m = W_P^{g^-m}.
-// Row I/O is coalesced: x[n] is scattered into smem at q = dlog[n]; X[n] is
-// gathered back from p = -dlog[n] mod M.
-template <int NT>
-__global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 2) k2_prime_dft(const __grid_constant__ K2Params p) {
+template <int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) k2_prime_dft(const __grid_constant__ K2Params p) {
   extern __shared__ double2 sm[];
-  __shared__ double2 red[NT / 32];
-  const int M = p.M;
-  double2* t1 = sm + M;
-  double2* t2 = t1 + p.nt1;
-  for (int i = threadIdx.x; i < p.nt1; i += NT) t1[i] = ldg2(p.tw1 + i);
-  for (int i = threadIdx.x; i < 64; i += NT) t2[i] = ldg2(p.tw2 + i);
+  __shared__ double2 sX0;
+  const int M = p.M, F = p.nfac;
   double2* row = p.Z + (int64_t)blockIdx.y * p.z_vec_stride + (int64_t)blockIdx.x * p.P;
-  const double2 x0 = row[0];
-  double2 acc = make_double2(0.0, 0.0);
-  for (int n = 1 + threadIdx.x; n < p.P; n += NT) {
-    const double2 val = row[n];
-    sm[__ldg(p.dlog + n)] = val;
-    acc = cadd(acc, val);
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
-    acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
-  }
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
-  __syncthreads();
-  const int last = p.nfac - 1;
+  const double2 x0 = __ldcg(row + M);
   int n = M;
-  for (int i = 0; i < last; ++i) {
-    run_dif<NT>(p.fac[i], sm, M, n, t1, t2);
-    n /= p.fac[i];
+  if (F >= 2) {
+    run_dif<NT, true>(p.fac[0], row, sm, M, n, p.tw + p.toff[0]);
+    n /= p.fac[0];
+  } else {
+    for (int i = threadIdx.x; i < M; i += NT) sm[i] = __ldcg(row + i);
   }
-  run_turn<NT>(p.fac[last], sm, M, p.bhat);
-  n = p.fac[last];
-  for (int i = last - 1; i >= 0; --i) {
-    n *= p.fac[i];
-    run_dit<NT>(p.fac[i], sm, M, n, t1, t2);
+  __syncthreads();
+  for (int st = 1; st < F - 1; ++st) {
+    run_dif<NT, false>(p.fac[st], sm, sm, M, n, p.tw + p.toff[st]);
+    n /= p.fac[st];
+    __syncthreads();
   }
-  for (int n1 = 1 + threadIdx.x; n1 < p.P; n1 += NT) {
-    const int d = __ldg(p.dlog + n1);
-    row[n1] = cadd(x0, cconj(sm[d == 0 ? 0 : M - d]));
+  run_turn<NT>(p.fac[F - 1], sm, M, p.bhat, &sX0);
+  __syncthreads();
+  n = p.fac[F - 1];
+  for (int st = F - 2; st >= 1; --st) {
+    n *= p.fac[st];
+    run_dit<NT, false>(p.fac[st], sm, sm, M, n, p.tw + p.toff[st], x0);
+    __syncthreads();
   }
-  if (threadIdx.x == 0) {
-    double2 X0 = x0;
-    for (int w = 0; w < NT / 32; ++w) X0 = cadd(X0, red[w]);
-    row[0] = X0;
+  if (F >= 2) {
+    n *= p.fac[0];
+    run_dit<NT, true>(p.fac[0], sm, row, M, n, p.tw + p.toff[0], x0);
+  } else {
+    const uint64_t pol = l2_evict_last();
+    for (int i = threadIdx.x; i < M; i += NT) st_keep(row + i, cadd(x0, cconj(sm[i])), pol);
   }
+  if (threadIdx.x == 0) row[M] = cadd(x0, sX0);  // X[0] = x0 + sum_q a_q
 }
 
 // ============================================================== K3 identify
@@ -665,6 +662,7 @@ struct K3Params {
   int64_t crtM;
   int64_t crtE[DSFT_MAX_K + 1];
   int64_t qfirst, qstep, halfN_up, halfN_dn, w, B_lo, B_hi;
+  const uint16_t* gpow;   // [P-1] g^q mod P (K2 left bin g^-p at Rader position p)
   int64_t* cand_w;
   double2* cand_v;
   int64_t cw_vec_stride;  // elements per vector in cand_w (nb * sumP)
@@ -702,8 +700,10 @@ __global__ void __launch_bounds__(256) k3_identify(const __grid_constant__ K3Par
   if (gid >= (int64_t)p.nb * p.P) return;
   const int v = blockIdx.y;
   const int j = (int)(gid / p.P);
-  const int64_t a = gid - (int64_t)j * p.P;
-  const double2* col = p.Z + (int64_t)v * p.z_vec_stride + (int64_t)j * p.S * p.P + a;
+  const int64_t pos = gid - (int64_t)j * p.P;  // Rader position: bucket a = g^-pos (pos < P-1), 0 (pos = P-1)
+  const int64_t Mr = p.P - 1;
+  const int64_t a = pos == Mr ? 0 : (int64_t)__ldg(p.gpow + (pos == 0 ? 0 : Mr - pos));
+  const double2* col = p.Z + (int64_t)v * p.z_vec_stride + (int64_t)j * p.S * p.P + pos;
   int64_t R = a * p.crtE[0];
   double2 yv[DSFT_MAX_K];
   for (int i = 0; i < p.K; ++i) {
@@ -1125,6 +1125,7 @@ __global__ void __launch_bounds__(kK6Threads) k6_merge(const __grid_constant__ K
 // ================================================================ debug grid
 struct DbgParams {
   const double2* Z;
+  const uint16_t* dlog;  // Rader position of node / bin n: dlog[n] (samples), -dlog[n] mod (P-1) (bins)
   int64_t P, r, L;
   int64_t rinvP, PinvR;  // r^-1 mod P, P^-1 mod r
   int S, sb, what, band;
@@ -1136,17 +1137,20 @@ __global__ void k_debug_grid(const __grid_constant__ DbgParams p) {
   if (k >= p.L) return;
   const double2* zb = p.Z + (int64_t)p.band * p.S * p.P;
   auto sig = [&](int64_t n2) -> int64_t { return n2 == 0 ? 0 : (int64_t)p.sb + n2 - 1; };
+  const int64_t Mr = p.P - 1;
   if (p.what == 0) {
     const int64_t n1 = ((k % p.P) * p.rinvP) % p.P;
     const int64_t n2 = ((k % p.r) * p.PinvR) % p.r;
-    p.out[k] = zb[sig(n2) * p.P + n1];
+    const int64_t q = n1 == 0 ? Mr : (int64_t)p.dlog[n1];
+    p.out[k] = zb[sig(n2) * p.P + q];
   } else {
     const int64_t a = k % p.P, c = k % p.r;
+    const int64_t pos = a == 0 ? Mr : (Mr - (int64_t)p.dlog[a]) % Mr;
     double2 acc = make_double2(0.0, 0.0);
     for (int64_t n2 = 0; n2 < p.r; ++n2) {
       double sn, cs;
       sincospi(-2.0 * (double)((c * n2) % p.r) / (double)p.r, &sn, &cs);
-      acc = cadd(acc, cmul(zb[sig(n2) * p.P + a], make_double2(cs, sn)));
+      acc = cadd(acc, cmul(zb[sig(n2) * p.P + pos], make_double2(cs, sn)));
     }
     p.out[k] = cscale(acc, 1.0 / (double)p.L);
   }
@@ -1160,11 +1164,11 @@ cudaError_t kernels_init() {
   if (done) return cudaSuccess;
   cudaError_t e;
   const int maxsm = 227 * 1024 - 1024;  // leave room for the static reduction buffer
-  if ((e = cudaFuncSetAttribute(k2_prime_dft<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm))) return e;
+  if ((e = cudaFuncSetAttribute(k2_prime_dft<64, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm))) return e;
   if ((e = cudaFuncSetAttribute(k6_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, kK6Stage * 16))) return e;
 
-  if ((e = cudaFuncSetAttribute(k2_prime_dft<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm))) return e;
-  if ((e = cudaFuncSetAttribute(k2_prime_dft<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm))) return e;
+  if ((e = cudaFuncSetAttribute(k2_prime_dft<256, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm))) return e;
+  if ((e = cudaFuncSetAttribute(k2_prime_dft<512, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm))) return e;
   done = true;
   return cudaSuccess;
 }
@@ -1185,6 +1189,7 @@ cudaError_t launch_k1(const Plan& p, int t, const double2* f, int64_t ld, int nv
   k.S = b.S;
   k.nb = nbands;
   k.kappa = p.kappa;
+  k.gpow = b.gpow;
   k.neg_half_inv_c1sq = -1.0 / (2.0 * p.c1 * p.c1);
   k.inv_c1N = 1.0 / (p.c1 * (double)p.N);
   const double h = 2.0 * M_PI / (double)p.N;
@@ -1227,17 +1232,17 @@ cudaError_t launch_k2(const Plan& p, int t, int nvec, void* ws, const int* /*ban
   k.P = (int)b.P;
   k.M = b.M;
   k.nfac = b.nfac;
-  for (int i = 0; i < b.nfac; ++i) k.fac[i] = b.fac[i];
-  k.dlog = b.dlog;
+  for (int i = 0; i < b.nfac; ++i) {
+    k.fac[i] = b.fac[i];
+    k.toff[i] = b.toff[i];
+  }
   k.bhat = b.bhat;
-  k.tw1 = b.tw1;
-  k.tw2 = b.tw2;
-  k.nt1 = b.nt1;
+  k.tw = b.tw;
   dim3 grid((unsigned)(nbands * b.S), nvec);
-  const size_t smem = (size_t)(b.M + b.nt1 + 64) * sizeof(double2);
-  if (b.fft_threads <= 64) k2_prime_dft<64><<<grid, 64, smem, st>>>(k);
-  else if (b.fft_threads <= 256) k2_prime_dft<256><<<grid, 256, smem, st>>>(k);
-  else k2_prime_dft<512><<<grid, 512, smem, st>>>(k);
+  const size_t smem = (size_t)b.M * sizeof(double2);
+  if (b.fft_threads <= 64) k2_prime_dft<64, 8><<<grid, 64, smem, st>>>(k);
+  else if (b.fft_threads <= 256) k2_prime_dft<256, 2><<<grid, 256, smem, st>>>(k);
+  else k2_prime_dft<512, 1><<<grid, 512, smem, st>>>(k);
   return cudaGetLastError();
 }
 
@@ -1267,6 +1272,7 @@ cudaError_t launch_k3(const Plan& p, int t, int nvec, void* ws, const int* bands
   k.w = p.w;
   k.B_lo = p.B_lo;
   k.B_hi = p.B_hi;
+  k.gpow = b.gpow;
   k.cand_w = (int64_t*)((char*)ws + L.cand_w);
   k.cand_v = (double2*)((char*)ws + L.cand_v);
   k.cw_vec_stride = L.cw_vec;
@@ -1391,6 +1397,7 @@ cudaError_t launch_debug_grid(const Plan& p, int t, int i, int band, int what, c
   const WsLayout L = ws_layout(p, p.ws_batch);
   DbgParams k{};
   k.Z = (const double2*)((const char*)ws + L.z);
+  k.dlog = b.dlog;
   k.P = b.P;
   k.r = b.r[i];
   k.L = b.P * b.r[i];

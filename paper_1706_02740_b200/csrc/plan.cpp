@@ -11,6 +11,8 @@
 #include <algorithm>
 #include <complex>
 #include <cstdio>
+#include <functional>
+#include <tuple>
 #include <string>
 #include <vector>
 
@@ -136,6 +138,50 @@ void fft_rec(const cld* x, cld* y, int64_t n, int64_t stride) {
 }
 
 size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+// K2 stage radices for an FFT of length M (DESIGN.md §6 K2): the fewest passes
+// with radices <= kMaxRadix; among those an odd last radix (the fused turn stage
+// reads R consecutive elements per thread: conflict-free in shared memory only
+// for odd R), then the largest smallest radix (balanced passes), then the
+// smallest largest radix (registers).  Order: even radices first (descending),
+// odd radices last (descending).
+bool choose_radices(int M, std::vector<int>& out) {
+  std::vector<int> cur, best;
+  auto key = [](const std::vector<int>& v) {
+    bool odd = false;
+    int mn = 1 << 30, mx = 0;
+    for (int r : v) {
+      odd |= (r & 1) != 0;
+      mn = std::min(mn, r);
+      mx = std::max(mx, r);
+    }
+    return std::make_tuple((int)v.size(), odd ? 0 : 1, -mn, mx);
+  };
+  std::function<void(int, int)> rec = [&](int m, int maxf) {
+    if (m == 1) {
+      if (best.empty() || key(cur) < key(best)) best = cur;
+      return;
+    }
+    if (!best.empty() && (int)cur.size() + 1 > (int)best.size()) return;
+    if ((int)cur.size() >= kMaxFac) return;
+    for (int d = std::min(maxf, m); d >= 2; --d)
+      if (m % d == 0) {
+        cur.push_back(d);
+        rec(m / d, d);
+        cur.pop_back();
+      }
+  };
+  if (M < 2) return false;
+  rec(M, kMaxRadix);
+  if (best.empty()) return false;
+  std::vector<int> ev, od;
+  for (int r : best) (r % 2 == 0 ? ev : od).push_back(r);
+  std::sort(ev.rbegin(), ev.rend());
+  std::sort(od.rbegin(), od.rend());
+  out = ev;
+  out.insert(out.end(), od.begin(), od.end());
+  return true;
+}
 
 }  // namespace
 
@@ -306,9 +352,8 @@ static dsft_status derive(int64_t N, int64_t s, const dsft_params& prm, Plan& P)
     P.Smax = std::max(P.Smax, S);
     // Rader setup: M = P - 1, primitive root g
     b.M = (int)(b.P - 1);
-    b.nt1 = b.M / 64 + 1;
-    if ((size_t)(b.M + b.nt1 + 64) * 16 > 226 * 1024)
-      return fail(DSFT_ERR_UNSUPPORTED, "bucket prime above ~14200 needs the multi-CTA DFT (not built yet)");
+    if ((size_t)b.M * 16 + 2048 > 227 * 1024)
+      return fail(DSFT_ERR_UNSUPPORTED, "bucket prime above ~14500 needs the multi-CTA DFT (not built yet)");
     const auto pf = prime_factors(b.M);
     int g = 2;
     for (;; ++g) {
@@ -321,38 +366,20 @@ static dsft_status derive(int64_t N, int64_t s, const dsft_params& prm, Plan& P)
       if (ok) break;
     }
     b.g = g;
-    // stage radices <= kMaxRadix (few smem passes at <= 128 registers): pack 2s,
-    // 3s, merge the smallest leftovers; radices with a factor 2 first (DIF
-    // stages with long contiguous runs), odd radices last.
-    int m = b.M, nf = 0;
     std::vector<int> rad;
-    int c2 = 0, c3 = 0, c5 = 0;
-    while (m % 2 == 0) ++c2, m /= 2;
-    while (m % 3 == 0) ++c3, m /= 3;
-    while (m % 5 == 0) ++c5, m /= 5;
-    for (; c2 >= 4; c2 -= 4) rad.push_back(16);
-    if (c2) rad.push_back(1 << c2);
-    for (; c3 >= 2; c3 -= 2) rad.push_back(9);
-    if (c3) rad.push_back(3);
-    for (; c5 >= 1; c5 -= 1) rad.push_back(5);
-    for (int pr : {7, 11, 13})
-      while (m % pr == 0) rad.push_back(pr), m /= pr;
-    if (m != 1) return fail(DSFT_ERR_INTERNAL, "P-1 not 13-smooth");
-    for (;;) {  // merge the two smallest radices while the product stays <= kMaxRadix
-      std::sort(rad.begin(), rad.end());
-      if (rad.size() < 2 || rad[0] * rad[1] > kMaxRadix) break;
-      const int merged = rad[0] * rad[1];
-      rad.erase(rad.begin(), rad.begin() + 2);
-      rad.push_back(merged);
+    if (!choose_radices(b.M, rad)) return fail(DSFT_ERR_INTERNAL, "P-1 not 13-smooth or too many FFT stages");
+    b.nfac = (int)rad.size();
+    for (int i = 0; i < b.nfac; ++i) b.fac[i] = rad[i];
+    // twiddle base tables of the DIF/DIT stages 0..F-2 (the last stage has span R, no twiddle)
+    int span = b.M, ntw = 0;
+    for (int i = 0; i + 1 < b.nfac; ++i) {
+      b.toff[i] = ntw;
+      ntw += span / b.fac[i];
+      span /= b.fac[i];
     }
-    std::stable_sort(rad.begin(), rad.end(), [](int x, int y) { return (x % 2 == 0) > (y % 2 == 0); });
-    for (int r : rad) {
-      if (nf >= kMaxFac) return fail(DSFT_ERR_INTERNAL, "too many FFT stages");
-      b.fac[nf++] = r;
-    }
-    b.nfac = nf;
-    // 256 threads (2 CTAs / SM) while two CTAs' shared memory fits, else 512 (1 CTA / SM)
-    b.fft_threads = b.M <= 1024 ? 64 : ((size_t)(b.M + b.nt1 + 64) * 16 * 2 <= 226 * 1024 ? 256 : 512);
+    b.ntw = std::max(ntw, 1);
+    // 256 threads at 2 CTAs / SM while two rows fit in shared memory, else 512 at 1 CTA / SM
+    b.fft_threads = b.M <= 1024 ? 64 : ((size_t)b.M * 16 * 2 + 4096 <= 228 * 1024 ? 256 : 512);
   }
   // K1 tables: cos/sin(q_j u h), h = 2 pi / N, angles reduced exactly mod N
   P.k1tab.assign((size_t)J * kappa * 2, 0.0);
@@ -400,15 +427,16 @@ static dsft_status derive(int64_t N, int64_t s, const dsft_params& prm, Plan& P)
 }
 
 static dsft_status upload_tables(Plan& P) {
-  // one allocation; per t: dlog [P] uint16 | bhat [M] | tw1 [nt1] | tw2 [64] (double2);
+  // one allocation; per t: dlog [P] uint16 | gpow [M] uint16 | bhat [M] | tw [ntw] (double2);
   // then the K1 tables k1tab [J][kappa][2], ctab [kappa+1]
   size_t bytes = 0;
-  std::vector<size_t> offs(P.T), cpx(P.T);
+  std::vector<size_t> offs(P.T), goff(P.T), cpx(P.T);
   for (int t = 0; t < P.T; ++t) {
     const Bucket& b = P.bk[t];
     offs[t] = bytes;
-    cpx[t] = align256(bytes + (size_t)b.P * 2);
-    bytes = align256(cpx[t] + (size_t)(b.M + b.nt1 + 64) * 16);
+    goff[t] = align256(bytes + (size_t)b.P * 2);
+    cpx[t] = align256(goff[t] + (size_t)b.M * 2);
+    bytes = align256(cpx[t] + (size_t)(b.M + b.ntw) * 16);
   }
   const size_t k1off = bytes;
   bytes = align256(bytes + (P.k1tab.size() + P.ctab.size()) * 8);
@@ -417,19 +445,21 @@ static dsft_status upload_tables(Plan& P) {
     Bucket& b = P.bk[t];
     const int M = b.M;
     uint16_t* dlog = (uint16_t*)(host.data() + offs[t]);
+    uint16_t* gpow = (uint16_t*)(host.data() + goff[t]);
     double* bhat = (double*)(host.data() + cpx[t]);
-    double* tw1 = bhat + 2 * (size_t)M;
-    double* tw2 = tw1 + 2 * (size_t)b.nt1;
+    double* tw = bhat + 2 * (size_t)M;
     const int64_t ginv = invmod(b.g, b.P);
     int64_t gp = 1, gn = 1;
     std::vector<cld> bseq(M), bf(M);
     for (int q = 0; q < M; ++q) {
       dlog[gp] = (uint16_t)q;        // g^q = gp
+      gpow[q] = (uint16_t)gp;
       bseq[q] = unit_root(gn, b.P);  // b_m = W_P^{g^-m}
       gp = gp * b.g % b.P;
       gn = gn * ginv % b.P;
     }
     fft_rec(bseq.data(), bf.data(), M, 1);
+    const int RL = b.fac[b.nfac - 1], nblk = M / RL;
     for (int c = 0; c < M; ++c) {
       // DIF output position of frequency c: pos = sum_s d_s M/(R_1..R_s), c = d_1 + R_1(d_2 + ...)
       int64_t cc = c, pos = 0, span = M;
@@ -439,18 +469,19 @@ static dsft_status upload_tables(Plan& P) {
         span /= b.fac[i];
         pos += d * span;
       }
-      bhat[2 * pos] = (double)(bf[c].real() / (long double)M);
-      bhat[2 * pos + 1] = (double)(bf[c].imag() / (long double)M);
+      const int64_t at = (pos % RL) * nblk + pos / RL;  // turn-stage layout [c][blk]
+      bhat[2 * at] = (double)(bf[c].real() / (long double)M);
+      bhat[2 * at + 1] = (double)(bf[c].imag() / (long double)M);
     }
-    for (int e = 0; e < b.nt1; ++e) {
-      const cld wv = unit_root((int64_t)64 * e, M);
-      tw1[2 * e] = (double)wv.real();
-      tw1[2 * e + 1] = (double)wv.imag();
-    }
-    for (int e = 0; e < 64; ++e) {
-      const cld wv = unit_root(e, M);
-      tw2[2 * e] = (double)wv.real();
-      tw2[2 * e + 1] = (double)wv.imag();
+    int span = M;
+    for (int i = 0; i + 1 < b.nfac; ++i) {
+      const int m = span / b.fac[i];
+      for (int k = 0; k < m; ++k) {
+        const cld wv = unit_root(k, span);
+        tw[2 * (b.toff[i] + k)] = (double)wv.real();
+        tw[2 * (b.toff[i] + k) + 1] = (double)wv.imag();
+      }
+      span = m;
     }
   }
   memcpy(host.data() + k1off, P.k1tab.data(), P.k1tab.size() * 8);
@@ -461,9 +492,9 @@ static dsft_status upload_tables(Plan& P) {
   for (int t = 0; t < P.T; ++t) {
     Bucket& b = P.bk[t];
     b.dlog = (uint16_t*)(base + offs[t]);
+    b.gpow = (uint16_t*)(base + goff[t]);
     b.bhat = (double2*)(base + cpx[t]);
-    b.tw1 = b.bhat + b.M;
-    b.tw2 = b.tw1 + b.nt1;
+    b.tw = b.bhat + b.M;
   }
   P.k1tab_dev = (double*)(base + k1off);
   return DSFT_OK;
