@@ -83,10 +83,12 @@ def lib() -> C.CDLL:
     """Load libdsft.so (built in-tree); raises if it is missing -- no fallback."""
     global _lib
     if _lib is None:
-        if not os.path.exists(LIB_PATH):
-            raise ImportError(f"{LIB_PATH} not built: run `python -m paper_1706_02740_b200.build` "
+        # DSFT_LIB: developer hook to load an instrumented build of the same ABI
+        path = os.environ.get("DSFT_LIB", LIB_PATH)
+        if not os.path.exists(path):
+            raise ImportError(f"{path} not built: run `python -m paper_1706_02740_b200.build` "
                               "(there is no CPU fallback)")
-        L = C.CDLL(LIB_PATH)
+        L = C.CDLL(path)
         for name, (res, args) in _SIGS.items():
             fn = getattr(L, name)
             fn.restype = res

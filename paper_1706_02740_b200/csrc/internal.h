@@ -49,7 +49,9 @@ struct Bucket {
   int g = 0;                 // primitive root mod P
   int nfac = 0;
   int fac[kMaxFac] = {};
-  int fft_threads = 0;
+  int fft_threads = 0;           // K2 CTA size (warps = fft_threads / 32)
+  int fft_variant = 0;           // K2 instantiation: 0 <64,8>, 1 <288,2>, 2 <512,1>
+  int fft_group = 1;             // reserved (warp-group sub-FFT layout, not used)
   int toff[kMaxFac] = {};       // offset of stage s's twiddle base table in tw
   int ntw = 0;                  // entries in tw: sum over DIF stages of n_s / R_s
   // device pointers
@@ -88,6 +90,11 @@ struct Plan {
   std::vector<cudaEvent_t> ev_pool;
   std::vector<int> ev_class;   // kernel class of pair i (0 K1, 1 K2, 2 K3, 3 K45, 4 K6)
   size_t ev_used = 0;          // pairs recorded since the last collect
+  // K1 of bucket prime t+1 runs on `aux` into the other Z buffer and K3 of prime
+  // t-1 on `aux3` while K2 of prime t runs on the caller's stream (pipe_ev:
+  // fork/join events, no timing)
+  cudaStream_t aux = nullptr, aux3 = nullptr;
+  std::vector<cudaEvent_t> pipe_ev;
 };
 
 // Workspace regions (byte offsets, 256-aligned) for `nvec` concurrent vectors,
@@ -96,6 +103,7 @@ struct WsLayout {
   size_t z, cand_w, cand_v, acc_w, acc_z, acc_r, acc_mask, acc_n, work_n, work, band_w, band_c, band_z, band_m, band_n,
       band_nz, total;
   int64_t z_vec;     // complex128 elements per vector in Z:        J * max_t S_t P_t
+  int64_t z_buf;     // elements per Z buffer (nvec * z_vec); two buffers (prime parity)
   int64_t cw_vec;    // elements per vector in cand_w / acc_w / acc_z: J * sum_t P_t
   int64_t band_vec;  // elements per vector in band_w / band_c / band_z: J * budget
   int64_t bn_vec;    // elements per vector in band_n: J
@@ -103,17 +111,17 @@ struct WsLayout {
 WsLayout ws_layout(const Plan& p, int64_t nvec);
 
 // ---- kernel launchers (kernels.cu); all stream-ordered, return cudaError_t
-cudaError_t launch_k1(const Plan& p, int t, const double2* f, int64_t ld, int nvec, void* ws,
+cudaError_t launch_k1(const Plan& p, int t, int zb, const double2* f, int64_t ld, int nvec, void* ws,
                       const int* band_list, int nbands, cudaStream_t st);
-cudaError_t launch_k2(const Plan& p, int t, int nvec, void* ws, const int* band_list, int nbands,
+cudaError_t launch_k2(const Plan& p, int t, int zb, int nvec, void* ws, const int* band_list, int nbands,
                       cudaStream_t st);
-cudaError_t launch_k3(const Plan& p, int t, int nvec, void* ws, const int* band_list, int nbands,
+cudaError_t launch_k3(const Plan& p, int t, int zb, int nvec, void* ws, const int* band_list, int nbands,
                       cudaStream_t st);
 cudaError_t launch_k45(const Plan& p, int nvec, void* ws, const int* band_list, int nbands,
                        cudaStream_t st);
 cudaError_t launch_k6(const Plan& p, int nvec, void* ws, int64_t* freqs, double2* coeffs,
                       cudaStream_t st);
-cudaError_t launch_debug_grid(const Plan& p, int t, int i, int band, int what, const void* ws,
+cudaError_t launch_debug_grid(const Plan& p, int t, int zb, int i, int band, int what, const void* ws,
                               double2* out, cudaStream_t st);
 cudaError_t kernels_init();  // one-time attribute setup (dynamic smem limits)
 cudaError_t launch_k6_blocks(const int64_t* bw, const double2* bc, const double* bm, const int32_t* bnz, int nblocks,

@@ -19,6 +19,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cmath>
 
 #include "internal.h"
 #include "radix_consts.h"
@@ -485,32 +486,35 @@ __global__ void __launch_bounds__(256) k1_gather_mix(const __grid_constant__ K1P
 // sample of node g^q at position q, node 0 at M).  X[0] = x0 + sum_q a_q and
 // X[g^-p] = x0 + (a (*) b)[p] with a_q = x[g^q], b_m = W_P^{g^-m}: the cyclic
 // convolution is DIF FFT_M -> pointwise * bhat -> conj -> DIT FFT_M -> conj.
-// Passes (radices R_0..R_{F-1}, plan.cpp choose_radices):
-//   DIF 0   global (L2) -> registers -> smem   (no separate load pass)
+// Passes (radices R_0..R_{F-1}, plan.cpp choose_k2_layout), CTA-wide:
+//   DIF 0      global (L2) -> registers -> smem (no separate load pass)
 //   DIF 1..F-2 in shared memory
-//   turn    last DIF stage, * bhat, conj, first DIT stage (span R_{F-1}, k = 0)
+//   turn       last DIF stage, * bhat, conj, first DIT stage (span R_{F-1}, k = 0)
 //   DIT F-2..1 in shared memory
-//   DIT 0   smem -> registers -> global, + x0 (no separate store pass)
+//   DIT 0      smem -> registers -> global, + x0 (no separate store pass)
 // Twiddles: W_n^k from the stage's base table (coalesced __ldg, L1-resident),
-// W_n^{ck} by recurrence.  The output stays in Rader order (bin g^-p at p).
+// W_n^{ck} by two interleaved recurrences.  The output stays in Rader order
+// (bin g^-p at position p).
 struct K2Params {
   double2* Z;
   int64_t z_vec_stride;
-  int P, M, nfac, pad_;
+  int P, M, nfac, t;     // t: bucket-prime index (trace builds only)
   int fac[kMaxFac];
   int toff[kMaxFac];
   const double2* bhat;   // [R_last][M/R_last] (see internal.h)
   const double2* tw;     // per-stage twiddle base tables
 };
 
-template <int NT, int R, bool GSRC>
-__device__ __forceinline__ void dif_stage(const double2* __restrict__ src, double2* s, int M, int n,
-                                          const double2* __restrict__ tw) {
+// DIF stage of span n over a region of `len` elements (stage 0: the row; else a
+// sub-FFT), butterflies strided over `nth` threads with index `t`.
+template <int R, bool GSRC>
+__device__ __forceinline__ void dif_stage(const double2* __restrict__ src, double2* s, int len, int n,
+                                          const double2* __restrict__ tw, int t, int nth) {
   const int m = n / R;
-  const int nbf = M / R;
+  const int nbf = len / R;
   const unsigned magic = 0xffffffffu / (unsigned)m + 1u;  // beta / m == umulhi(beta, magic) for beta*m < 2^32
-  for (int beta = threadIdx.x; beta < nbf; beta += NT) {
-    const int blk = GSRC ? 0 : (m == 1 ? beta : (int)__umulhi((unsigned)beta, magic));
+  for (int beta = t; beta < nbf; beta += nth) {
+    const int blk = (GSRC || m == nbf) ? 0 : (m == 1 ? beta : (int)__umulhi((unsigned)beta, magic));
     const int k = beta - blk * m;
     const int base = blk * n + k;
     const double2 w1 = ldg2(tw + k);
@@ -518,35 +522,49 @@ __device__ __forceinline__ void dif_stage(const double2* __restrict__ src, doubl
 #pragma unroll
     for (int r = 0; r < R; ++r) v[r] = GSRC ? __ldcg(src + base + r * m) : s[base + r * m];
     dft<R>(v);
-    double2 w = w1;
+    // W^c by two interleaved recurrences W^c = W^{c-2} W^2 (half the dependency depth)
+    const double2 w2 = cmul(w1, w1);
+    double2 wa = w1, wb = w2;
     s[base] = v[0];
 #pragma unroll
     for (int c = 1; c < R; ++c) {
-      s[base + c * m] = cmul(v[c], w);
-      if (c + 1 < R) w = cmul(w, w1);
+      if (c & 1) {
+        s[base + c * m] = cmul(v[c], wa);
+        if (c + 2 < R) wa = cmul(wa, w2);
+      } else {
+        s[base + c * m] = cmul(v[c], wb);
+        if (c + 2 < R) wb = cmul(wb, w2);
+      }
     }
   }
 }
 
-template <int NT, int R, bool GDST>
-__device__ __forceinline__ void dit_stage(double2* s, double2* __restrict__ dst, int M, int n,
-                                          const double2* __restrict__ tw, double2 x0) {
+template <int R, bool GDST>
+__device__ __forceinline__ void dit_stage(double2* s, double2* __restrict__ dst, int len, int n,
+                                          const double2* __restrict__ tw, double2 x0, int t, int nth) {
   const int m = n / R;
-  const int nbf = M / R;
+  const int nbf = len / R;
   const unsigned magic = 0xffffffffu / (unsigned)m + 1u;
   const uint64_t pol = l2_evict_last();
-  for (int beta = threadIdx.x; beta < nbf; beta += NT) {
-    const int blk = GDST ? 0 : (m == 1 ? beta : (int)__umulhi((unsigned)beta, magic));
+  for (int beta = t; beta < nbf; beta += nth) {
+    const int blk = (GDST || m == nbf) ? 0 : (m == 1 ? beta : (int)__umulhi((unsigned)beta, magic));
     const int k = beta - blk * m;
     const int base = blk * n + k;
     const double2 w1 = ldg2(tw + k);
     double2 v[R];
-    v[0] = s[base];
-    double2 w = w1;
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[r] = s[base + r * m];
+    const double2 w2 = cmul(w1, w1);
+    double2 wa = w1, wb = w2;
 #pragma unroll
     for (int r = 1; r < R; ++r) {
-      v[r] = cmul(s[base + r * m], w);
-      if (r + 1 < R) w = cmul(w, w1);
+      if (r & 1) {
+        v[r] = cmul(v[r], wa);
+        if (r + 2 < R) wa = cmul(wa, w2);
+      } else {
+        v[r] = cmul(v[r], wb);
+        if (r + 2 < R) wb = cmul(wb, w2);
+      }
     }
     dft<R>(v);
 #pragma unroll
@@ -557,20 +575,22 @@ __device__ __forceinline__ void dit_stage(double2* s, double2* __restrict__ dst,
   }
 }
 
-// last DIF stage + pointwise * bhat + conj + first DIT stage (span R, k = 0);
-// the DC bin A[0] (position 0) is kept for X[0] = x0 + A[0].
-template <int NT, int R>
-__device__ __forceinline__ void turn_stage(double2* s, int M, const double2* __restrict__ bhat, double2* sX0) {
-  const int nblk = M / R;
-  for (int blk = threadIdx.x; blk < nblk; blk += NT) {
+// last DIF stage + pointwise * bhat + conj + first DIT stage (span R, k = 0) over
+// the `len` elements of one sub-FFT whose first turn block is blk0; the DC bin
+// A[0] (row position 0) is kept for X[0] = x0 + A[0].
+template <int R>
+__device__ __forceinline__ void turn_stage(double2* s, int len, const double2* __restrict__ bhat, int blk0, int nblk,
+                                           double2* sX0, int t, int nth) {
+  const int nb = len / R;
+  for (int blk = t; blk < nb; blk += nth) {
     const int base = blk * R;
     double2 v[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) v[r] = s[base + r];
     dft<R>(v);
-    if (blk == 0) *sX0 = v[0];
+    if (sX0 != nullptr && blk == 0) *sX0 = v[0];
 #pragma unroll
-    for (int c = 0; c < R; ++c) v[c] = cconj(cmul(v[c], ldg2(bhat + c * nblk + blk)));
+    for (int c = 0; c < R; ++c) v[c] = cconj(cmul(v[c], ldg2(bhat + c * nblk + blk0 + blk)));
     dft<R>(v);
 #pragma unroll
     for (int c = 0; c < R; ++c) s[base + c] = v[c];
@@ -579,75 +599,114 @@ __device__ __forceinline__ void turn_stage(double2* s, int M, const double2* __r
 
 #define DSFT_RADICES(X) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13) X(14) X(15) X(16)
 
-template <int NT, bool G>
-__device__ __forceinline__ void run_dif(int R, const double2* src, double2* s, int M, int n, const double2* tw) {
+template <bool G>
+__device__ __forceinline__ void run_dif(int R, const double2* src, double2* s, int len, int n, const double2* tw,
+                                        int t, int nth) {
   switch (R) {
 #define DSFT_C(RR) \
-  case RR: dif_stage<NT, RR, G>(src, s, M, n, tw); break;
+  case RR: dif_stage<RR, G>(src, s, len, n, tw, t, nth); break;
     DSFT_RADICES(DSFT_C)
 #undef DSFT_C
     default: break;
   }
 }
 
-template <int NT, bool G>
-__device__ __forceinline__ void run_dit(int R, double2* s, double2* dst, int M, int n, const double2* tw, double2 x0) {
+template <bool G>
+__device__ __forceinline__ void run_dit(int R, double2* s, double2* dst, int len, int n, const double2* tw, double2 x0,
+                                        int t, int nth) {
   switch (R) {
 #define DSFT_C(RR) \
-  case RR: dit_stage<NT, RR, G>(s, dst, M, n, tw, x0); break;
+  case RR: dit_stage<RR, G>(s, dst, len, n, tw, x0, t, nth); break;
     DSFT_RADICES(DSFT_C)
 #undef DSFT_C
     default: break;
   }
 }
 
-template <int NT>
-__device__ __forceinline__ void run_turn(int R, double2* s, int M, const double2* bhat, double2* sX0) {
+__device__ __forceinline__ void run_turn(int R, double2* s, int len, const double2* bhat, int blk0, int nblk,
+                                         double2* sX0, int t, int nth) {
   switch (R) {
 #define DSFT_C(RR) \
-  case RR: turn_stage<NT, RR>(s, M, bhat, sX0); break;
+  case RR: turn_stage<RR>(s, len, bhat, blk0, nblk, sX0, t, nth); break;
     DSFT_RADICES(DSFT_C)
 #undef DSFT_C
     default: break;
   }
 }
 
-template <int NT, int MINB>
-__global__ void __launch_bounds__(NT, MINB) k2_prime_dft(const __grid_constant__ K2Params p) {
+#ifdef DSFT_K2_TRACE
+// Developer instrumentation (scripts/k2_trace.py): clock64 at every stage boundary
+// of the first kTraceCtas CTAs of the most recent K2 launch of each bucket prime.
+constexpr int kTraceCtas = 1024, kTraceSlots = 16, kTraceT = 8;
+__device__ long long g_k2trace[kTraceT][kTraceCtas][kTraceSlots];
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define K2T()                                                                                        \
+  do {                                                                                               \
+    if (threadIdx.x == 0 && blockIdx.y == 0 && blockIdx.x < kTraceCtas && p.t < kTraceT) {          \
+      if (tslot == 0) g_k2trace[p.t][blockIdx.x][kTraceSlots - 1] = (long long)globaltimer_ns();    \
+      g_k2trace[p.t][blockIdx.x][tslot] = clock64();                                                 \
+    }                                                                                                \
+    ++tslot;                                                                                         \
+  } while (0)
+#else
+#define K2T() \
+  do {        \
+  } while (0)
+#endif
+
+// register cap: 65536 / (MAXT * MINB) rounded down to a multiple of 8
+template <int MAXT, int MINB>
+__global__ void __launch_bounds__(MAXT) __maxnreg__(((65536 / (MAXT * MINB)) & ~7) > 255 ? 255 : ((65536 / (MAXT * MINB)) & ~7))
+    k2_prime_dft(const __grid_constant__ K2Params p) {
   extern __shared__ double2 sm[];
   __shared__ double2 sX0;
+  [[maybe_unused]] int tslot = 0;
+  K2T();
   const int M = p.M, F = p.nfac;
+  const int NT = blockDim.x, tid = threadIdx.x;
   double2* row = p.Z + (int64_t)blockIdx.y * p.z_vec_stride + (int64_t)blockIdx.x * p.P;
   const double2 x0 = __ldcg(row + M);
   int n = M;
   if (F >= 2) {
-    run_dif<NT, true>(p.fac[0], row, sm, M, n, p.tw + p.toff[0]);
+    run_dif<true>(p.fac[0], row, sm, M, n, p.tw + p.toff[0], tid, NT);
     n /= p.fac[0];
   } else {
-    for (int i = threadIdx.x; i < M; i += NT) sm[i] = __ldcg(row + i);
+    for (int i = tid; i < M; i += NT) sm[i] = __ldcg(row + i);
   }
   __syncthreads();
+  K2T();
   for (int st = 1; st < F - 1; ++st) {
-    run_dif<NT, false>(p.fac[st], sm, sm, M, n, p.tw + p.toff[st]);
+    run_dif<false>(p.fac[st], sm, sm, M, n, p.tw + p.toff[st], tid, NT);
     n /= p.fac[st];
     __syncthreads();
+    K2T();
   }
-  run_turn<NT>(p.fac[F - 1], sm, M, p.bhat, &sX0);
+  run_turn(p.fac[F - 1], sm, M, p.bhat, 0, M / p.fac[F - 1], &sX0, tid, NT);
   __syncthreads();
+  K2T();
   n = p.fac[F - 1];
   for (int st = F - 2; st >= 1; --st) {
     n *= p.fac[st];
-    run_dit<NT, false>(p.fac[st], sm, sm, M, n, p.tw + p.toff[st], x0);
+    run_dit<false>(p.fac[st], sm, sm, M, n, p.tw + p.toff[st], x0, tid, NT);
     __syncthreads();
+    K2T();
   }
   if (F >= 2) {
     n *= p.fac[0];
-    run_dit<NT, true>(p.fac[0], sm, row, M, n, p.tw + p.toff[0], x0);
+    run_dit<true>(p.fac[0], sm, row, M, n, p.tw + p.toff[0], x0, tid, NT);
   } else {
     const uint64_t pol = l2_evict_last();
-    for (int i = threadIdx.x; i < M; i += NT) st_keep(row + i, cadd(x0, cconj(sm[i])), pol);
+    for (int i = tid; i < M; i += NT) st_keep(row + i, cadd(x0, cconj(sm[i])), pol);
   }
-  if (threadIdx.x == 0) row[M] = cadd(x0, sX0);  // X[0] = x0 + sum_q a_q
+  if (tid == 0) row[M] = cadd(x0, sX0);  // X[0] = x0 + sum_q a_q
+#ifdef DSFT_K2_TRACE
+  __syncthreads();
+  K2T();
+#endif
 }
 
 // ============================================================== K3 identify
@@ -1175,7 +1234,7 @@ cudaError_t kernels_init() {
 
 static int64_t band_q(const Plan& p, int j) { return p.q1 + 2 * p.w * (int64_t)j; }
 
-cudaError_t launch_k1(const Plan& p, int t, const double2* f, int64_t ld, int nvec, void* ws,
+cudaError_t launch_k1(const Plan& p, int t, int zb, const double2* f, int64_t ld, int nvec, void* ws,
                       const int* bands, int nbands, cudaStream_t st) {
   const Bucket& b = p.bk[t];
   const WsLayout L = ws_layout(p, p.ws_batch);
@@ -1183,7 +1242,7 @@ cudaError_t launch_k1(const Plan& p, int t, const double2* f, int64_t ld, int nv
   k.f = f;
   k.ld = ld;
   k.N = p.N;
-  k.Z = (double2*)((char*)ws + L.z);
+  k.Z = (double2*)((char*)ws + L.z) + zb * L.z_buf;
   k.z_vec_stride = L.z_vec;
   k.P = b.P;
   k.S = b.S;
@@ -1223,15 +1282,16 @@ cudaError_t launch_k1(const Plan& p, int t, const double2* f, int64_t ld, int nv
   return cudaGetLastError();
 }
 
-cudaError_t launch_k2(const Plan& p, int t, int nvec, void* ws, const int* /*bands*/, int nbands, cudaStream_t st) {
+cudaError_t launch_k2(const Plan& p, int t, int zb, int nvec, void* ws, const int* /*bands*/, int nbands, cudaStream_t st) {
   const Bucket& b = p.bk[t];
   const WsLayout L = ws_layout(p, p.ws_batch);
   K2Params k{};
-  k.Z = (double2*)((char*)ws + L.z);
+  k.Z = (double2*)((char*)ws + L.z) + zb * L.z_buf;
   k.z_vec_stride = L.z_vec;
   k.P = (int)b.P;
   k.M = b.M;
   k.nfac = b.nfac;
+  k.t = t;
   for (int i = 0; i < b.nfac; ++i) {
     k.fac[i] = b.fac[i];
     k.toff[i] = b.toff[i];
@@ -1240,17 +1300,37 @@ cudaError_t launch_k2(const Plan& p, int t, int nvec, void* ws, const int* /*ban
   k.tw = b.tw;
   dim3 grid((unsigned)(nbands * b.S), nvec);
   const size_t smem = (size_t)b.M * sizeof(double2);
-  if (b.fft_threads <= 64) k2_prime_dft<64, 8><<<grid, 64, smem, st>>>(k);
-  else if (b.fft_threads <= 256) k2_prime_dft<256, 2><<<grid, 256, smem, st>>>(k);
-  else k2_prime_dft<512, 1><<<grid, 512, smem, st>>>(k);
+  // Shared-memory carveout: just enough for the resident rows, so the rest of
+  // the unified 256 KB stays L1 for bhat and the twiddle tables (read by every
+  // CTA on the SM).
+  auto carve = [&](const void* fn, int slot, int minb) -> cudaError_t {
+    static int last_pct[3] = {-1, -1, -1};
+    const double need = (double)minb * ((double)smem + 1024.0 + 64.0);
+    const int pct = std::min(100, (int)std::ceil(100.0 * need / (228.0 * 1024.0)));
+    if (last_pct[slot] == pct) return cudaSuccess;
+    last_pct[slot] = pct;
+    return cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+  };
+  cudaError_t e;
+  const int nt = b.fft_threads;
+  if (b.fft_variant == 0) {
+    if ((e = carve((const void*)k2_prime_dft<64, 8>, 0, 8))) return e;
+    k2_prime_dft<64, 8><<<grid, nt, smem, st>>>(k);
+  } else if (b.fft_variant == 1) {
+    if ((e = carve((const void*)k2_prime_dft<256, 2>, 1, 2))) return e;
+    k2_prime_dft<256, 2><<<grid, nt, smem, st>>>(k);
+  } else {
+    if ((e = carve((const void*)k2_prime_dft<512, 1>, 2, 1))) return e;
+    k2_prime_dft<512, 1><<<grid, nt, smem, st>>>(k);
+  }
   return cudaGetLastError();
 }
 
-cudaError_t launch_k3(const Plan& p, int t, int nvec, void* ws, const int* bands, int nbands, cudaStream_t st) {
+cudaError_t launch_k3(const Plan& p, int t, int zb, int nvec, void* ws, const int* bands, int nbands, cudaStream_t st) {
   const Bucket& b = p.bk[t];
   const WsLayout L = ws_layout(p, p.ws_batch);
   K3Params k{};
-  k.Z = (const double2*)((char*)ws + L.z);
+  k.Z = (const double2*)((char*)ws + L.z) + zb * L.z_buf;
   k.z_vec_stride = L.z_vec;
   k.P = b.P;
   k.S = b.S;
@@ -1391,12 +1471,12 @@ static int64_t modinv(int64_t a, int64_t m) {
   return 0;
 }
 
-cudaError_t launch_debug_grid(const Plan& p, int t, int i, int band, int what, const void* ws, double2* out,
+cudaError_t launch_debug_grid(const Plan& p, int t, int zb, int i, int band, int what, const void* ws, double2* out,
                               cudaStream_t st) {
   const Bucket& b = p.bk[t];
   const WsLayout L = ws_layout(p, p.ws_batch);
   DbgParams k{};
-  k.Z = (const double2*)((const char*)ws + L.z);
+  k.Z = (const double2*)((const char*)ws + L.z) + zb * L.z_buf;
   k.dlog = b.dlog;
   k.P = b.P;
   k.r = b.r[i];
@@ -1413,3 +1493,10 @@ cudaError_t launch_debug_grid(const Plan& p, int t, int i, int band, int what, c
 }
 
 }  // namespace dsft
+
+#ifdef DSFT_K2_TRACE
+extern "C" int dsft_debug_k2_trace(long long* host, size_t n) {
+  const size_t bytes = std::min(n * sizeof(long long), sizeof(dsft::g_k2trace));
+  return (int)cudaMemcpyFromSymbol(host, dsft::g_k2trace, bytes);
+}
+#endif

@@ -183,6 +183,21 @@ bool choose_radices(int M, std::vector<int>& out) {
   return true;
 }
 
+// K2 layout (DESIGN.md §6 K2): radices of choose_radices, CTA-wide stages.
+// Instantiation by shared-memory fit: <64,8> small rows, <256,2> two rows per
+// SM (8 warps, 128 registers: 4 warps per SM sub-partition), <512,1> one row per
+// SM.  (Measured alternative, round 1: the middle stages as independent
+// warp-group sub-FFTs with group barriers ran 1.2-1.4x slower per row.)
+bool choose_k2_layout(Bucket& b, std::vector<int>& rad) {
+  const int M = b.M;
+  if (!choose_radices(M, rad)) return false;
+  if (M <= 1200) b.fft_variant = 0, b.fft_threads = 64;
+  else if ((size_t)2 * ((size_t)M * 16 + 2048) <= 228 * 1024) b.fft_variant = 1, b.fft_threads = 256;
+  else b.fft_variant = 2, b.fft_threads = 512;
+  b.fft_group = 1;
+  return true;
+}
+
 }  // namespace
 
 // ======================================================================= layout
@@ -200,7 +215,8 @@ WsLayout ws_layout(const Plan& p, int64_t nvec) {
     o = align256(o + bytes);
     return at;
   };
-  L.z = take((size_t)nvec * L.z_vec * 16);
+  L.z_buf = nvec * L.z_vec;
+  L.z = take((size_t)2 * L.z_buf * 16);
   L.cand_w = take((size_t)nvec * L.cw_vec * 8);
   L.cand_v = take((size_t)nvec * L.cw_vec * p.Kmax * 16);
   L.acc_w = take((size_t)nvec * L.cw_vec * 8);
@@ -367,7 +383,7 @@ static dsft_status derive(int64_t N, int64_t s, const dsft_params& prm, Plan& P)
     }
     b.g = g;
     std::vector<int> rad;
-    if (!choose_radices(b.M, rad)) return fail(DSFT_ERR_INTERNAL, "P-1 not 13-smooth or too many FFT stages");
+    if (!choose_k2_layout(b, rad)) return fail(DSFT_ERR_INTERNAL, "P-1 not 13-smooth or too many FFT stages");
     b.nfac = (int)rad.size();
     for (int i = 0; i < b.nfac; ++i) b.fac[i] = rad[i];
     // twiddle base tables of the DIF/DIT stages 0..F-2 (the last stage has span R, no twiddle)
@@ -378,8 +394,6 @@ static dsft_status derive(int64_t N, int64_t s, const dsft_params& prm, Plan& P)
       span /= b.fac[i];
     }
     b.ntw = std::max(ntw, 1);
-    // 256 threads at 2 CTAs / SM while two rows fit in shared memory, else 512 at 1 CTA / SM
-    b.fft_threads = b.M <= 1024 ? 64 : ((size_t)b.M * 16 * 2 + 4096 <= 228 * 1024 ? 256 : 512);
   }
   // K1 tables: cos/sin(q_j u h), h = 2 pi / N, angles reduced exactly mod N
   P.k1tab.assign((size_t)J * kappa * 2, 0.0);
@@ -566,6 +580,9 @@ dsft_status dsft_plan_create(int64_t N, int64_t s, const dsft_params* params, ds
 void dsft_plan_destroy(dsft_plan* pl) {
   if (!pl) return;
   for (cudaEvent_t e : pl->p.ev_pool) cudaEventDestroy(e);
+  for (cudaEvent_t e : pl->p.pipe_ev) cudaEventDestroy(e);
+  if (pl->p.aux) cudaStreamDestroy(pl->p.aux);
+  if (pl->p.aux3) cudaStreamDestroy(pl->p.aux3);
   if (pl->p.dev_tables) cudaFree(pl->p.dev_tables);
   if (pl->p.ws_owned && pl->p.ws) cudaFree(pl->p.ws);
   if (pl->p.io_dev) cudaFree(pl->p.io_dev);
@@ -670,13 +687,55 @@ inline cudaError_t timed(Plan& p, int cls, cudaStream_t st, F&& launch) {
 }
 
 // The stream-ordered pipeline for `nv` vectors (<= ws_batch) and a band list.
+// Bucket primes alternate between two Z buffers and three streams: K1 (HBM-
+// bound window gather) on the plan's `aux` stream, K2 (FP64 / shared-memory
+// bound) on the caller's stream, K3 (latency bound) on `aux3`.  Dependencies:
+// K2(t) after K1(t); K3(t) after K2(t); K1(t+2) after K3(t) (same Z buffer);
+// K45 after every K3.  So K1(t+1) and K3(t-1) overlap K2(t).
+static dsft_status ensure_pipe(Plan& p) {
+  if (!p.aux) CU(cudaStreamCreateWithFlags(&p.aux, cudaStreamNonBlocking), "create aux stream");
+  if (!p.aux3) CU(cudaStreamCreateWithFlags(&p.aux3, cudaStreamNonBlocking), "create aux3 stream");
+  const size_t need = 3 * (size_t)p.T + 3;
+  while (p.pipe_ev.size() < need) {
+    cudaEvent_t e;
+    CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "create pipeline event");
+    p.pipe_ev.push_back(e);
+  }
+  return DSFT_OK;
+}
+
 static dsft_status run_bands(Plan& p, const double2* f, int64_t ld, int nv, const int* bands, int nb,
                              cudaStream_t st) {
+  dsft_status stt = ensure_pipe(p);
+  if (stt != DSFT_OK) return stt;
+  cudaStream_t a1 = p.aux, a3 = p.aux3;
+  cudaEvent_t* evK1 = p.pipe_ev.data();            // [T] K1(t) done (aux)
+  cudaEvent_t* evK2 = p.pipe_ev.data() + p.T;      // [T] K2(t) done (st)
+  cudaEvent_t* evK3 = p.pipe_ev.data() + 2 * p.T;  // [T] K3(t) done (aux3)
+  cudaEvent_t evFork = p.pipe_ev[3 * p.T], evJoin1 = p.pipe_ev[3 * p.T + 1], evJoin3 = p.pipe_ev[3 * p.T + 2];
+  CU(cudaEventRecord(evFork, st), "pipeline fork");
+  CU(cudaStreamWaitEvent(a1, evFork, 0), "pipeline fork wait");
+  CU(cudaStreamWaitEvent(a3, evFork, 0), "pipeline fork wait");
+  auto k1 = [&](int t) -> dsft_status {
+    if (t >= 2) CU(cudaStreamWaitEvent(a1, evK3[t - 2], 0), "K1 waits K3");
+    CU(timed(p, 0, a1, [&] { return launch_k1(p, t, t & 1, f, ld, nv, p.ws, bands, nb, a1); }), "K1 gather_mix launch");
+    CU(cudaEventRecord(evK1[t], a1), "K1 event");
+    return DSFT_OK;
+  };
+  if ((stt = k1(0)) != DSFT_OK) return stt;
   for (int t = 0; t < p.T; ++t) {
-    CU(timed(p, 0, st, [&] { return launch_k1(p, t, f, ld, nv, p.ws, bands, nb, st); }), "K1 gather_mix launch");
-    CU(timed(p, 1, st, [&] { return launch_k2(p, t, nv, p.ws, bands, nb, st); }), "K2 prime_dft launch");
-    CU(timed(p, 2, st, [&] { return launch_k3(p, t, nv, p.ws, bands, nb, st); }), "K3 identify launch");
+    if (t + 1 < p.T && (stt = k1(t + 1)) != DSFT_OK) return stt;
+    CU(cudaStreamWaitEvent(st, evK1[t], 0), "K2 waits K1");
+    CU(timed(p, 1, st, [&] { return launch_k2(p, t, t & 1, nv, p.ws, bands, nb, st); }), "K2 prime_dft launch");
+    CU(cudaEventRecord(evK2[t], st), "K2 event");
+    CU(cudaStreamWaitEvent(a3, evK2[t], 0), "K3 waits K2");
+    CU(timed(p, 2, a3, [&] { return launch_k3(p, t, t & 1, nv, p.ws, bands, nb, a3); }), "K3 identify launch");
+    CU(cudaEventRecord(evK3[t], a3), "K3 event");
   }
+  CU(cudaEventRecord(evJoin1, a1), "pipeline join");
+  CU(cudaEventRecord(evJoin3, a3), "pipeline join");
+  CU(cudaStreamWaitEvent(st, evJoin1, 0), "pipeline join wait");
+  CU(cudaStreamWaitEvent(st, evJoin3, 0), "pipeline join wait");
   CU(timed(p, 3, st, [&] { return launch_k45(p, nv, p.ws, bands, nb, st); }), "K45 vote_estimate launch");
   return DSFT_OK;
 }
@@ -774,9 +833,9 @@ dsft_status dsft_debug_grid(dsft_plan* pl, const dsft_c128* f_dev, int32_t band,
   if (stt != DSFT_OK) return stt;
   cudaStream_t st = (cudaStream_t)stream;
   int b = band;
-  CU(launch_k1(p, t, (const double2*)f_dev, p.N, 1, p.ws, &b, 1, st), "K1 launch");
-  if (what == 1) CU(launch_k2(p, t, 1, p.ws, &b, 1, st), "K2 launch");
-  CU(launch_debug_grid(p, t, i, 0, what, p.ws, (double2*)out_dev, st), "debug grid launch");
+  CU(launch_k1(p, t, 0, (const double2*)f_dev, p.N, 1, p.ws, &b, 1, st), "K1 launch");
+  if (what == 1) CU(launch_k2(p, t, 0, 1, p.ws, &b, 1, st), "K2 launch");
+  CU(launch_debug_grid(p, t, 0, i, 0, what, p.ws, (double2*)out_dev, st), "debug grid launch");
   return DSFT_OK;
 }
 
