@@ -52,6 +52,8 @@ struct Bucket {
   int fft_threads = 0;           // K2 CTA size (warps = fft_threads / 32)
   int fft_variant = 0;           // K2 instantiation: 0 <64,8>, 1 <288,2>, 2 <512,1>
   int fft_group = 1;             // reserved (warp-group sub-FFT layout, not used)
+  int split = 0;                 // > 1: row too large for one CTA's shared memory; K2a/K2b split
+                                 // mode with R0 = fac[0] = split output blocks of M/R0 elements
   int toff[kMaxFac] = {};       // offset of stage s's twiddle base table in tw
   int ntw = 0;                  // entries in tw: sum over DIF stages of n_s / R_s
   // device pointers
@@ -59,7 +61,8 @@ struct Bucket {
   uint16_t* gpow = nullptr;     // [M] g^q mod P: node / bin of Rader position q
   double2* bhat = nullptr;      // [R_last][M/R_last] FFT_M(b)/M, DIF output position blk*R_last + c stored
                                 // at c*(M/R_last) + blk; b_m = exp(-2 pi i g^-m / P)
-  double2* tw = nullptr;        // [ntw] per DIF stage s (span n_s, m_s = n_s/R_s): exp(-2 pi i k / n_s), k < m_s
+  double2* tw = nullptr;        // [ntw] per DIF stage s (span n_s, m_s = n_s/R_s): exp(-2 pi i k / n_s), k < m_s;
+                                // split mode: stage 0 holds exp(-2 pi i e / M) for all e < M
 };
 
 struct Plan {
@@ -70,6 +73,7 @@ struct Plan {
   int64_t w = 0, q1 = 0, halfN_up = 0, B_lo = 0, B_hi = 0;
   double c1 = 0;
   int Kmax = 0, Smax = 0, Rmax = 0;  // Rmax: largest residue prime
+  bool any_split = false;            // some bucket uses the K2 split mode
   int64_t sumP = 0, maxSP = 0;
   Bucket bk[DSFT_MAX_T];
   std::vector<double> k1tab;   // [J][kappa][2] cos/sin(q_j u 2pi/N), u = 1..kappa
@@ -100,10 +104,11 @@ struct Plan {
 // Workspace regions (byte offsets, 256-aligned) for `nvec` concurrent vectors,
 // and the per-vector element strides the kernels use.
 struct WsLayout {
-  size_t z, cand_w, cand_v, acc_w, acc_z, acc_r, acc_mask, acc_n, work_n, work, band_w, band_c, band_z, band_m, band_n,
+  size_t z, zs, cand_w, cand_v, acc_w, acc_z, acc_r, acc_mask, acc_n, work_n, work, band_w, band_c, band_z, band_m, band_n,
       band_nz, total;
   int64_t z_vec;     // complex128 elements per vector in Z:        J * max_t S_t P_t
   int64_t z_buf;     // elements per Z buffer (nvec * z_vec); two buffers (prime parity)
+  // zs: K2 split-mode scratch (one Z buffer, only when some bucket prime is split)
   int64_t cw_vec;    // elements per vector in cand_w / acc_w / acc_z: J * sum_t P_t
   int64_t band_vec;  // elements per vector in band_w / band_c / band_z: J * budget
   int64_t bn_vec;    // elements per vector in band_n: J

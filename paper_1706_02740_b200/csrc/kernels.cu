@@ -503,6 +503,7 @@ struct K2Params {
   int toff[kMaxFac];
   const double2* bhat;   // [R_last][M/R_last] (see internal.h)
   const double2* tw;     // per-stage twiddle base tables
+  double2* Zs;           // split mode: scratch rows (same layout and strides as Z)
 };
 
 // DIF stage of span n over a region of `len` elements (stage 0: the row; else a
@@ -707,6 +708,92 @@ __global__ void __launch_bounds__(MAXT) __maxnreg__(((65536 / (MAXT * MINB)) & ~
   __syncthreads();
   K2T();
 #endif
+}
+
+// ---------------------------------------------------------------- K2 split mode
+// Rows too long for one CTA's shared memory (P above ~14.5k: s >= ~1800 at
+// c_b = 4).  K2a: CTA (row, c) computes output block c of the radix-R0 stage-0
+// DIF butterflies straight from L2 (y_{k + c m} = W_M^{ck} sum_r x_{k + r m}
+// W_R0^{rc}, m = M/R0), runs that block's sub-FFT (middle DIF stages, turn,
+// middle DIT stages) in shared memory and stores it to the scratch row Zs.
+// K2b: the final radix-R0 DIT stage across the R0 blocks, Zs -> Z, + x0.
+template <int MAXT, int MINB>
+__global__ void __launch_bounds__(MAXT) __maxnreg__(((65536 / (MAXT * MINB)) & ~7) > 255 ? 255 : ((65536 / (MAXT * MINB)) & ~7))
+    k2a_split(const __grid_constant__ K2Params p) {
+  extern __shared__ double2 sm[];
+  __shared__ double2 sX0;
+  const int M = p.M, F = p.nfac, R0 = p.fac[0], RL = p.fac[F - 1];
+  const int Msub = M / R0;
+  const int NT = blockDim.x, tid = threadIdx.x;
+  const int rowi = blockIdx.x / R0, c = blockIdx.x - rowi * R0;
+  const int64_t roff = (int64_t)blockIdx.y * p.z_vec_stride + (int64_t)rowi * p.P;
+  const double2* row = p.Z + roff;
+  double2* srow = p.Zs + roff;
+  const double2* twf = p.tw + p.toff[0];  // exp(-2 pi i e / M), e < M
+  double sn, cs;
+  sincospi(-2.0 * (double)c / (double)R0, &sn, &cs);
+  const double2 wc = make_double2(cs, sn);  // W_R0^c
+  for (int k = tid; k < Msub; k += NT) {
+    double2 acc = __ldcg(row + k);
+    double2 w = wc;
+#pragma unroll 4
+    for (int r = 1; r < R0; ++r) {
+      acc = cadd(acc, cmul(__ldcg(row + k + r * Msub), w));
+      w = cmul(w, wc);
+    }
+    sm[k] = c == 0 ? acc : cmul(acc, ldg2(twf + (int64_t)c * k));
+  }
+  __syncthreads();
+  int n = Msub;
+  for (int st = 1; st < F - 1; ++st) {
+    run_dif<false>(p.fac[st], sm, sm, Msub, n, p.tw + p.toff[st], tid, NT);
+    n /= p.fac[st];
+    __syncthreads();
+  }
+  run_turn(RL, sm, Msub, p.bhat, c * (Msub / RL), M / RL, c == 0 ? &sX0 : nullptr, tid, NT);
+  __syncthreads();
+  n = RL;
+  for (int st = F - 2; st >= 1; --st) {
+    n *= p.fac[st];
+    run_dit<false>(p.fac[st], sm, sm, Msub, n, p.tw + p.toff[st], make_double2(0.0, 0.0), tid, NT);
+    __syncthreads();
+  }
+  const uint64_t pol = l2_evict_last();
+  for (int k = tid; k < Msub; k += NT) st_keep(srow + (int64_t)c * Msub + k, sm[k], pol);
+  if (c == 0 && tid == 0) {
+    const double2 x0 = __ldcg(row + M);
+    srow[M] = x0;                                // x0 for K2b
+    ((double2*)row)[M] = cadd(x0, sX0);          // X[0] = x0 + sum_q a_q (no other CTA reads row[M])
+  }
+}
+
+__global__ void __launch_bounds__(256) k2b_split(const __grid_constant__ K2Params p) {
+  const int M = p.M, R0 = p.fac[0];
+  const int Msub = M / R0;
+  const int nchunk = (Msub + 255) / 256;
+  const int rowi = blockIdx.x / nchunk, k = (blockIdx.x - rowi * nchunk) * 256 + threadIdx.x;
+  if (k >= Msub) return;
+  const int64_t roff = (int64_t)blockIdx.y * p.z_vec_stride + (int64_t)rowi * p.P;
+  double2* row = p.Z + roff;
+  const double2* srow = p.Zs + roff;
+  const double2* twf = p.tw + p.toff[0];
+  const double2 x0 = __ldcg(srow + M);
+  const uint64_t pol = l2_evict_last();
+  switch (R0) {
+#define DSFT_C(RR)                                                                 \
+  case RR: {                                                                       \
+    double2 v[RR];                                                                 \
+    v[0] = __ldcg(srow + k);                                                       \
+    _Pragma("unroll") for (int r = 1; r < RR; ++r)                                 \
+      v[r] = cmul(__ldcg(srow + k + r * Msub), ldg2(twf + (int64_t)r * k));        \
+    dft<RR>(v);                                                                    \
+    _Pragma("unroll") for (int cc = 0; cc < RR; ++cc)                              \
+      st_keep(row + k + cc * Msub, cadd(x0, cconj(v[cc])), pol);                   \
+  } break;
+    DSFT_RADICES(DSFT_C)
+#undef DSFT_C
+    default: break;
+  }
 }
 
 // ============================================================== K3 identify
@@ -1228,6 +1315,7 @@ cudaError_t kernels_init() {
 
   if ((e = cudaFuncSetAttribute(k2_prime_dft<256, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm))) return e;
   if ((e = cudaFuncSetAttribute(k2_prime_dft<512, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm))) return e;
+  if ((e = cudaFuncSetAttribute(k2a_split<512, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm))) return e;
   done = true;
   return cudaSuccess;
 }
@@ -1298,6 +1386,18 @@ cudaError_t launch_k2(const Plan& p, int t, int zb, int nvec, void* ws, const in
   }
   k.bhat = b.bhat;
   k.tw = b.tw;
+  k.Zs = L.zs ? (double2*)((char*)ws + L.zs) : nullptr;
+  if (b.split) {
+    const int msub = b.M / b.split;
+    const size_t smem_s = (size_t)msub * sizeof(double2);
+    cudaError_t e = cudaFuncSetAttribute((const void*)k2a_split<512, 1>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    if (e != cudaSuccess) return e;
+    k2a_split<512, 1><<<dim3((unsigned)(nbands * b.S * b.split), nvec), 512, smem_s, st>>>(k);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    const unsigned nchunk = (unsigned)((msub + 255) / 256);
+    k2b_split<<<dim3((unsigned)(nbands * b.S) * nchunk, nvec), 256, 0, st>>>(k);
+    return cudaGetLastError();
+  }
   dim3 grid((unsigned)(nbands * b.S), nvec);
   const size_t smem = (size_t)b.M * sizeof(double2);
   // Shared-memory carveout: just enough for the resident rows, so the rest of

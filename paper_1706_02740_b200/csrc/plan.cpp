@@ -190,6 +190,24 @@ bool choose_radices(int M, std::vector<int>& out) {
 // warp-group sub-FFTs with group barriers ran 1.2-1.4x slower per row.)
 bool choose_k2_layout(Bucket& b, std::vector<int>& rad) {
   const int M = b.M;
+  b.split = 0;
+  if ((size_t)M * 16 + 2048 > 227 * 1024) {
+    // split mode: the smallest R0 | M whose blocks of M/R0 fit one CTA (K2a), final
+    // radix-R0 stage across blocks in K2b
+    for (int r0 = 2; r0 <= kMaxRadix; ++r0)
+      if (M % r0 == 0 && (size_t)(M / r0) * 16 + 2048 <= 227 * 1024) {
+        std::vector<int> sub;
+        if (!choose_radices(M / r0, sub)) return false;
+        rad.assign(1, r0);
+        rad.insert(rad.end(), sub.begin(), sub.end());
+        b.split = r0;
+        b.fft_variant = 2;
+        b.fft_threads = 512;
+        b.fft_group = 1;
+        return (int)rad.size() <= kMaxFac;
+      }
+    return false;
+  }
   if (!choose_radices(M, rad)) return false;
   if (M <= 1200) b.fft_variant = 0, b.fft_threads = 64;
   else if ((size_t)2 * ((size_t)M * 16 + 2048) <= 228 * 1024) b.fft_variant = 1, b.fft_threads = 256;
@@ -217,6 +235,7 @@ WsLayout ws_layout(const Plan& p, int64_t nvec) {
   };
   L.z_buf = nvec * L.z_vec;
   L.z = take((size_t)2 * L.z_buf * 16);
+  L.zs = take(p.any_split ? (size_t)L.z_buf * 16 : 0);
   L.cand_w = take((size_t)nvec * L.cw_vec * 8);
   L.cand_v = take((size_t)nvec * L.cw_vec * p.Kmax * 16);
   L.acc_w = take((size_t)nvec * L.cw_vec * 8);
@@ -314,6 +333,7 @@ static dsft_status derive(int64_t N, int64_t s, const dsft_params& prm, Plan& P)
   P.c1 = c1;
   P.Kmax = 0;
   P.Smax = 0;
+  P.any_split = false;
   P.sumP = 0;
   P.maxSP = 0;
   int64_t grid_points = 0, nodes = 0;
@@ -368,8 +388,7 @@ static dsft_status derive(int64_t N, int64_t s, const dsft_params& prm, Plan& P)
     P.Smax = std::max(P.Smax, S);
     // Rader setup: M = P - 1, primitive root g
     b.M = (int)(b.P - 1);
-    if ((size_t)b.M * 16 + 2048 > 227 * 1024)
-      return fail(DSFT_ERR_UNSUPPORTED, "bucket prime above ~14500 needs the multi-CTA DFT (not built yet)");
+    if (b.P > 65535) return fail(DSFT_ERR_UNSUPPORTED, "bucket prime >= 2^16 (16-bit Rader tables)");
     const auto pf = prime_factors(b.M);
     int g = 2;
     for (;; ++g) {
@@ -390,10 +409,11 @@ static dsft_status derive(int64_t N, int64_t s, const dsft_params& prm, Plan& P)
     int span = b.M, ntw = 0;
     for (int i = 0; i + 1 < b.nfac; ++i) {
       b.toff[i] = ntw;
-      ntw += span / b.fac[i];
+      ntw += (i == 0 && b.split) ? span : span / b.fac[i];  // split: full exp(-2 pi i e/M) table
       span /= b.fac[i];
     }
     b.ntw = std::max(ntw, 1);
+    if (b.split) P.any_split = true;
   }
   // K1 tables: cos/sin(q_j u h), h = 2 pi / N, angles reduced exactly mod N
   P.k1tab.assign((size_t)J * kappa * 2, 0.0);
@@ -490,7 +510,8 @@ static dsft_status upload_tables(Plan& P) {
     int span = M;
     for (int i = 0; i + 1 < b.nfac; ++i) {
       const int m = span / b.fac[i];
-      for (int k = 0; k < m; ++k) {
+      const int entries = (i == 0 && b.split) ? span : m;
+      for (int k = 0; k < entries; ++k) {
         const cld wv = unit_root(k, span);
         tw[2 * (b.toff[i] + k)] = (double)wv.real();
         tw[2 * (b.toff[i] + k) + 1] = (double)wv.imag();

@@ -53,7 +53,8 @@ def assert_parity(gpu, ref, s):
 
 
 # ------------------------------------------------------------------ stage parity
-@pytest.mark.parametrize("N,s,seed", [(4096, 8, 0), (2**16, 50, 4), (6007, 16, 2)])
+@pytest.mark.parametrize("N,s,seed", [(4096, 8, 0), (2**16, 50, 4), (6007, 16, 2),
+                                      (2**21, 4000, 1)])  # last: bucket primes > 16000 -> K2 split mode
 def test_filtered_samples_and_alias_dft(N, s, seed):
     """K1 vs O2 and K1+K2 (+ the length-r fold) vs O3, element by element."""
     prm = OracleParams(seed=seed)
@@ -109,6 +110,8 @@ E2E = [
     (2**16, 50, 5, None, 0), (2**16, 50, 5, 20.0, 1),
     (2**22, 50, 1, None, 0),
     (6000011, 100, 3, 20.0, 0), (6000011, 100, 3, 0.0, 0),
+    (2**20, 2000, 2, None, 0),  # bucket primes in [8000, 16000): single-CTA and split K2 rows
+    (2**21, 4000, 2, None, 1),  # bucket primes in [16000, 32000): K2 split mode only
 ]
 
 
@@ -119,7 +122,11 @@ def test_end_to_end(N, s, cfg, snr, trial):
     plan = d.Plan(N, s, d.make_params(seed=trial))
     assert_parity(run_gpu(plan, pl.f), ref, s)
     if snr is None:
-        assert sorted(ref.freqs.tolist()) == pl.freqs.tolist()
+        found = set(ref.freqs.tolist()) & set(pl.freqs.tolist())
+        if s <= 1000:
+            assert sorted(ref.freqs.tolist()) == pl.freqs.tolist()
+        else:  # s/N = 2^-9 with 2^-8 stride buckets: collisions are possible; the paper reports rates
+            assert len(found) >= 0.99 * s
 
 
 def test_presets_and_options():
@@ -200,7 +207,7 @@ def test_sharded_world1_equals_execute():
     comm.close()
 
 
-@pytest.mark.parametrize("s", [1000])
+@pytest.mark.parametrize("s", [1000, 2000, 4000])
 def test_headline_config_full_size(s):
     """BASELINE config 2 at the bench's size and launch configuration (N = 2^26)."""
     N = 2**26
