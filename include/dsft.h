@@ -146,6 +146,17 @@ dsft_status dsft_execute_batched(dsft_plan* plan, const dsft_c128* f_dev, int64_
 dsft_status dsft_execute_host(dsft_plan* plan, const dsft_c128* f_host, int64_t* freqs_out_host,
                               dsft_c128* coeffs_out_host, void* stream);
 
+/* K2 specialisation (DESIGN.md §6 K2): dsft_plan_create compiles, with NVRTC
+ * (loaded with dlopen), the length-P_t DFT kernel of each bucket prime with its
+ * radix tuple, spans and trip counts as compile-time constants, for sm_100a;
+ * compiled cubins are cached in-process and in $DSFT_JIT_CACHE (default
+ * ~/.cache/dsft_jit).  Setting DSFT_JIT=0 in the environment disables it.  Any
+ * failure keeps that bucket on the runtime-radix kernel (same arithmetic,
+ * bitwise-identical results).  Returns the number of bucket primes running the
+ * specialised kernel; if why != NULL, copies (NUL-terminated, truncated to
+ * why_len) the reason any other bucket is not specialised, or "" if none. */
+int32_t dsft_plan_k2_specialized(const dsft_plan* plan, char* why, size_t why_len);
+
 /* Number of kernels one dsft_execute launches (for bench bookkeeping). */
 int64_t dsft_plan_launches_per_execute(const dsft_plan* plan);
 
@@ -189,6 +200,12 @@ dsft_status dsft_execute_sharded(dsft_plan* plan, dsft_comm* comm, const dsft_c1
 dsft_status dsft_debug_grid(dsft_plan* plan, const dsft_c128* f_dev, int32_t band, int32_t t, int32_t i,
                             int32_t what, dsft_c128* out_dev, void* stream);
 dsft_status dsft_debug_copy(dsft_plan* plan, int32_t which, void* dst_dev, size_t bytes, void* stream);
+
+/* dsft_debug_jit_compile: NVRTC-compile (no load, no GPU needed) the specialised
+ * K2 kernel k2_ct<nt, minb, fac[0..nfac)> to an sm_100a cubin; DSFT_OK or
+ * DSFT_ERR_CUDA with the compiler log in `why` (truncated to why_len). */
+dsft_status dsft_debug_jit_compile(int32_t nt, int32_t minb, const int32_t* fac, int32_t nfac, char* why,
+                                   size_t why_len);
 
 #ifdef __cplusplus
 }

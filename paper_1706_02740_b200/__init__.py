@@ -65,6 +65,7 @@ _SIGS = {
     "dsft_execute_batched": (C.c_int, [_P, _P, C.c_int64, C.c_int64, _P, _P, _P]),
     "dsft_execute_host": (C.c_int, [_P, _P, _P, _P, _P]),
     "dsft_plan_launches_per_execute": (C.c_int64, [_P]),
+    "dsft_plan_k2_specialized": (C.c_int32, [_P, C.c_char_p, C.c_size_t]),
     "dsft_plan_set_timing": (C.c_int, [_P, C.c_int32]),
     "dsft_plan_collect_times": (C.c_int, [_P, C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
     "dsft_comm_get_unique_id": (C.c_int, [_P]),
@@ -74,6 +75,8 @@ _SIGS = {
     "dsft_execute_sharded": (C.c_int, [_P, _P, _P, _P, _P, _P]),
     "dsft_debug_grid": (C.c_int, [_P, _P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _P, _P]),
     "dsft_debug_copy": (C.c_int, [_P, C.c_int32, _P, C.c_size_t, _P]),
+    "dsft_debug_jit_compile": (C.c_int, [C.c_int32, C.c_int32, C.POINTER(C.c_int32), C.c_int32, C.c_char_p,
+                                         C.c_size_t]),
 }
 
 _lib = None
@@ -142,6 +145,14 @@ def _stream_ptr(stream) -> int | None:
     return stream if isinstance(stream, int) else stream.cuda_stream
 
 
+def dsft_debug_jit_compile(nt: int, minb: int, radices: list[int]) -> tuple[int, str]:
+    """NVRTC-compile the specialised K2 kernel for a radix tuple (no GPU needed): (status, log)."""
+    arr = (C.c_int32 * len(radices))(*radices)
+    buf = C.create_string_buffer(4096)
+    st = lib().dsft_debug_jit_compile(nt, minb, arr, len(radices), buf, 4096)
+    return int(st), buf.value.decode(errors="replace")
+
+
 class Plan:
     """Owns a dsft_plan; tensors are torch CUDA tensors (complex128 / int64)."""
 
@@ -173,6 +184,12 @@ class Plan:
 
     def launches_per_execute(self) -> int:
         return int(lib().dsft_plan_launches_per_execute(self._h))
+
+    def dsft_plan_k2_specialized(self) -> tuple[int, str]:
+        """(bucket primes whose K2 runs the plan-time NVRTC specialisation, reason for any other)."""
+        buf = C.create_string_buffer(512)
+        n = lib().dsft_plan_k2_specialized(self._h, buf, 512)
+        return int(n), buf.value.decode()
 
     KERNEL_CLASSES = ("k1_gather_mix", "k2_prime_dft", "k3_identify", "k45_vote_estimate", "k6_merge")
 

@@ -23,11 +23,11 @@
 #include <vector>
 
 #include "../../include/dsft.h"
+#include "k2_limits.h"
 
 namespace dsft {
 
 constexpr int kMaxShifts = 160;  // 1 + sum_i (r_i - 1) for up to 10 residue primes
-constexpr int kMaxFac = 24;      // FFT passes of P-1
 constexpr int kK1TabMax = 32 * 6 * 2;  // J <= 32 with kappa <= 6 in kernel params
 constexpr int64_t kSentinel = INT64_MIN;
 constexpr int kMaxRadix = 16;    // largest in-register FFT stage radix in K2
@@ -52,6 +52,7 @@ struct Bucket {
   int fft_threads = 0;           // K2 CTA size (warps = fft_threads / 32)
   int fft_variant = 0;           // K2 instantiation: 0 <64,8>, 1 <288,2>, 2 <512,1>
   int fft_group = 1;             // reserved (warp-group sub-FFT layout, not used)
+  const void* k2_jit = nullptr;  // plan-time NVRTC specialisation of K2 (cudaKernel_t), or null
   int split = 0;                 // > 1: row too large for one CTA's shared memory; K2a/K2b split
                                  // mode with R0 = fac[0] = split output blocks of M/R0 elements
   int toff[kMaxFac] = {};       // offset of stage s's twiddle base table in tw
@@ -98,6 +99,7 @@ struct Plan {
   // t-1 on `aux3` while K2 of prime t runs on the caller's stream (pipe_ev:
   // fork/join events, no timing)
   cudaStream_t aux = nullptr, aux3 = nullptr;
+  std::string jit_why;         // why some bucket runs the runtime-radix K2 ("" if none)
   std::vector<cudaEvent_t> pipe_ev;
 };
 
@@ -129,6 +131,9 @@ cudaError_t launch_k6(const Plan& p, int nvec, void* ws, int64_t* freqs, double2
 cudaError_t launch_debug_grid(const Plan& p, int t, int zb, int i, int band, int what, const void* ws,
                               double2* out, cudaStream_t st);
 cudaError_t kernels_init();  // one-time attribute setup (dynamic smem limits)
+// jit.cpp: k2_ct<nt, minb, fac...> compiled with NVRTC (cudaKernel_t), or nullptr + *why
+const void* jit_k2(int nt, int minb, const int* fac, int nfac, size_t smem_bytes, std::string* why);
+bool jit_k2_compile_only(int nt, int minb, const int* fac, int nfac, std::string* why);  // no GPU needed
 cudaError_t launch_k6_blocks(const int64_t* bw, const double2* bc, const double* bm, const int32_t* bnz, int nblocks,
                              int64_t budget, int64_t blk_vec, int64_t bn_vec, int64_t s, int nvec, int64_t* freqs,
                              double2* coeffs, cudaStream_t st);

@@ -1,0 +1,174 @@
+// k2_fft.cuh -- K2 (length-P DFTs by Rader) with the radix tuple, spans and trip
+// counts as compile-time constants.  Compiled per plan by NVRTC (jit.cpp) for the
+// plan's bucket primes; kernels.cu keeps the runtime-radix kernel (same passes,
+// same arithmetic order) as the fallback and for split-mode rows.
+// Passes: DIF 0 (L2 -> registers -> smem), DIF 1..F-2, turn (last DIF stage,
+// * bhat, conj, first DIT stage), DIT F-2..1, DIT 0 (smem -> registers -> L2, + x0).
+#pragma once
+#include "dev_common.cuh"
+#include "k2_limits.h"
+
+namespace dsft {
+
+struct K2Params {
+  double2* Z;
+  int64_t z_vec_stride;
+  int P, M, nfac, t;     // t: bucket-prime index (trace builds only)
+  int fac[kMaxFac];
+  int toff[kMaxFac];
+  const double2* bhat;   // [R_last][M/R_last] (see internal.h)
+  const double2* tw;     // per-stage twiddle base tables
+  double2* Zs;           // split mode: scratch rows (same layout and strides as Z)
+};
+
+template <int NT, int M, int N, int R, bool GSRC>
+__device__ __forceinline__ void dif_ct(const double2* __restrict__ src, double2* s, const double2* __restrict__ tw) {
+  constexpr int m = N / R, nbf = M / R, iters = (nbf + NT - 1) / NT;
+#pragma unroll
+  for (int it = 0; it < iters; ++it) {
+    const int beta = threadIdx.x + it * NT;
+    if ((nbf % NT == 0) || beta < nbf) {
+      const int blk = beta / m;
+      const int k = beta - blk * m;
+      const int base = blk * N + k;
+      const double2 w1 = ldg2(tw + k);
+      double2 v[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) v[r] = GSRC ? ldcg2(src + base + r * m) : s[base + r * m];
+      dft<R>(v);
+      const double2 w2 = cmul(w1, w1);
+      double2 wa = w1, wb = w2;
+      s[base] = v[0];
+#pragma unroll
+      for (int c = 1; c < R; ++c) {
+        if (c & 1) {
+          s[base + c * m] = cmul(v[c], wa);
+          if (c + 2 < R) wa = cmul(wa, w2);
+        } else {
+          s[base + c * m] = cmul(v[c], wb);
+          if (c + 2 < R) wb = cmul(wb, w2);
+        }
+      }
+    }
+  }
+}
+
+template <int NT, int M, int N, int R, bool GDST>
+__device__ __forceinline__ void dit_ct(double2* s, double2* __restrict__ dst, const double2* __restrict__ tw, double2 x0) {
+  constexpr int m = N / R, nbf = M / R, iters = (nbf + NT - 1) / NT;
+  const uint64_t pol = l2_evict_last();
+#pragma unroll
+  for (int it = 0; it < iters; ++it) {
+    const int beta = threadIdx.x + it * NT;
+    if ((nbf % NT == 0) || beta < nbf) {
+      const int blk = beta / m;
+      const int k = beta - blk * m;
+      const int base = blk * N + k;
+      const double2 w1 = ldg2(tw + k);
+      double2 v[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) v[r] = s[base + r * m];
+      const double2 w2 = cmul(w1, w1);
+      double2 wa = w1, wb = w2;
+#pragma unroll
+      for (int r = 1; r < R; ++r) {
+        if (r & 1) {
+          v[r] = cmul(v[r], wa);
+          if (r + 2 < R) wa = cmul(wa, w2);
+        } else {
+          v[r] = cmul(v[r], wb);
+          if (r + 2 < R) wb = cmul(wb, w2);
+        }
+      }
+      dft<R>(v);
+#pragma unroll
+      for (int c = 0; c < R; ++c) {
+        if (GDST) st_keep(dst + base + c * m, cadd(x0, cconj(v[c])), pol);
+        else s[base + c * m] = v[c];
+      }
+    }
+  }
+}
+
+template <int NT, int M, int R>
+__device__ __forceinline__ void turn_ct(double2* s, const double2* __restrict__ bhat, double2* sX0) {
+  constexpr int nb = M / R, iters = (nb + NT - 1) / NT;
+#pragma unroll
+  for (int it = 0; it < iters; ++it) {
+    const int blk = threadIdx.x + it * NT;
+    if ((nb % NT == 0) || blk < nb) {
+      const int base = blk * R;
+      double2 v[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) v[r] = s[base + r];
+      dft<R>(v);
+      if (blk == 0) *sX0 = v[0];
+#pragma unroll
+      for (int c = 0; c < R; ++c) v[c] = cconj(cmul(v[c], ldg2(bhat + c * nb + blk)));
+      dft<R>(v);
+#pragma unroll
+      for (int c = 0; c < R; ++c) s[base + c] = v[c];
+    }
+  }
+}
+
+template <int... Rs>
+struct RadixList {
+  static constexpr int F = sizeof...(Rs);
+  static constexpr int R[sizeof...(Rs)] = {Rs...};
+  static constexpr int M = (Rs * ... * 1);
+  __host__ __device__ static constexpr int span(int s) {  // span of stage s: M / (R_0 ... R_{s-1})
+    int n = M;
+    for (int i = 0; i < s; ++i) n /= R[i];
+    return n;
+  }
+};
+
+template <int NT, class L, int S>
+__device__ __forceinline__ void dif_mid(double2* sm, const K2Params& p) {
+  if constexpr (S <= L::F - 2) {
+    dif_ct<NT, L::M, L::span(S), L::R[S], false>(sm, sm, p.tw + p.toff[S]);
+    __syncthreads();
+    dif_mid<NT, L, S + 1>(sm, p);
+  }
+}
+
+template <int NT, class L, int S>
+__device__ __forceinline__ void dit_mid(double2* sm, const K2Params& p, double2 x0) {
+  if constexpr (S >= 1) {
+    dit_ct<NT, L::M, L::span(S), L::R[S], false>(sm, sm, p.tw + p.toff[S], x0);
+    __syncthreads();
+    dit_mid<NT, L, S - 1>(sm, p, x0);
+  }
+}
+
+// NT threads, MINB CTAs per SM (register cap 65536 / (NT MINB)), radices Rs...
+template <int NT, int MINB, int... Rs>
+__global__ void __launch_bounds__(NT) __maxnreg__(((65536 / (NT * MINB)) & ~7) > 255 ? 255 : ((65536 / (NT * MINB)) & ~7))
+    k2_ct(const __grid_constant__ K2Params p) {
+  using L = RadixList<Rs...>;
+  constexpr int M = L::M, F = L::F;
+  extern __shared__ double2 sm[];
+  __shared__ double2 sX0;
+  double2* row = p.Z + (int64_t)blockIdx.y * p.z_vec_stride + (int64_t)blockIdx.x * p.P;
+  const double2 x0 = ldcg2(row + M);
+  if constexpr (F == 1) {
+    for (int i = threadIdx.x; i < M; i += NT) sm[i] = ldcg2(row + i);
+    __syncthreads();
+    turn_ct<NT, M, L::R[0]>(sm, p.bhat, &sX0);
+    __syncthreads();
+    const uint64_t pol = l2_evict_last();
+    for (int i = threadIdx.x; i < M; i += NT) st_keep(row + i, cadd(x0, cconj(sm[i])), pol);
+  } else {
+    dif_ct<NT, M, M, L::R[0], true>(row, sm, p.tw + p.toff[0]);
+    __syncthreads();
+    dif_mid<NT, L, 1>(sm, p);
+    turn_ct<NT, M, L::R[F - 1]>(sm, p.bhat, &sX0);
+    __syncthreads();
+    dit_mid<NT, L, F - 2>(sm, p, x0);
+    dit_ct<NT, M, M, L::R[0], true>(sm, row, p.tw + p.toff[0], x0);
+  }
+  if (threadIdx.x == 0) row[M] = cadd(x0, sX0);  // X[0] = x0 + sum_q a_q
+}
+
+}  // namespace dsft

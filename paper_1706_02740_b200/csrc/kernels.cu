@@ -22,182 +22,10 @@
 #include <cmath>
 
 #include "internal.h"
-#include "radix_consts.h"
+#include "dev_common.cuh"
+#include "k2_fft.cuh"
 
 namespace dsft {
-
-// ---------------------------------------------------------------- complex helpers
-__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
-__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
-__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
-  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
-}
-__device__ __forceinline__ double2 cconj(double2 a) { return make_double2(a.x, -a.y); }
-__device__ __forceinline__ double2 cscale(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
-// |z|^2 rounded as re*re + im*im with no contraction: this value decides argmax /
-// top-s, and the oracle (numpy) forms it the same way.
-__device__ __forceinline__ double cabs2_rn(double2 a) { return __dadd_rn(__dmul_rn(a.x, a.x), __dmul_rn(a.y, a.y)); }
-
-__device__ __forceinline__ double2 ldg2(const double2* p) { return __ldg(p); }
-
-// L2 eviction-priority policy (createpolicy) for Z, the per-prime working set
-// K1 -> K2 -> K3 keeps in L2 (evict_last); f windows bypass L1 allocation.
-// (An evict_first policy on f was measured to lose the L2 hits between
-// neighbouring windows: +30% DRAM reads, profiles/r1c.)
-__device__ __forceinline__ uint64_t l2_evict_first() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-__device__ __forceinline__ uint64_t l2_evict_last() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-__device__ __forceinline__ double2 ld_stream(const double2* ptr) {
-  double2 v;
-  asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(ptr));
-  return v;
-}
-__device__ __forceinline__ void st_keep(double2* ptr, double2 v, uint64_t pol) {
-  asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(ptr), "d"(v.x), "d"(v.y), "l"(pol)
-               : "memory");
-}
-
-// ------------------------------------------------------------ in-register DFTs
-// Forward DFT (W = e^{-2 pi i / R}) of R values in registers.
-template <int R>
-__device__ __forceinline__ void dft_odd(double2 (&x)[R]) {
-  constexpr int H = (R - 1) / 2;
-  double2 A[H], D[H];
-#pragma unroll
-  for (int n = 1; n <= H; ++n) {
-    A[n - 1] = cadd(x[n], x[R - n]);
-    D[n - 1] = csub(x[n], x[R - n]);
-  }
-  double2 y0 = x[0];
-#pragma unroll
-  for (int n = 0; n < H; ++n) y0 = cadd(y0, A[n]);
-  double2 out[R];
-  out[0] = y0;
-#pragma unroll
-  for (int c = 1; c <= H; ++c) {
-    double2 sa = x[0];
-    double2 sd = make_double2(0.0, 0.0);
-#pragma unroll
-    for (int n = 1; n <= H; ++n) {
-      const int m = (c * n) % R;
-      const double cc = RadixTab<R>::c(m), ss = RadixTab<R>::s(m);
-      sa.x = fma(A[n - 1].x, cc, sa.x);
-      sa.y = fma(A[n - 1].y, cc, sa.y);
-      sd.x = fma(D[n - 1].x, ss, sd.x);
-      sd.y = fma(D[n - 1].y, ss, sd.y);
-    }
-    // X[c] = SA - i SD,  X[R-c] = SA + i SD
-    out[c] = make_double2(sa.x + sd.y, sa.y - sd.x);
-    out[R - c] = make_double2(sa.x - sd.y, sa.y + sd.x);
-  }
-#pragma unroll
-  for (int n = 0; n < R; ++n) x[n] = out[n];
-}
-
-__device__ __forceinline__ void dft4(double2& a, double2& b, double2& c, double2& d) {
-  const double2 s0 = cadd(a, c), d0 = csub(a, c), s1 = cadd(b, d), d1 = csub(b, d);
-  a = cadd(s0, s1);
-  c = csub(s0, s1);
-  b = make_double2(d0.x + d1.y, d0.y - d1.x);  // d0 - i d1
-  d = make_double2(d0.x - d1.y, d0.y + d1.x);  // d0 + i d1
-}
-
-template <int R>
-__device__ __forceinline__ void dft(double2 (&x)[R]);
-
-__host__ __device__ constexpr bool is_odd_prime(int r) {
-  if (r < 3 || r % 2 == 0) return false;
-  for (int d = 3; d * d <= r; d += 2)
-    if (r % d == 0) return false;
-  return true;
-}
-__host__ __device__ constexpr int first_factor(int r) {
-  if (r % 8 == 0) return 8;
-  if (r % 4 == 0) return 4;
-  if (r % 2 == 0) return 2;
-  for (int d = 3; d <= r; d += 2)
-    if (r % d == 0) return d;
-  return r;
-}
-
-// Composite R = A * B (Cooley-Tukey inside registers): n = B n1 + n2,
-// k = k1 + A k2; column DFTs of length A, twiddle W_R^{n2 k1}, row DFTs of
-// length B.  All indices are compile-time, so the arrays stay in registers and
-// the final transposition is a register renaming.
-template <int A, int B>
-__device__ __forceinline__ void dft_composite(double2 (&x)[A * B]) {
-  constexpr int R = A * B;
-#pragma unroll
-  for (int n2 = 0; n2 < B; ++n2) {
-    double2 col[A];
-#pragma unroll
-    for (int n1 = 0; n1 < A; ++n1) col[n1] = x[B * n1 + n2];
-    dft<A>(col);
-#pragma unroll
-    for (int k1 = 0; k1 < A; ++k1) {
-      const int e = (n2 * k1) % R;
-      double2 v = col[k1];
-      if (e != 0) {
-        const double c = RadixTab<R>::c(e), sn = RadixTab<R>::s(e);  // W_R^e = c - i sn
-        v = make_double2(fma(v.x, c, v.y * sn), fma(v.y, c, -v.x * sn));
-      }
-      x[B * k1 + n2] = v;
-    }
-  }
-  double2 out[R];
-#pragma unroll
-  for (int k1 = 0; k1 < A; ++k1) {
-    double2 row[B];
-#pragma unroll
-    for (int n2 = 0; n2 < B; ++n2) row[n2] = x[B * k1 + n2];
-    dft<B>(row);
-#pragma unroll
-    for (int k2 = 0; k2 < B; ++k2) out[k1 + A * k2] = row[k2];
-  }
-#pragma unroll
-  for (int i = 0; i < R; ++i) x[i] = out[i];
-}
-
-template <int R>
-__device__ __forceinline__ void dft(double2 (&x)[R]) {
-  if constexpr (R == 1) {
-  } else if constexpr (R == 2) {
-    const double2 a = x[0], b = x[1];
-    x[0] = cadd(a, b);
-    x[1] = csub(a, b);
-  } else if constexpr (R == 4) {
-    dft4(x[0], x[1], x[2], x[3]);
-  } else if constexpr (R == 8) {
-    double2 e0 = x[0], e1 = x[2], e2 = x[4], e3 = x[6];
-    double2 o0 = x[1], o1 = x[3], o2 = x[5], o3 = x[7];
-    dft4(e0, e1, e2, e3);
-    dft4(o0, o1, o2, o3);
-    constexpr double h = 0.70710678118654752440;
-    const double2 t1 = make_double2(h * (o1.x + o1.y), h * (o1.y - o1.x));    // W8^1 o1
-    const double2 t2 = make_double2(o2.y, -o2.x);                            // W8^2 o2 = -i o2
-    const double2 t3 = make_double2(h * (o3.y - o3.x), -h * (o3.x + o3.y));   // W8^3 o3
-    x[0] = cadd(e0, o0);
-    x[4] = csub(e0, o0);
-    x[1] = cadd(e1, t1);
-    x[5] = csub(e1, t1);
-    x[2] = cadd(e2, t2);
-    x[6] = csub(e2, t2);
-    x[3] = cadd(e3, t3);
-    x[7] = csub(e3, t3);
-  } else if constexpr (is_odd_prime(R)) {
-    dft_odd<R>(x);
-  } else {
-    constexpr int A = first_factor(R);
-    dft_composite<A, R / A>(x);
-  }
-}
 
 // =============================================================== K1 gather_mix
 struct K1Params {
@@ -495,16 +323,6 @@ __global__ void __launch_bounds__(256) k1_gather_mix(const __grid_constant__ K1P
 // Twiddles: W_n^k from the stage's base table (coalesced __ldg, L1-resident),
 // W_n^{ck} by two interleaved recurrences.  The output stays in Rader order
 // (bin g^-p at position p).
-struct K2Params {
-  double2* Z;
-  int64_t z_vec_stride;
-  int P, M, nfac, t;     // t: bucket-prime index (trace builds only)
-  int fac[kMaxFac];
-  int toff[kMaxFac];
-  const double2* bhat;   // [R_last][M/R_last] (see internal.h)
-  const double2* tw;     // per-stage twiddle base tables
-  double2* Zs;           // split mode: scratch rows (same layout and strides as Z)
-};
 
 // DIF stage of span n over a region of `len` elements (stage 0: the row; else a
 // sub-FFT), butterflies strided over `nth` threads with index `t`.
@@ -521,7 +339,7 @@ __device__ __forceinline__ void dif_stage(const double2* __restrict__ src, doubl
     const double2 w1 = ldg2(tw + k);
     double2 v[R];
 #pragma unroll
-    for (int r = 0; r < R; ++r) v[r] = GSRC ? __ldcg(src + base + r * m) : s[base + r * m];
+    for (int r = 0; r < R; ++r) v[r] = GSRC ? ldcg2(src + base + r * m) : s[base + r * m];
     dft<R>(v);
     // W^c by two interleaved recurrences W^c = W^{c-2} W^2 (half the dependency depth)
     const double2 w2 = cmul(w1, w1);
@@ -670,13 +488,13 @@ __global__ void __launch_bounds__(MAXT) __maxnreg__(((65536 / (MAXT * MINB)) & ~
   const int M = p.M, F = p.nfac;
   const int NT = blockDim.x, tid = threadIdx.x;
   double2* row = p.Z + (int64_t)blockIdx.y * p.z_vec_stride + (int64_t)blockIdx.x * p.P;
-  const double2 x0 = __ldcg(row + M);
+  const double2 x0 = ldcg2(row + M);
   int n = M;
   if (F >= 2) {
     run_dif<true>(p.fac[0], row, sm, M, n, p.tw + p.toff[0], tid, NT);
     n /= p.fac[0];
   } else {
-    for (int i = tid; i < M; i += NT) sm[i] = __ldcg(row + i);
+    for (int i = tid; i < M; i += NT) sm[i] = ldcg2(row + i);
   }
   __syncthreads();
   K2T();
@@ -710,6 +528,7 @@ __global__ void __launch_bounds__(MAXT) __maxnreg__(((65536 / (MAXT * MINB)) & ~
 #endif
 }
 
+
 // ---------------------------------------------------------------- K2 split mode
 // Rows too long for one CTA's shared memory (P above ~14.5k: s >= ~1800 at
 // c_b = 4).  K2a: CTA (row, c) computes output block c of the radix-R0 stage-0
@@ -734,11 +553,11 @@ __global__ void __launch_bounds__(MAXT) __maxnreg__(((65536 / (MAXT * MINB)) & ~
   sincospi(-2.0 * (double)c / (double)R0, &sn, &cs);
   const double2 wc = make_double2(cs, sn);  // W_R0^c
   for (int k = tid; k < Msub; k += NT) {
-    double2 acc = __ldcg(row + k);
+    double2 acc = ldcg2(row + k);
     double2 w = wc;
 #pragma unroll 4
     for (int r = 1; r < R0; ++r) {
-      acc = cadd(acc, cmul(__ldcg(row + k + r * Msub), w));
+      acc = cadd(acc, cmul(ldcg2(row + k + r * Msub), w));
       w = cmul(w, wc);
     }
     sm[k] = c == 0 ? acc : cmul(acc, ldg2(twf + (int64_t)c * k));
@@ -761,7 +580,7 @@ __global__ void __launch_bounds__(MAXT) __maxnreg__(((65536 / (MAXT * MINB)) & ~
   const uint64_t pol = l2_evict_last();
   for (int k = tid; k < Msub; k += NT) st_keep(srow + (int64_t)c * Msub + k, sm[k], pol);
   if (c == 0 && tid == 0) {
-    const double2 x0 = __ldcg(row + M);
+    const double2 x0 = ldcg2(row + M);
     srow[M] = x0;                                // x0 for K2b
     ((double2*)row)[M] = cadd(x0, sX0);          // X[0] = x0 + sum_q a_q (no other CTA reads row[M])
   }
@@ -777,15 +596,15 @@ __global__ void __launch_bounds__(256) k2b_split(const __grid_constant__ K2Param
   double2* row = p.Z + roff;
   const double2* srow = p.Zs + roff;
   const double2* twf = p.tw + p.toff[0];
-  const double2 x0 = __ldcg(srow + M);
+  const double2 x0 = ldcg2(srow + M);
   const uint64_t pol = l2_evict_last();
   switch (R0) {
 #define DSFT_C(RR)                                                                 \
   case RR: {                                                                       \
     double2 v[RR];                                                                 \
-    v[0] = __ldcg(srow + k);                                                       \
+    v[0] = ldcg2(srow + k);                                                       \
     _Pragma("unroll") for (int r = 1; r < RR; ++r)                                 \
-      v[r] = cmul(__ldcg(srow + k + r * Msub), ldg2(twf + (int64_t)r * k));        \
+      v[r] = cmul(ldcg2(srow + k + r * Msub), ldg2(twf + (int64_t)r * k));        \
     dft<RR>(v);                                                                    \
     _Pragma("unroll") for (int cc = 0; cc < RR; ++cc)                              \
       st_keep(row + k + cc * Msub, cadd(x0, cconj(v[cc])), pol);                   \
@@ -1400,6 +1219,10 @@ cudaError_t launch_k2(const Plan& p, int t, int zb, int nvec, void* ws, const in
   }
   dim3 grid((unsigned)(nbands * b.S), nvec);
   const size_t smem = (size_t)b.M * sizeof(double2);
+  if (b.k2_jit) {  // plan-time specialisation (jit.cpp): same arguments, compile-time radices
+    void* args[] = {(void*)&k};
+    return cudaLaunchKernel(b.k2_jit, grid, dim3(b.fft_threads), args, smem, st);
+  }
   // Shared-memory carveout: just enough for the resident rows, so the rest of
   // the unified 256 KB stays L1 for bhat and the twiddle tables (read by every
   // CTA on the SM).

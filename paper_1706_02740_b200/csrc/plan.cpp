@@ -12,6 +12,7 @@
 #include <complex>
 #include <cstdio>
 #include <functional>
+#include <thread>
 #include <tuple>
 #include <string>
 #include <vector>
@@ -535,6 +536,38 @@ static dsft_status upload_tables(Plan& P) {
   return DSFT_OK;
 }
 
+// K2 plan-time specialisation (jit.cpp): one NVRTC compile per distinct radix
+// tuple, bucket primes compiled in parallel threads.  Rows of the runtime-radix
+// instantiation <64,8> (M <= 1200: cheap) and split-mode rows stay generic.
+static void specialise_k2(Plan& P) {
+  const char* env = getenv("DSFT_JIT");
+  if (env && strcmp(env, "0") == 0) {
+    P.jit_why = "disabled by DSFT_JIT=0";
+    return;
+  }
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::vector<std::thread> th;
+  std::vector<std::string> why(P.T);
+  for (int t = 0; t < P.T; ++t) {
+    Bucket& b = P.bk[t];
+    if (b.split || b.fft_variant == 0) continue;
+    th.emplace_back([&, t, dev] {
+      cudaSetDevice(dev);
+      Bucket& bb = P.bk[t];
+      const int minb = bb.fft_variant == 1 ? 2 : 1;
+      bb.k2_jit = jit_k2(bb.fft_threads, minb, bb.fac, bb.nfac, (size_t)bb.M * 16, &why[t]);
+    });
+  }
+  for (auto& x : th) x.join();
+  P.jit_why.clear();
+  for (int t = 0; t < P.T; ++t)
+    if (!why[t].empty()) {
+      P.jit_why = "P=" + std::to_string(P.bk[t].P) + ": " + why[t];
+      break;
+    }
+}
+
 // =============================================================== ABI: basics
 extern "C" {
 
@@ -594,8 +627,35 @@ dsft_status dsft_plan_create(int64_t N, int64_t s, const dsft_params* params, ds
     delete pl;
     return st;
   }
+  specialise_k2(pl->p);
   *out = pl;
   return DSFT_OK;
+}
+
+dsft_status dsft_debug_jit_compile(int32_t nt, int32_t minb, const int32_t* fac, int32_t nfac, char* why,
+                                   size_t why_len) {
+  if (!fac || nfac < 1 || nfac > kMaxFac || nt < 32 || minb < 1) return fail(DSFT_ERR_ARG, "bad arguments");
+  std::vector<int> f(fac, fac + nfac);
+  std::string w;
+  const bool ok = jit_k2_compile_only(nt, minb, f.data(), nfac, &w);
+  if (why && why_len) {
+    const size_t c = std::min(why_len - 1, w.size());
+    memcpy(why, w.data(), c);
+    why[c] = '\0';
+  }
+  return ok ? DSFT_OK : fail(DSFT_ERR_CUDA, "NVRTC compile failed: " + w.substr(0, 200));
+}
+
+int32_t dsft_plan_k2_specialized(const dsft_plan* pl, char* why, size_t why_len) {
+  if (!pl) return 0;
+  int32_t n = 0;
+  for (int t = 0; t < pl->p.T; ++t) n += pl->p.bk[t].k2_jit != nullptr;
+  if (why && why_len) {
+    const size_t c = std::min(why_len - 1, pl->p.jit_why.size());
+    memcpy(why, pl->p.jit_why.data(), c);
+    why[c] = '\0';
+  }
+  return n;
 }
 
 void dsft_plan_destroy(dsft_plan* pl) {

@@ -59,3 +59,14 @@ def test_shard_bands_partition():
             got = sorted(j for r in range(world) for j in d.dsft_shard_bands(J, r, world))
             assert got == list(range(J))
             assert all(j % world == r for r in range(world) for j in d.dsft_shard_bands(J, r, world))
+
+
+def test_k2_specialisation_compiles_with_nvrtc(tmp_path, monkeypatch):
+    """Plan-time K2 specialisation (jit.cpp): the embedded device sources compile
+    with NVRTC for sm_100a (no GPU needed), for 1- to 4-pass radix tuples."""
+    monkeypatch.setenv("DSFT_JIT_CACHE", str(tmp_path))  # force real compiles
+    import paper_1706_02740_b200 as d
+    for nt, minb, rad in ((256, 2, [10, 9, 9, 5]), (512, 1, [12, 10, 9, 7]), (256, 2, [13]), (256, 2, [16, 3])):
+        st, log = d.dsft_debug_jit_compile(nt, minb, rad)
+        assert st == 0, log
+    assert len(list(tmp_path.glob("k2_*.cubin"))) == 4

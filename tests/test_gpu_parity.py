@@ -181,6 +181,22 @@ def test_host_path_equals_device_path():
     assert np.array_equal(frh.numpy(), f1) and np.array_equal(coh.numpy(), c1)
 
 
+def test_k2_specialised_equals_runtime_radix(monkeypatch):
+    """The plan-time NVRTC specialisation of K2 and the runtime-radix kernel run the
+    same passes in the same arithmetic order: outputs bitwise identical."""
+    N, s = 2**20, 300  # bucket primes in [1200, 2400): runtime-radix <256,2> rows -> specialised
+    pl = planted(N, s, cfg=38, trial=0)
+    plan = d.Plan(N, s)
+    nspec, why = plan.dsft_plan_k2_specialized()
+    assert nspec == plan.info.T, why
+    a = run_gpu(plan, pl.f)
+    monkeypatch.setenv("DSFT_JIT", "0")
+    plan0 = d.Plan(N, s)
+    assert plan0.dsft_plan_k2_specialized()[0] == 0
+    b = run_gpu(plan0, pl.f)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
 def test_deterministic_repeat():
     N, s = 2**16, 50
     pl = planted(N, s, cfg=36, trial=0)
