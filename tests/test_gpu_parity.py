@@ -188,7 +188,8 @@ def test_k2_specialised_equals_runtime_radix(monkeypatch):
     pl = planted(N, s, cfg=38, trial=0)
     plan = d.Plan(N, s)
     nspec, why = plan.dsft_plan_k2_specialized()
-    assert nspec == plan.info.T, why
+    big = sum(1 for P in plan.primes() if P - 1 > 1200)  # rows of the <64,8> instantiation stay generic
+    assert nspec == big and big >= 1 and why == "", why
     a = run_gpu(plan, pl.f)
     monkeypatch.setenv("DSFT_JIT", "0")
     plan0 = d.Plan(N, s)
