@@ -11,6 +11,8 @@
 //   cand_w       [vec][band][sum_t P_t] int64   omega' per bucket (or INT64_MIN)
 //   cand_v       [vec][band][sum_t P_t][Kmax] complex128, E_{t,i}[bin] of the
 //                residue argmax (written only for in-passband candidates)
+//   vmask        [vec][band][sum_t P_t] int32 vote mask per candidate slot: bit t set
+//                on the owner slot (smallest prime producing omega) by K3 of prime t
 //   acc_w/acc_z/acc_r [vec][band][sum_t P_t] accepted omegas, median z, |z| rank; acc_n [vec][band]
 //   band_w/c/z/m [vec][band][band_budget] line-9/11 output per band sorted by the
 //                merge key m = |c|^2 (-1 for exact zeros); band_n / band_nz counts
@@ -106,8 +108,8 @@ struct Plan {
 // Workspace regions (byte offsets, 256-aligned) for `nvec` concurrent vectors,
 // and the per-vector element strides the kernels use.
 struct WsLayout {
-  size_t z, zs, cand_w, cand_v, acc_w, acc_z, acc_r, acc_mask, acc_n, work_n, work, band_w, band_c, band_z, band_m, band_n,
-      band_nz, total;
+  size_t z, zs, cand_w, cand_v, vmask, acc_w, acc_z, acc_r, acc_mask, acc_n, work_n, ticket, work, band_w, band_c,
+      band_z, band_m, band_n, band_nz, total;
   int64_t z_vec;     // complex128 elements per vector in Z:        J * max_t S_t P_t
   int64_t z_buf;     // elements per Z buffer (nvec * z_vec); two buffers (prime parity)
   // zs: K2 split-mode scratch (one Z buffer, only when some bucket prime is split)
@@ -124,8 +126,10 @@ cudaError_t launch_k2(const Plan& p, int t, int zb, int nvec, void* ws, const in
                       cudaStream_t st);
 cudaError_t launch_k3(const Plan& p, int t, int zb, int nvec, void* ws, const int* band_list, int nbands,
                       cudaStream_t st);
-cudaError_t launch_k45(const Plan& p, int nvec, void* ws, const int* band_list, int nbands,
-                       cudaStream_t st);
+// K4..K6 in one cooperative launch; freqs == nullptr: no merge (sharded path merges
+// after the allgather with launch_k6_blocks)
+cudaError_t launch_k45(const Plan& p, int nvec, void* ws, const int* band_list, int nbands, cudaStream_t st,
+                       int64_t* freqs, double2* coeffs);
 cudaError_t launch_k6(const Plan& p, int nvec, void* ws, int64_t* freqs, double2* coeffs,
                       cudaStream_t st);
 cudaError_t launch_debug_grid(const Plan& p, int t, int zb, int i, int band, int what, const void* ws,

@@ -18,6 +18,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cooperative_groups.h>
+
 #include <algorithm>
 #include <cmath>
 
@@ -26,6 +28,7 @@
 #include "k2_fft.cuh"
 
 namespace dsft {
+namespace cg = cooperative_groups;
 
 // =============================================================== K1 gather_mix
 struct K1Params {
@@ -616,6 +619,11 @@ __global__ void __launch_bounds__(256) k2b_split(const __grid_constant__ K2Param
 }
 
 // ============================================================== K3 identify
+__device__ __forceinline__ int64_t pmod(int64_t x, int64_t m) {
+  int64_t r = x % m;
+  return r < 0 ? r + m : r;
+}
+
 struct K3Params {
   const double2* Z;
   int64_t z_vec_stride;
@@ -632,6 +640,9 @@ struct K3Params {
   double2* cand_v;
   int64_t cw_vec_stride;  // elements per vector in cand_w (nb * sumP)
   int64_t sumP, off;
+  int t;                  // this bucket prime's index
+  int64_t Pt[DSFT_MAX_T], offt[DSFT_MAX_T];  // all bucket primes and their slot offsets
+  int32_t* vmask;         // [vec][band][sum_t P_t] vote mask per candidate slot (reading R9)
 };
 
 template <int R>
@@ -697,64 +708,25 @@ __global__ void __launch_bounds__(256) k3_identify(const __grid_constant__ K3Par
   const bool ok = (om <= q + p.halfN_dn) && (om >= q - p.w) && (om < q + p.w) && (om >= p.B_lo) && (om <= p.B_hi);
   const int64_t slot = (int64_t)v * p.cw_vec_stride + (int64_t)j * p.sumP + p.off + a;
   p.cand_w[slot] = ok ? om : kSentinel;
+  int32_t mk = 0;
   if (ok) {
     double2* cv = p.cand_v + slot * p.Kmax;
     for (int i = 0; i < p.K; ++i) cv[i] = yv[i];
+    // Vote (reading R9), incrementally over the bucket primes in order: the owner
+    // of omega in this band is the smallest prime that produced it; K3 of every
+    // later producing prime ORs its bit into the owner's mask (K3 launches are
+    // sequential, so the earlier primes' candidates are final here).
+    const int64_t bb = (int64_t)v * p.cw_vec_stride + (int64_t)j * p.sumP;
+    int t0 = p.t;
+    for (int t2 = 0; t2 < p.t; ++t2)
+      if (__ldcg(p.cand_w + bb + p.offt[t2] + pmod(om, p.Pt[t2])) == om) {
+        t0 = t2;
+        break;
+      }
+    if (t0 == p.t) mk = 1 << p.t;
+    else atomicOr(p.vmask + bb + p.offt[t0] + pmod(om, p.Pt[t0]), 1 << p.t);
   }
-}
-
-// ================================================================ K4 vote
-// Reading R9: omega is accepted in its band when at least v_min distinct bucket
-// primes produced it.  The owner slot (smallest such t) appends (omega, voter
-// mask) to the band's list and (band, position) to one global worklist, with
-// atomic counters.  List order is arbitrary; everything downstream is rank-
-// based on a total order, so results are deterministic.
-struct K4Params {
-  const int64_t* cand_w;
-  int64_t cw_vec_stride, sumP;
-  int T, vote_min, nb, pad_;
-  int64_t P[DSFT_MAX_T];
-  int64_t off[DSFT_MAX_T];
-  int64_t* acc_w;
-  int32_t* acc_mask;
-  int32_t* acc_n;    // [vec][band]
-  int64_t bn_vec;
-  int64_t* work;     // [vec][band * sumP] packed (band << 32 | pos)
-  int32_t* work_n;   // [vec]
-};
-
-__device__ __forceinline__ int64_t pmod(int64_t x, int64_t m) {
-  int64_t r = x % m;
-  return r < 0 ? r + m : r;
-}
-
-__global__ void __launch_bounds__(256) k4_vote(const __grid_constant__ K4Params p) {
-  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (gid >= (int64_t)p.nb * p.sumP) return;
-  const int v = blockIdx.y;
-  const int j = (int)(gid / p.sumP);
-  const int64_t idx = gid - (int64_t)j * p.sumP;
-  const int64_t base = (int64_t)v * p.cw_vec_stride + (int64_t)j * p.sumP;
-  const int64_t* cw = p.cand_w + base;
-  const int64_t om = cw[idx];
-  if (om == kSentinel) return;
-  int t = 0;
-  while (t + 1 < p.T && idx >= p.off[t + 1]) ++t;
-  int votes = 0;
-  int32_t mask = 0;
-  for (int t2 = 0; t2 < p.T; ++t2) {
-    if (t2 == t || __ldg(cw + p.off[t2] + pmod(om, p.P[t2])) == om) {
-      if (t2 < t) return;  // not the owner
-      ++votes;
-      mask |= 1 << t2;
-    }
-  }
-  if (votes < p.vote_min) return;
-  const int pos = atomicAdd(p.acc_n + (int64_t)v * p.bn_vec + j, 1);
-  p.acc_w[base + pos] = om;
-  p.acc_mask[base + pos] = mask;
-  const int gpos = atomicAdd(p.work_n + v, 1);
-  p.work[(int64_t)v * p.cw_vec_stride + gpos] = ((int64_t)j << 32) | (int64_t)pos;
+  p.vmask[slot] = mk;  // this prime's slots: written only here, OR-ed only by later K3s
 }
 
 // =========================================================== K5a medians
@@ -771,8 +743,6 @@ struct K5aParams {
   const int64_t* acc_w;
   const int32_t* acc_mask;
   double2* acc_z;
-  const int64_t* work;
-  const int32_t* work_n;
 };
 
 constexpr int kMaxVals = DSFT_MAX_T * DSFT_MAX_K;
@@ -808,18 +778,12 @@ __device__ __forceinline__ double warp_median(double v, int cnt, int lane) {
   return (cnt & 1) ? b : 0.5 * (a + b);
 }
 
-__global__ void __launch_bounds__(256) k5a_medians(const __grid_constant__ K5aParams p) {
-  const int v = blockIdx.y;
-  const int lane = threadIdx.x & 31;
-  const int nwarps = gridDim.x * (blockDim.x >> 5);
-  const int total = p.work_n[v];
-  for (int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w < total; w += nwarps) {
-    const int64_t packed = p.work[(int64_t)v * p.cw_vec_stride + w];
-    const int j = (int)(packed >> 32);
-    const int pos = (int)(packed & 0xffffffff);
+// accepted entry `pos` of band j of vector v, one warp
+__device__ __forceinline__ void median_warp(const K5aParams& p, int v, int j, int pos, int lane) {
+  {
     const int64_t base = (int64_t)v * p.cw_vec_stride + (int64_t)j * p.sumP;
-    const int64_t om = p.acc_w[base + pos];
-    const int32_t mask = p.acc_mask[base + pos];
+    const int64_t om = __ldcg(p.acc_w + base + pos);
+    const int32_t mask = __ldcg(p.acc_mask + base + pos);
     const double sgn = (om & 1) ? -1.0 : 1.0;
     // lane -> (t, i) over the voting primes in ascending t
     int cnt = 0, my_t = -1, my_i = 0;
@@ -897,34 +861,83 @@ __device__ __forceinline__ double ghat_dev(double c1, int64_t dq) {
   return exp(-(c1 * c1) * d * d / 2.0) / 2.5066282746310002;  // Lemma 2
 }
 
-__global__ void __launch_bounds__(kK5Threads) k5b_select(const __grid_constant__ K5bParams p) {
-  const int j = blockIdx.x, v = blockIdx.y, tid = threadIdx.x;
+// one band of one vector per CTA (kK5Threads threads); sm_m / sm_w: kRankTile each
+__device__ void select_band(const K5bParams& p, int v, int j, double* sm_m, int64_t* sm_w, int* s_nzp) {
+  const int tid = threadIdx.x;
+  int& s_nz = *s_nzp;
   const int64_t base = (int64_t)v * p.cw_vec_stride + (int64_t)j * p.sumP;
   const int64_t* accw = p.acc_w + base;
   const double2* accz = p.acc_z + base;
   int32_t* accr = p.acc_r + base;
-  const int n = p.acc_n[(int64_t)v * p.bn_vec + j];
+  const int n = __ldcg(p.acc_n + (int64_t)v * p.bn_vec + j);
   const int64_t q = p.qfirst + (int64_t)j * p.qstep;
-  __shared__ double sm_m[kRankTile];
-  __shared__ int64_t sm_w[kRankTile];
-  __shared__ int s_nz;
+  __syncthreads();  // smem reuse across calls
   if (tid == 0) s_nz = 0;
+  if (n <= kRankTile) {
+    // staged: keys in shared memory, one global read per entry
+    double* sm_m2 = sm_m + kRankTile;  // rank-2 keys (the buffer holds kK6Stage >= 2 kRankTile)
+#pragma unroll
+    for (int it = 0; it < kRankTile / kK5Threads; ++it) {  // fixed trip: loads in flight together
+      const int i = tid + it * kK5Threads;
+      if (i < n) {
+        sm_m[i] = cabs2_rn(ldcg2(accz + i));
+        sm_w[i] = __ldcg(accw + i);
+      }
+    }
+    __syncthreads();
+    for (int e = tid; e < n; e += kK5Threads) {  // rank 1: (|z|^2 desc, omega asc); keep rank < budget
+      const double my_m = sm_m[e];
+      const int64_t my_w = sm_w[e];
+      int rank = 0;
+      for (int i = 0; i < n; ++i) rank += (sm_m[i] > my_m || (sm_m[i] == my_m && sm_w[i] < my_w)) ? 1 : 0;
+      double m2 = -2.0;  // not kept: never ranks ahead
+      if (rank < p.budget) {
+        const double2 z = ldcg2(accz + e);
+        const double gh = ghat_dev(p.c1, my_w - q);
+        const double2 c = make_double2(z.x / gh, z.y / gh);
+        m2 = (c.x == 0.0 && c.y == 0.0) ? -1.0 : cabs2_rn(c);
+      }
+      sm_m2[e] = m2;
+    }
+    __syncthreads();
+    for (int e = tid; e < n; e += kK5Threads) {  // rank 2 among kept -> output slot
+      const double my_m = sm_m2[e];
+      if (my_m < -1.5) continue;
+      const int64_t my_w = sm_w[e];
+      int rank = 0;
+      for (int i = 0; i < n; ++i) rank += (sm_m2[i] > my_m || (sm_m2[i] == my_m && sm_w[i] < my_w)) ? 1 : 0;
+      const double2 z = ldcg2(accz + e);
+      const double gh = ghat_dev(p.c1, my_w - q);
+      const int64_t o = (int64_t)v * p.band_vec + (int64_t)j * p.budget + rank;
+      p.band_w[o] = my_w;
+      p.band_z[o] = z;
+      p.band_c[o] = make_double2(z.x / gh, z.y / gh);
+      p.band_m[o] = my_m;
+      if (my_m >= 0.0) atomicAdd(&s_nz, 1);
+    }
+    __syncthreads();
+    if (tid == 0) {
+      p.band_n[(int64_t)v * p.bn_vec + j] = (int32_t)(n < p.budget ? n : p.budget);
+      p.band_nz[(int64_t)v * p.bn_vec + j] = s_nz;
+    }
+    return;
+  }
   // ---- rank 1: (|z|^2 desc, omega asc); keep rank < budget
   for (int e0 = 0; e0 < n; e0 += kK5Threads) {
     const int e = e0 + tid;
     double my_m = 0.0;
     int64_t my_w = 0;
     if (e < n) {
-      my_m = cabs2_rn(accz[e]);
-      my_w = accw[e];
+      my_m = cabs2_rn(ldcg2(accz + e));
+      my_w = __ldcg(accw + e);
     }
     int rank = 0;
     for (int t0 = 0; t0 < n; t0 += kRankTile) {
       const int len = min(kRankTile, n - t0);
       __syncthreads();
       for (int i = tid; i < len; i += kK5Threads) {
-        sm_m[i] = cabs2_rn(accz[t0 + i]);
-        sm_w[i] = accw[t0 + i];
+        sm_m[i] = cabs2_rn(ldcg2(accz + t0 + i));
+        sm_w[i] = __ldcg(accw + t0 + i);
       }
       __syncthreads();
       if (e < n)
@@ -942,8 +955,8 @@ __global__ void __launch_bounds__(kK5Threads) k5b_select(const __grid_constant__
     double2 my_z = make_double2(0.0, 0.0), my_c = my_z;
     if (e < n && accr[e] < p.budget) {
       keep = true;
-      my_w = accw[e];
-      my_z = accz[e];
+      my_w = __ldcg(accw + e);
+      my_z = ldcg2(accz + e);
       const double gh = ghat_dev(p.c1, my_w - q);
       my_c = make_double2(my_z.x / gh, my_z.y / gh);
       my_m = (my_c.x == 0.0 && my_c.y == 0.0) ? -1.0 : cabs2_rn(my_c);
@@ -954,8 +967,8 @@ __global__ void __launch_bounds__(kK5Threads) k5b_select(const __grid_constant__
       __syncthreads();
       for (int i = tid; i < len; i += kK5Threads) {
         if (accr[t0 + i] < p.budget) {
-          const int64_t w2 = accw[t0 + i];
-          const double2 z2 = accz[t0 + i];
+          const int64_t w2 = __ldcg(accw + t0 + i);
+          const double2 z2 = ldcg2(accz + t0 + i);
           const double gh = ghat_dev(p.c1, w2 - q);
           const double2 c2 = make_double2(z2.x / gh, z2.y / gh);
           sm_m[i] = (c2.x == 0.0 && c2.y == 0.0) ? -1.0 : cabs2_rn(c2);
@@ -1013,16 +1026,17 @@ __device__ __forceinline__ bool key_ahead(double m2, int64_t w2, double m, int64
   return m2 > m || (m2 == m && w2 < w);
 }
 
-__global__ void __launch_bounds__(kK6Threads) k6_merge(const __grid_constant__ K6Params p) {
-  const int v = blockIdx.y;
-  extern __shared__ unsigned char k6_smem[];
-  double* sm_m = (double*)k6_smem;
-  int64_t* sm_w = (int64_t*)(sm_m + kK6Stage);
-  __shared__ int32_t pre[kK6MaxBlocks + 1];
+// output ranks [e_lo, e_hi) of vector v by one CTA of kK6Threads threads;
+// sm_m / sm_w: kK6Stage each, pre: kK6MaxBlocks + 1
+__device__ void merge_range(const K6Params& p, int v, int64_t e_lo, int64_t e_hi, double* sm_m, int64_t* sm_w,
+                            int32_t* pre) {
   const int32_t* bz = p.band_nz + (int64_t)v * p.bn_vec;
+  __syncthreads();  // smem reuse across calls
+  for (int b = threadIdx.x; b < p.nb; b += blockDim.x) pre[b + 1] = __ldcg(bz + b);  // parallel loads
+  __syncthreads();
   if (threadIdx.x == 0) {
     pre[0] = 0;
-    for (int b = 0; b < p.nb; ++b) pre[b + 1] = pre[b] + bz[b];
+    for (int b = 0; b < p.nb; ++b) pre[b + 1] += pre[b];
   }
   __syncthreads();
   const int64_t n = pre[p.nb];  // eligible (non-zero) entries
@@ -1031,59 +1045,162 @@ __global__ void __launch_bounds__(kK6Threads) k6_merge(const __grid_constant__ K
   const double2* bc = p.band_c + (int64_t)v * p.blk_vec;
   int64_t* ow = p.out_w + (int64_t)v * p.s;
   double2* oc = p.out_c + (int64_t)v * p.s;
-  const int64_t e = (int64_t)blockIdx.x * kK6Threads + threadIdx.x;  // flat eligible index
-  const int64_t e0 = (int64_t)blockIdx.x * kK6Threads;
-  if (e0 < n) {  // CTA-uniform
-    const bool staged = n <= kK6Stage;
-    if (staged) {
-      for (int64_t i = threadIdx.x; i < n; i += kK6Threads) {
-        int lo = 0, hi = p.nb;  // block of flat entry i: largest b with pre[b] <= i
-        while (hi - lo > 1) {
-          const int mid = (lo + hi) >> 1;
-          if (pre[mid] <= i) lo = mid;
-          else hi = mid;
-        }
-        const int64_t sl = (int64_t)lo * p.budget + (i - pre[lo]);
-        sm_m[i] = bm[sl];
-        sm_w[i] = bw[sl];
+  const int64_t hi = e_hi < (n > p.s ? n : p.s) ? e_hi : (n > p.s ? n : p.s);
+  const bool staged = n <= kK6Stage && e_lo < n;  // CTA-uniform
+  if (staged) {
+    for (int64_t i = threadIdx.x; i < n; i += kK6Threads) {
+      int lo = 0, hb = p.nb;  // block of flat entry i: largest b with pre[b] <= i
+      while (hb - lo > 1) {
+        const int mid = (lo + hb) >> 1;
+        if (pre[mid] <= i) lo = mid;
+        else hb = mid;
       }
-      __syncthreads();
+      const int64_t sl = (int64_t)lo * p.budget + (i - pre[lo]);
+      sm_m[i] = __ldcg(bm + sl);
+      sm_w[i] = __ldcg(bw + sl);
     }
+    __syncthreads();
+  }
+  for (int64_t e = e_lo + threadIdx.x; e < hi; e += kK6Threads) {
     if (e < n) {
-      int lo = 0, hi = p.nb;
-      while (hi - lo > 1) {
-        const int mid = (lo + hi) >> 1;
+      int lo = 0, hb = p.nb;
+      while (hb - lo > 1) {
+        const int mid = (lo + hb) >> 1;
         if (pre[mid] <= e) lo = mid;
-        else hi = mid;
+        else hb = mid;
       }
       const int b = lo;
       const int64_t i = e - pre[b];
       const int64_t sl = (int64_t)b * p.budget + i;
-      const double m = staged ? sm_m[e] : bm[sl];
-      const int64_t w = staged ? sm_w[e] : bw[sl];
       int64_t rank = i;
-      for (int b2 = 0; b2 < p.nb; ++b2) {
-        if (b2 == b) continue;
-        int l2 = 0, h2 = pre[b2 + 1] - pre[b2];  // first entry of b2 not ahead of (m, w)
-        const int64_t f2 = pre[b2], o2 = (int64_t)b2 * p.budget;
-        while (l2 < h2) {
-          const int mid = (l2 + h2) >> 1;
-          const bool ahead = staged ? key_ahead(sm_m[f2 + mid], sm_w[f2 + mid], m, w)
-                                    : key_ahead(bm[o2 + mid], bw[o2 + mid], m, w);
-          if (ahead) l2 = mid + 1;
-          else h2 = mid;
+      if (staged) {  // (separate loops: a select between an smem and a global load issues both)
+        const double m = sm_m[e];
+        const int64_t w = sm_w[e];
+        for (int b2 = 0; b2 < p.nb; ++b2) {
+          if (b2 == b) continue;
+          int l2 = 0, h2 = pre[b2 + 1] - pre[b2];  // first entry of b2 not ahead of (m, w)
+          const int f2 = pre[b2];
+          while (l2 < h2) {
+            const int mid = (l2 + h2) >> 1;
+            if (key_ahead(sm_m[f2 + mid], sm_w[f2 + mid], m, w)) l2 = mid + 1;
+            else h2 = mid;
+          }
+          rank += l2;
         }
-        rank += l2;
+      } else {
+        const double m = __ldcg(bm + sl);
+        const int64_t w = __ldcg(bw + sl);
+        for (int b2 = 0; b2 < p.nb; ++b2) {
+          if (b2 == b) continue;
+          int l2 = 0, h2 = pre[b2 + 1] - pre[b2];
+          const int64_t o2 = (int64_t)b2 * p.budget;
+          while (l2 < h2) {
+            const int mid = (l2 + h2) >> 1;
+            if (key_ahead(__ldcg(bm + o2 + mid), __ldcg(bw + o2 + mid), m, w)) l2 = mid + 1;
+            else h2 = mid;
+          }
+          rank += l2;
+        }
       }
+      const int64_t w = staged ? sm_w[e] : __ldcg(bw + sl);
       if (rank < p.s) {
         ow[rank] = w;
-        oc[rank] = bc[sl];
+        oc[rank] = ldcg2(bc + sl);
       }
+    } else if (e < p.s) {  // unused output slots
+      ow[e] = kSentinel;
+      oc[e] = make_double2(0.0, 0.0);
     }
   }
-  if (e >= n && e < p.s) {  // unused output slots
-    ow[e] = kSentinel;
-    oc[e] = make_double2(0.0, 0.0);
+}
+
+__global__ void __launch_bounds__(kK6Threads) k6_merge(const __grid_constant__ K6Params p) {
+  extern __shared__ unsigned char k6_smem[];
+  __shared__ int32_t pre[kK6MaxBlocks + 1];
+  double* sm_m = (double*)k6_smem;
+  merge_range(p, blockIdx.y, (int64_t)blockIdx.x * kK6Threads, (int64_t)(blockIdx.x + 1) * kK6Threads, sm_m,
+              (int64_t*)(sm_m + kK6Stage), pre);
+}
+
+// ======================================================== K5 tail (+ merge)
+// K5s  scan: accepted = slots whose vote mask has >= v_min bits (R9; masks built
+//      by K3), compacted per band (atomic counters) and into one worklist.
+// K5a  Re/Im medians (R10), one warp per accepted omega anywhere on the GPU.
+// K5b  one CTA per (band, vector): band top-budget + unbias (R11, line 11); the
+//      last band CTA of a vector (ticket) re-zeroes the vector's counters for the
+//      next execute (zeroed at allocation).
+// K6   top-s merge over the band blocks (line 13), one entry per thread; the
+//      sharded path runs it after the allgather instead.
+struct K5Params {
+  K5aParams a;
+  K5bParams b;
+  const int32_t* vmask;
+  const int64_t* cand_w;
+  int64_t* acc_w;
+  int32_t* acc_mask;
+  int32_t* acc_n;    // [vec][band]
+  int64_t* work;     // [vec][band * sumP] packed (band << 32 | pos)
+  int32_t* work_n;   // [vec]
+  int32_t* ticket;   // [vec]
+  int vote_min, nb;
+};
+
+__global__ void __launch_bounds__(256) k5s_scan(const __grid_constant__ K5Params p) {
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= (int64_t)p.nb * p.b.sumP) return;
+  const int v = blockIdx.y;
+  const int j = (int)(gid / p.b.sumP);
+  const int64_t base = (int64_t)v * p.b.cw_vec_stride + (int64_t)j * p.b.sumP;
+  const int32_t mk = __ldcg(p.vmask + (int64_t)v * p.b.cw_vec_stride + gid);
+  if (__popc(mk) < p.vote_min) return;
+  const int pos = atomicAdd(p.acc_n + (int64_t)v * p.b.bn_vec + j, 1);
+  p.acc_w[base + pos] = __ldcg(p.cand_w + (int64_t)v * p.b.cw_vec_stride + gid);
+  p.acc_mask[base + pos] = mk;
+  const int gpos = atomicAdd(p.work_n + v, 1);
+  p.work[(int64_t)v * p.b.cw_vec_stride + gpos] = ((int64_t)j << 32) | (int64_t)pos;
+}
+
+__global__ void __launch_bounds__(256) k5a_medians(const __grid_constant__ K5Params p) {
+  const int v = blockIdx.y;
+  const int lane = threadIdx.x & 31;
+  const int nwarps = gridDim.x * (blockDim.x >> 5);
+  const int total = __ldcg(p.work_n + v);
+  for (int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w < total; w += nwarps) {
+    const int64_t packed = __ldcg(p.work + (int64_t)v * p.b.cw_vec_stride + w);
+    median_warp(p.a, v, (int)(packed >> 32), (int)(packed & 0xffffffff), lane);
+  }
+}
+
+#ifdef DSFT_K2_TRACE
+__device__ unsigned long long g_k5trace[64][4];
+#define K5T(i)                                                                      \
+  do {                                                                              \
+    if (threadIdx.x == 0 && blockIdx.x < 64) g_k5trace[blockIdx.x][(i)] = globaltimer_ns(); \
+  } while (0)
+#else
+#define K5T(i) \
+  do {         \
+  } while (0)
+#endif
+
+__global__ void __launch_bounds__(kK5Threads) k5b_select(const __grid_constant__ K5Params p) {
+  K5T(0);
+  extern __shared__ unsigned char k5_smem[];
+  __shared__ int s_nz, s_last;
+  double* sm_m = (double*)k5_smem;             // [2 kRankTile]: rank-1 and rank-2 keys
+  int64_t* sm_w = (int64_t*)(sm_m + 2 * kRankTile);
+  const int j = blockIdx.x, v = blockIdx.y, tid = threadIdx.x;
+  select_band(p.b, v, j, sm_m, sm_w, &s_nz);
+  K5T(1);
+  // the last band CTA of this vector to finish re-zeroes the counters
+  __syncthreads();
+  if (tid == 0) s_last = atomicAdd(p.ticket + v, 1) == p.nb - 1;
+  __syncthreads();
+  if (!s_last) return;
+  for (int b = tid; b < p.nb; b += kK5Threads) p.acc_n[(int64_t)v * p.b.bn_vec + b] = 0;
+  if (tid == 0) {
+    p.work_n[v] = 0;
+    p.ticket[v] = 0;
   }
 }
 
@@ -1131,6 +1248,7 @@ cudaError_t kernels_init() {
   const int maxsm = 227 * 1024 - 1024;  // leave room for the static reduction buffer
   if ((e = cudaFuncSetAttribute(k2_prime_dft<64, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm))) return e;
   if ((e = cudaFuncSetAttribute(k6_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, kK6Stage * 16))) return e;
+  if ((e = cudaFuncSetAttribute(k5b_select, cudaFuncAttributeMaxDynamicSharedMemorySize, kRankTile * 24))) return e;
 
   if ((e = cudaFuncSetAttribute(k2_prime_dft<256, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm))) return e;
   if ((e = cudaFuncSetAttribute(k2_prime_dft<512, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm))) return e;
@@ -1276,6 +1394,12 @@ cudaError_t launch_k3(const Plan& p, int t, int zb, int nvec, void* ws, const in
   k.B_lo = p.B_lo;
   k.B_hi = p.B_hi;
   k.gpow = b.gpow;
+  k.t = t;
+  for (int t2 = 0; t2 < p.T; ++t2) {
+    k.Pt[t2] = p.bk[t2].P;
+    k.offt[t2] = p.bk[t2].off;
+  }
+  k.vmask = (int32_t*)((char*)ws + L.vmask);
   k.cand_w = (int64_t*)((char*)ws + L.cand_w);
   k.cand_v = (double2*)((char*)ws + L.cand_v);
   k.cw_vec_stride = L.cw_vec;
@@ -1289,79 +1413,9 @@ cudaError_t launch_k3(const Plan& p, int t, int zb, int nvec, void* ws, const in
   return cudaGetLastError();
 }
 
-cudaError_t launch_k45(const Plan& p, int nvec, void* ws, const int* bands, int nbands, cudaStream_t st) {
-  const WsLayout L = ws_layout(p, p.ws_batch);
-  // zero the per-band and worklist counters (contiguous region)
-  cudaError_t e = cudaMemsetAsync((char*)ws + L.acc_n, 0, L.work - L.acc_n, st);
-  if (e != cudaSuccess) return e;
-  K4Params k4{};
-  k4.cand_w = (const int64_t*)((char*)ws + L.cand_w);
-  k4.cw_vec_stride = L.cw_vec;
-  k4.sumP = p.sumP;
-  k4.T = p.T;
-  k4.vote_min = p.params.vote_min;
-  k4.nb = nbands;
-  for (int t = 0; t < p.T; ++t) {
-    k4.P[t] = p.bk[t].P;
-    k4.off[t] = p.bk[t].off;
-  }
-  k4.acc_w = (int64_t*)((char*)ws + L.acc_w);
-  k4.acc_mask = (int32_t*)((char*)ws + L.acc_mask);
-  k4.acc_n = (int32_t*)((char*)ws + L.acc_n);
-  k4.bn_vec = L.bn_vec;
-  k4.work = (int64_t*)((char*)ws + L.work);
-  k4.work_n = (int32_t*)((char*)ws + L.work_n);
-  k4_vote<<<dim3(cdiv((int64_t)nbands * p.sumP, 256), nvec), 256, 0, st>>>(k4);
-  if ((e = cudaGetLastError()) != cudaSuccess) return e;
-
-  K5aParams ka{};
-  ka.cand_v = (const double2*)((char*)ws + L.cand_v);
-  ka.cw_vec_stride = L.cw_vec;
-  ka.sumP = p.sumP;
-  ka.T = p.T;
-  ka.Kmax = p.Kmax;
-  for (int t = 0; t < p.T; ++t) {
-    ka.P[t] = p.bk[t].P;
-    ka.off[t] = p.bk[t].off;
-    ka.K[t] = p.bk[t].K;
-  }
-  ka.acc_w = k4.acc_w;
-  ka.acc_mask = k4.acc_mask;
-  ka.acc_z = (double2*)((char*)ws + L.acc_z);
-  ka.work = k4.work;
-  ka.work_n = k4.work_n;
-  k5a_medians<<<dim3(2 * 148, nvec), 256, 0, st>>>(ka);
-  if ((e = cudaGetLastError()) != cudaSuccess) return e;
-
-  K5bParams k{};
-  k.cw_vec_stride = L.cw_vec;
-  k.sumP = p.sumP;
-  k.nb = nbands;
-  const int stride = nbands > 1 ? bands[1] - bands[0] : 1;
-  k.qfirst = band_q(p, bands[0]);
-  k.qstep = 2 * p.w * (int64_t)stride;
-  k.c1 = p.c1;
-  k.budget = p.info.band_budget;
-  k.band_vec = L.band_vec;
-  k.bn_vec = L.bn_vec;
-  k.acc_w = k4.acc_w;
-  k.acc_z = ka.acc_z;
-  k.acc_r = (int32_t*)((char*)ws + L.acc_r);
-  k.acc_n = k4.acc_n;
-  k.band_w = (int64_t*)((char*)ws + L.band_w);
-  k.band_c = (double2*)((char*)ws + L.band_c);
-  k.band_z = (double2*)((char*)ws + L.band_z);
-  k.band_m = (double*)((char*)ws + L.band_m);
-  k.band_n = (int32_t*)((char*)ws + L.band_n);
-  k.band_nz = (int32_t*)((char*)ws + L.band_nz);
-  k5b_select<<<dim3(nbands, nvec), kK5Threads, 0, st>>>(k);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_k6_blocks(const int64_t* bw, const double2* bc, const double* bm, const int32_t* bnz, int nblocks,
-                             int64_t budget, int64_t blk_vec, int64_t bn_vec, int64_t s, int nvec, int64_t* freqs,
-                             double2* coeffs, cudaStream_t st) {
-  if (nblocks > kK6MaxBlocks) return cudaErrorInvalidValue;
+// K6 parameters over the plan's band blocks
+static K6Params k6_params(const int64_t* bw, const double2* bc, const double* bm, const int32_t* bnz, int nblocks,
+                          int64_t budget, int64_t blk_vec, int64_t bn_vec, int64_t s, int64_t* freqs, double2* coeffs) {
   K6Params k{};
   k.band_w = bw;
   k.band_c = bc;
@@ -1374,6 +1428,79 @@ cudaError_t launch_k6_blocks(const int64_t* bw, const double2* bc, const double*
   k.s = s;
   k.out_w = freqs;
   k.out_c = coeffs;
+  return k;
+}
+
+cudaError_t launch_k45(const Plan& p, int nvec, void* ws, const int* bands, int nbands, cudaStream_t st,
+                       int64_t* freqs, double2* coeffs) {
+  const WsLayout L = ws_layout(p, p.ws_batch);
+  K5Params f{};
+  f.vmask = (const int32_t*)((char*)ws + L.vmask);
+  f.cand_w = (const int64_t*)((char*)ws + L.cand_w);
+  f.acc_w = (int64_t*)((char*)ws + L.acc_w);
+  f.acc_mask = (int32_t*)((char*)ws + L.acc_mask);
+  f.acc_n = (int32_t*)((char*)ws + L.acc_n);
+  f.work = (int64_t*)((char*)ws + L.work);
+  f.work_n = (int32_t*)((char*)ws + L.work_n);
+  f.ticket = (int32_t*)((char*)ws + L.ticket);
+  f.vote_min = p.params.vote_min;
+  f.nb = nbands;
+
+  K5aParams& ka = f.a;
+  ka.cand_v = (const double2*)((char*)ws + L.cand_v);
+  ka.cw_vec_stride = L.cw_vec;
+  ka.sumP = p.sumP;
+  ka.T = p.T;
+  ka.Kmax = p.Kmax;
+  for (int t = 0; t < p.T; ++t) {
+    ka.P[t] = p.bk[t].P;
+    ka.off[t] = p.bk[t].off;
+    ka.K[t] = p.bk[t].K;
+  }
+  ka.acc_w = f.acc_w;
+  ka.acc_mask = f.acc_mask;
+  ka.acc_z = (double2*)((char*)ws + L.acc_z);
+
+  K5bParams& k = f.b;
+  k.cw_vec_stride = L.cw_vec;
+  k.sumP = p.sumP;
+  k.nb = nbands;
+  const int stride = nbands > 1 ? bands[1] - bands[0] : 1;
+  k.qfirst = band_q(p, bands[0]);
+  k.qstep = 2 * p.w * (int64_t)stride;
+  k.c1 = p.c1;
+  k.budget = p.info.band_budget;
+  k.band_vec = L.band_vec;
+  k.bn_vec = L.bn_vec;
+  k.acc_w = f.acc_w;
+  k.acc_z = ka.acc_z;
+  k.acc_r = (int32_t*)((char*)ws + L.acc_r);
+  k.acc_n = f.acc_n;
+  k.band_w = (int64_t*)((char*)ws + L.band_w);
+  k.band_c = (double2*)((char*)ws + L.band_c);
+  k.band_z = (double2*)((char*)ws + L.band_z);
+  k.band_m = (double*)((char*)ws + L.band_m);
+  k.band_n = (int32_t*)((char*)ws + L.band_n);
+  k.band_nz = (int32_t*)((char*)ws + L.band_nz);
+
+  cudaError_t e;
+  k5s_scan<<<dim3(cdiv((int64_t)nbands * p.sumP, 256), nvec), 256, 0, st>>>(f);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  k5a_medians<<<dim3(2 * 148, nvec), 256, 0, st>>>(f);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  k5b_select<<<dim3(nbands, nvec), kK5Threads, kRankTile * 2 * 8 + kRankTile * 8, st>>>(f);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  if (!freqs) return cudaSuccess;  // sharded: merged after the allgather
+  if (nbands != p.J) return cudaErrorInvalidValue;
+  return launch_k6_blocks(k.band_w, k.band_c, k.band_m, k.band_nz, p.J, p.info.band_budget, L.band_vec, L.bn_vec, p.s,
+                          nvec, freqs, coeffs, st);
+}
+
+cudaError_t launch_k6_blocks(const int64_t* bw, const double2* bc, const double* bm, const int32_t* bnz, int nblocks,
+                             int64_t budget, int64_t blk_vec, int64_t bn_vec, int64_t s, int nvec, int64_t* freqs,
+                             double2* coeffs, cudaStream_t st) {
+  if (nblocks > kK6MaxBlocks) return cudaErrorInvalidValue;
+  const K6Params k = k6_params(bw, bc, bm, bnz, nblocks, budget, blk_vec, bn_vec, s, freqs, coeffs);
   const int64_t cap = std::max<int64_t>((int64_t)nblocks * budget, s);
   k6_merge<<<dim3(cdiv(cap, kK6Threads), nvec), kK6Threads, kK6Stage * 16, st>>>(k);
   return cudaGetLastError();
@@ -1418,6 +1545,9 @@ cudaError_t launch_debug_grid(const Plan& p, int t, int zb, int i, int band, int
 }  // namespace dsft
 
 #ifdef DSFT_K2_TRACE
+extern "C" int dsft_debug_k5_trace(unsigned long long* host) {
+  return (int)cudaMemcpyFromSymbol(host, dsft::g_k5trace, sizeof(dsft::g_k5trace));
+}
 extern "C" int dsft_debug_k2_trace(long long* host, size_t n) {
   const size_t bytes = std::min(n * sizeof(long long), sizeof(dsft::g_k2trace));
   return (int)cudaMemcpyFromSymbol(host, dsft::g_k2trace, bytes);

@@ -239,13 +239,16 @@ WsLayout ws_layout(const Plan& p, int64_t nvec) {
   L.zs = take(p.any_split ? (size_t)L.z_buf * 16 : 0);
   L.cand_w = take((size_t)nvec * L.cw_vec * 8);
   L.cand_v = take((size_t)nvec * L.cw_vec * p.Kmax * 16);
+  L.vmask = take((size_t)nvec * L.cw_vec * 4);
   L.acc_w = take((size_t)nvec * L.cw_vec * 8);
   L.acc_z = take((size_t)nvec * L.cw_vec * 16);
   L.acc_r = take((size_t)nvec * L.cw_vec * 4);
   L.acc_mask = take((size_t)nvec * L.cw_vec * 4);
-  // counters acc_n and work_n are contiguous (zeroed by one memset before K4)
+  // counters acc_n, work_n, ticket: contiguous, zeroed at allocation, re-zeroed by
+  // the last K5b CTA of each vector after use
   L.acc_n = take((size_t)nvec * L.bn_vec * 4);
   L.work_n = take((size_t)nvec * 4);
+  L.ticket = take((size_t)nvec * 4);
   L.work = take((size_t)nvec * L.cw_vec * 8);
   L.band_w = take((size_t)nvec * L.band_vec * 8);
   L.band_c = take((size_t)nvec * L.band_vec * 16);
@@ -711,6 +714,14 @@ size_t dsft_plan_workspace_bytes(const dsft_plan* pl, int64_t batch) {
   return ws_layout(pl->p, choose_wave(pl->p, batch)).total;
 }
 
+// K5 counters start at zero (the last K5b CTA of a vector re-zeroes them after use)
+static dsft_status zero_tickets(Plan& p) {
+  const WsLayout L = ws_layout(p, p.ws_batch);
+  CU(cudaMemset((char*)p.ws + L.acc_n, 0, L.work - L.acc_n), "zero K5 counters");
+  CU(cudaDeviceSynchronize(), "zero merge tickets (sync)");
+  return DSFT_OK;
+}
+
 dsft_status dsft_plan_set_workspace(dsft_plan* pl, void* dev, size_t bytes) {
   if (!pl) return fail(DSFT_ERR_ARG, "plan is NULL");
   if (!dev || ((uintptr_t)dev & 255)) return fail(DSFT_ERR_ARG, "workspace must be non-NULL and 256-B aligned");
@@ -723,7 +734,7 @@ dsft_status dsft_plan_set_workspace(dsft_plan* pl, void* dev, size_t bytes) {
   p.ws_bytes = bytes;
   p.ws_owned = false;
   p.ws_batch = nv;
-  return DSFT_OK;
+  return zero_tickets(p);
 }
 
 static dsft_status ensure_ws(Plan& p, int64_t want) {
@@ -742,7 +753,7 @@ static dsft_status ensure_ws(Plan& p, int64_t want) {
   p.ws_bytes = bytes;
   p.ws_owned = true;
   p.ws_batch = want;
-  return DSFT_OK;
+  return zero_tickets(p);
 }
 
 // Per-kernel timing: record an event pair around a launch when enabled.
@@ -786,7 +797,7 @@ static dsft_status ensure_pipe(Plan& p) {
 }
 
 static dsft_status run_bands(Plan& p, const double2* f, int64_t ld, int nv, const int* bands, int nb,
-                             cudaStream_t st) {
+                             cudaStream_t st, int64_t* freqs = nullptr, double2* coeffs = nullptr) {
   dsft_status stt = ensure_pipe(p);
   if (stt != DSFT_OK) return stt;
   cudaStream_t a1 = p.aux, a3 = p.aux3;
@@ -817,7 +828,8 @@ static dsft_status run_bands(Plan& p, const double2* f, int64_t ld, int nv, cons
   CU(cudaEventRecord(evJoin3, a3), "pipeline join");
   CU(cudaStreamWaitEvent(st, evJoin1, 0), "pipeline join wait");
   CU(cudaStreamWaitEvent(st, evJoin3, 0), "pipeline join wait");
-  CU(timed(p, 3, st, [&] { return launch_k45(p, nv, p.ws, bands, nb, st); }), "K45 vote_estimate launch");
+  CU(timed(p, 3, st, [&] { return launch_k45(p, nv, p.ws, bands, nb, st, freqs, coeffs); }),
+     "K456 vote/estimate/merge launch");
   return DSFT_OK;
 }
 
@@ -836,10 +848,9 @@ static dsft_status execute_impl(dsft_plan* pl, const dsft_c128* f, int64_t batch
   for (int j = 0; j < p.J; ++j) bands[j] = j;
   for (int64_t v0 = 0; v0 < batch; v0 += p.ws_batch) {
     const int nv = (int)std::min<int64_t>(p.ws_batch, batch - v0);
-    stt = run_bands(p, (const double2*)f + v0 * ld, ld, nv, bands.data(), p.J, st);
+    stt = run_bands(p, (const double2*)f + v0 * ld, ld, nv, bands.data(), p.J, st, freqs + v0 * p.s,
+                    (double2*)coeffs + v0 * p.s);
     if (stt != DSFT_OK) return stt;
-    CU(timed(p, 4, st, [&] { return launch_k6(p, nv, p.ws, freqs + v0 * p.s, (double2*)coeffs + v0 * p.s, st); }),
-       "K6 merge launch");
   }
   return DSFT_OK;
 }
@@ -900,7 +911,9 @@ dsft_status dsft_plan_collect_times(dsft_plan* pl, double* ms_out, int64_t* laun
 
 int64_t dsft_plan_launches_per_execute(const dsft_plan* pl) {
   if (!pl) return 0;
-  return 3 * (int64_t)pl->p.T + 3;  // K1..K3 per bucket prime, K4, K5, K6
+  int64_t n = 4;  // K5 scan, K5 medians, K5 select, K6 merge
+  for (int t = 0; t < pl->p.T; ++t) n += 3 + (pl->p.bk[t].split ? 1 : 0);  // K1, K2 (K2a + K2b), K3
+  return n;
 }
 
 // -------------------------------------------------------------- parity hooks

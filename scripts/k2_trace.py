@@ -46,3 +46,13 @@ for t in range(info.T):
     print(f"t={t} P={P} rows={nb} stage-boundaries={nst}: mean cycles per phase",
           np.round(d_.mean(axis=0)).astype(int).tolist(), "total", int(d_.sum(axis=1).mean()),
           "| start spread us", round((start.max() - start.min()) / 1e3, 1))
+
+
+t5 = np.zeros((64, 4), dtype=np.uint64)
+if hasattr(L, "dsft_debug_k5_trace") and L.dsft_debug_k5_trace(t5.ctypes.data_as(C.c_void_p)) == 0:
+    t5 = t5.astype(np.int64)[:info.J]
+    t0 = t5[:, 0].min()
+    for j in range(info.J):
+        r = t5[j]
+        print(f"K5b band {j}: start {(r[0]-t0)/1e3:7.2f} select {(r[1]-r[0])/1e3:7.2f} us" +
+              "")
