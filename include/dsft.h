@@ -168,6 +168,11 @@ int64_t dsft_plan_launches_per_execute(const dsft_plan* plan);
 #define DSFT_KERNEL_CLASSES 5
 dsft_status dsft_plan_set_timing(dsft_plan* plan, int32_t enable);
 dsft_status dsft_plan_collect_times(dsft_plan* plan, double* ms_out, int64_t* launches_out);
+/* Same events as a timeline (call instead of dsft_plan_collect_times): for the
+ * first min(n, recorded) launches, rows of 3 doubles (kernel class, start ms,
+ * end ms) relative to the first recorded event; returns the number of launches
+ * recorded (may exceed n), or -1 on error.  Clears the record like collect. */
+int64_t dsft_plan_collect_timeline(dsft_plan* plan, double* rows_out, int64_t n);
 
 /* ---- multi-GPU (NCCL loaded with dlopen; one process per GPU) ----------
  * dsft_comm_get_unique_id writes NCCL's 128-byte unique id on rank 0; the

@@ -68,6 +68,7 @@ _SIGS = {
     "dsft_plan_k2_specialized": (C.c_int32, [_P, C.c_char_p, C.c_size_t]),
     "dsft_plan_set_timing": (C.c_int, [_P, C.c_int32]),
     "dsft_plan_collect_times": (C.c_int, [_P, C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
+    "dsft_plan_collect_timeline": (C.c_int64, [_P, C.POINTER(C.c_double), C.c_int64]),
     "dsft_comm_get_unique_id": (C.c_int, [_P]),
     "dsft_shard_bands": (None, [C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
     "dsft_comm_create": (C.c_int, [C.c_int32, C.c_int32, _P, C.POINTER(_P)]),
@@ -201,6 +202,14 @@ class Plan:
         n = (C.c_int64 * 5)()
         _check(lib().dsft_plan_collect_times(self._h, ms, n))
         return {k: (ms[i], n[i]) for i, k in enumerate(self.KERNEL_CLASSES)}
+
+    def dsft_plan_collect_timeline(self, n: int = 4096) -> list[tuple[str, float, float]]:
+        """(kernel class, start ms, end ms) per recorded launch, relative to the first."""
+        rows = (C.c_double * (3 * n))()
+        rec = lib().dsft_plan_collect_timeline(self._h, rows, n)
+        if rec < 0:
+            raise DsftError(-1, "dsft_plan_collect_timeline failed")
+        return [(self.KERNEL_CLASSES[int(rows[3 * i])], rows[3 * i + 1], rows[3 * i + 2]) for i in range(min(rec, n))]
 
     def dsft_execute(self, f, freqs_out, coeffs_out, stream=None):
         _check(lib().dsft_execute(self._h, f.data_ptr(), freqs_out.data_ptr(), coeffs_out.data_ptr(),

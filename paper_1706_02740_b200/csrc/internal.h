@@ -32,6 +32,7 @@ namespace dsft {
 constexpr int kMaxShifts = 160;  // 1 + sum_i (r_i - 1) for up to 10 residue primes
 constexpr int kK1TabMax = 32 * 6 * 2;  // J <= 32 with kappa <= 6 in kernel params
 constexpr int64_t kSentinel = INT64_MIN;
+constexpr int kZBufs = 2;        // Z buffers the bucket-prime pipeline rotates through (3: measured worse, L2)
 constexpr int kMaxRadix = 16;    // largest in-register FFT stage radix in K2
 
 // Per-bucket-prime tables (host copy + device pointers into plan->dev_tables).
@@ -111,7 +112,7 @@ struct WsLayout {
   size_t z, zs, cand_w, cand_v, vmask, acc_w, acc_z, acc_r, acc_mask, acc_n, work_n, ticket, work, band_w, band_c,
       band_z, band_m, band_n, band_nz, total;
   int64_t z_vec;     // complex128 elements per vector in Z:        J * max_t S_t P_t
-  int64_t z_buf;     // elements per Z buffer (nvec * z_vec); two buffers (prime parity)
+  int64_t z_buf;     // elements per Z buffer (nvec * z_vec); kZBufs buffers (prime t uses t % kZBufs)
   // zs: K2 split-mode scratch (one Z buffer, only when some bucket prime is split)
   int64_t cw_vec;    // elements per vector in cand_w / acc_w / acc_z: J * sum_t P_t
   int64_t band_vec;  // elements per vector in band_w / band_c / band_z: J * budget

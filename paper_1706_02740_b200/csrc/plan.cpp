@@ -235,7 +235,7 @@ WsLayout ws_layout(const Plan& p, int64_t nvec) {
     return at;
   };
   L.z_buf = nvec * L.z_vec;
-  L.z = take((size_t)2 * L.z_buf * 16);
+  L.z = take((size_t)kZBufs * L.z_buf * 16);
   L.zs = take(p.any_split ? (size_t)L.z_buf * 16 : 0);
   L.cand_w = take((size_t)nvec * L.cw_vec * 8);
   L.cand_v = take((size_t)nvec * L.cw_vec * p.Kmax * 16);
@@ -779,14 +779,21 @@ inline cudaError_t timed(Plan& p, int cls, cudaStream_t st, F&& launch) {
 }
 
 // The stream-ordered pipeline for `nv` vectors (<= ws_batch) and a band list.
-// Bucket primes alternate between two Z buffers and three streams: K1 (HBM-
+// Bucket primes rotate through kZBufs Z buffers and three streams: K1 (HBM-
 // bound window gather) on the plan's `aux` stream, K2 (FP64 / shared-memory
 // bound) on the caller's stream, K3 (latency bound) on `aux3`.  Dependencies:
-// K2(t) after K1(t); K3(t) after K2(t); K1(t+2) after K3(t) (same Z buffer);
-// K45 after every K3.  So K1(t+1) and K3(t-1) overlap K2(t).
+// K2(t) after K1(t); K3(t) after K2(t); K1(t+kZBufs) after K3(t) (same Z
+// buffer); the tail after every K3.  So K1(t+1) and K3(t-1) overlap K2(t).
+// (Three buffers were measured slower: two K1s then contend with K2(0) and the
+// Z working set no longer fits L2; scripts/timeline.py.)
 static dsft_status ensure_pipe(Plan& p) {
-  if (!p.aux) CU(cudaStreamCreateWithFlags(&p.aux, cudaStreamNonBlocking), "create aux stream");
-  if (!p.aux3) CU(cudaStreamCreateWithFlags(&p.aux3, cudaStreamNonBlocking), "create aux3 stream");
+  // K1 and K3 streams at the highest priority: their CTAs are dispatched ahead of
+  // the pending CTAs of the (long, many-wave) K2 launch on the caller's stream,
+  // so K1(t+1) finishes while K2(t) still runs instead of during its last wave.
+  int lo = 0, hi = 0;
+  CU(cudaDeviceGetStreamPriorityRange(&lo, &hi), "stream priority range");
+  if (!p.aux) CU(cudaStreamCreateWithPriority(&p.aux, cudaStreamNonBlocking, hi), "create aux stream");
+  if (!p.aux3) CU(cudaStreamCreateWithPriority(&p.aux3, cudaStreamNonBlocking, hi), "create aux3 stream");
   const size_t need = 3 * (size_t)p.T + 3;
   while (p.pipe_ev.size() < need) {
     cudaEvent_t e;
@@ -809,8 +816,9 @@ static dsft_status run_bands(Plan& p, const double2* f, int64_t ld, int nv, cons
   CU(cudaStreamWaitEvent(a1, evFork, 0), "pipeline fork wait");
   CU(cudaStreamWaitEvent(a3, evFork, 0), "pipeline fork wait");
   auto k1 = [&](int t) -> dsft_status {
-    if (t >= 2) CU(cudaStreamWaitEvent(a1, evK3[t - 2], 0), "K1 waits K3");
-    CU(timed(p, 0, a1, [&] { return launch_k1(p, t, t & 1, f, ld, nv, p.ws, bands, nb, a1); }), "K1 gather_mix launch");
+    if (t >= kZBufs) CU(cudaStreamWaitEvent(a1, evK3[t - kZBufs], 0), "K1 waits K3");
+    CU(timed(p, 0, a1, [&] { return launch_k1(p, t, t % kZBufs, f, ld, nv, p.ws, bands, nb, a1); }),
+       "K1 gather_mix launch");
     CU(cudaEventRecord(evK1[t], a1), "K1 event");
     return DSFT_OK;
   };
@@ -818,10 +826,10 @@ static dsft_status run_bands(Plan& p, const double2* f, int64_t ld, int nv, cons
   for (int t = 0; t < p.T; ++t) {
     if (t + 1 < p.T && (stt = k1(t + 1)) != DSFT_OK) return stt;
     CU(cudaStreamWaitEvent(st, evK1[t], 0), "K2 waits K1");
-    CU(timed(p, 1, st, [&] { return launch_k2(p, t, t & 1, nv, p.ws, bands, nb, st); }), "K2 prime_dft launch");
+    CU(timed(p, 1, st, [&] { return launch_k2(p, t, t % kZBufs, nv, p.ws, bands, nb, st); }), "K2 prime_dft launch");
     CU(cudaEventRecord(evK2[t], st), "K2 event");
     CU(cudaStreamWaitEvent(a3, evK2[t], 0), "K3 waits K2");
-    CU(timed(p, 2, a3, [&] { return launch_k3(p, t, t & 1, nv, p.ws, bands, nb, a3); }), "K3 identify launch");
+    CU(timed(p, 2, a3, [&] { return launch_k3(p, t, t % kZBufs, nv, p.ws, bands, nb, a3); }), "K3 identify launch");
     CU(cudaEventRecord(evK3[t], a3), "K3 event");
   }
   CU(cudaEventRecord(evJoin1, a1), "pipeline join");
@@ -907,6 +915,23 @@ dsft_status dsft_plan_collect_times(dsft_plan* pl, double* ms_out, int64_t* laun
   }
   p.ev_used = 0;
   return DSFT_OK;
+}
+
+int64_t dsft_plan_collect_timeline(dsft_plan* pl, double* rows, int64_t n) {
+  if (!pl || (!rows && n > 0)) return -1;
+  Plan& p = pl->p;
+  const int64_t rec = (int64_t)p.ev_used;
+  for (int64_t i = 0; i < rec && i < n; ++i) {
+    if (cudaEventSynchronize(p.ev_pool[2 * i + 1]) != cudaSuccess) return -1;
+    float a = 0.f, b = 0.f;
+    if (cudaEventElapsedTime(&a, p.ev_pool[0], p.ev_pool[2 * i]) != cudaSuccess) return -1;
+    if (cudaEventElapsedTime(&b, p.ev_pool[0], p.ev_pool[2 * i + 1]) != cudaSuccess) return -1;
+    rows[3 * i] = p.ev_class[i];
+    rows[3 * i + 1] = a;
+    rows[3 * i + 2] = b;
+  }
+  p.ev_used = 0;
+  return rec;
 }
 
 int64_t dsft_plan_launches_per_execute(const dsft_plan* pl) {
