@@ -163,8 +163,9 @@ int64_t dsft_plan_launches_per_execute(const dsft_plan* plan);
 /* Optional per-kernel timing.  When enabled, every launch is bracketed by a
  * CUDA event pair recorded on the launching stream.  dsft_plan_collect_times
  * waits for those events and returns, per kernel class (0 K1 gather_mix,
- * 1 K2 prime_dft, 2 K3 identify, 3 K45 vote_estimate, 4 K6 merge), the summed
- * milliseconds and launch counts since the previous collect. */
+ * 1 K2 prime_dft (split mode: K2a + K2b), 2 K3 identify + vote, 3 K5 scan /
+ * medians / band select + K6 merge, 4 unused), the summed milliseconds and
+ * launch counts since the previous collect. */
 #define DSFT_KERNEL_CLASSES 5
 dsft_status dsft_plan_set_timing(dsft_plan* plan, int32_t enable);
 dsft_status dsft_plan_collect_times(dsft_plan* plan, double* ms_out, int64_t* launches_out);

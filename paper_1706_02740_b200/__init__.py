@@ -192,7 +192,7 @@ class Plan:
         n = lib().dsft_plan_k2_specialized(self._h, buf, 512)
         return int(n), buf.value.decode()
 
-    KERNEL_CLASSES = ("k1_gather_mix", "k2_prime_dft", "k3_identify", "k45_vote_estimate", "k6_merge")
+    KERNEL_CLASSES = ("k1_gather_mix", "k2_prime_dft", "k3_identify_vote", "k5_estimate_merge", "k6_unused")
 
     def dsft_plan_set_timing(self, enable: bool):
         _check(lib().dsft_plan_set_timing(self._h, 1 if enable else 0))
