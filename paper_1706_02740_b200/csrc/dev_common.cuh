@@ -48,6 +48,11 @@ __device__ __forceinline__ uint64_t l2_evict_first() {
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
+__device__ __forceinline__ uint64_t l2_evict_normal() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
 __device__ __forceinline__ uint64_t l2_evict_last() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
@@ -164,6 +169,42 @@ __device__ __forceinline__ void dft_composite(double2 (&x)[A * B]) {
   for (int i = 0; i < R; ++i) x[i] = out[i];
 }
 
+__host__ __device__ constexpr int gcd_c(int a, int b) { return b == 0 ? a : gcd_c(b, a % b); }
+__host__ __device__ constexpr int inv_mod_c(int a, int m) {
+  for (int x = 1; x < m; ++x)
+    if ((a * x) % m == 1) return x;
+  return 0;
+}
+
+// Coprime R = A * B (Good-Thomas prime-factor algorithm inside registers): no
+// twiddles; input n = (B n1 + A n2) mod R, output k = (e1 k1 + e2 k2) mod R with
+// the CRT idempotents e1 (= 1 mod A, 0 mod B) and e2 (= 0 mod A, 1 mod B).
+template <int A, int B>
+__device__ __forceinline__ void dft_pfa(double2 (&x)[A * B]) {
+  constexpr int R = A * B;
+  constexpr int e1 = (B * inv_mod_c(B % A, A)) % R;
+  constexpr int e2 = (A * inv_mod_c(A % B, B)) % R;
+  double2 t[R];
+#pragma unroll
+  for (int n2 = 0; n2 < B; ++n2) {
+    double2 col[A];
+#pragma unroll
+    for (int n1 = 0; n1 < A; ++n1) col[n1] = x[(B * n1 + A * n2) % R];
+    dft<A>(col);
+#pragma unroll
+    for (int k1 = 0; k1 < A; ++k1) t[B * k1 + n2] = col[k1];
+  }
+#pragma unroll
+  for (int k1 = 0; k1 < A; ++k1) {
+    double2 row[B];
+#pragma unroll
+    for (int n2 = 0; n2 < B; ++n2) row[n2] = t[B * k1 + n2];
+    dft<B>(row);
+#pragma unroll
+    for (int k2 = 0; k2 < B; ++k2) x[(k1 * e1 + k2 * e2) % R] = row[k2];
+  }
+}
+
 template <int R>
 __device__ __forceinline__ void dft(double2 (&x)[R]) {
   if constexpr (R == 1) {
@@ -194,7 +235,11 @@ __device__ __forceinline__ void dft(double2 (&x)[R]) {
     dft_odd<R>(x);
   } else {
     constexpr int A = first_factor(R);
-    dft_composite<A, R / A>(x);
+#ifndef DSFT_NO_PFA
+    if constexpr (gcd_c(A, R / A) == 1) dft_pfa<A, R / A>(x);
+    else
+#endif
+      dft_composite<A, R / A>(x);
   }
 }
 

@@ -807,7 +807,9 @@ static dsft_status run_bands(Plan& p, const double2* f, int64_t ld, int nv, cons
                              cudaStream_t st, int64_t* freqs = nullptr, double2* coeffs = nullptr) {
   dsft_status stt = ensure_pipe(p);
   if (stt != DSFT_OK) return stt;
-  cudaStream_t a1 = p.aux, a3 = p.aux3;
+  const char* ser = getenv("DSFT_SERIAL");  // experiment knob: every launch on the caller's stream
+  const bool serial = ser && strcmp(ser, "1") == 0;
+  cudaStream_t a1 = serial ? st : p.aux, a3 = serial ? st : p.aux3;
   cudaEvent_t* evK1 = p.pipe_ev.data();            // [T] K1(t) done (aux)
   cudaEvent_t* evK2 = p.pipe_ev.data() + p.T;      // [T] K2(t) done (st)
   cudaEvent_t* evK3 = p.pipe_ev.data() + 2 * p.T;  // [T] K3(t) done (aux3)
