@@ -15,6 +15,7 @@ Readings R1..R12 are listed in DESIGN.md §3.
 
 from __future__ import annotations
 
+import itertools
 import math
 from dataclasses import dataclass, field
 
@@ -104,6 +105,29 @@ def passband_plan(N: int, alpha: float) -> tuple[int, int, list[int]]:
     return w, J, q
 
 
+RESIDUE_PRIME_MAX = 31
+
+
+def residue_moduli(P: int, N: int) -> list[int]:
+    """Reading R8: the residue primes r_i of bucket prime P are the
+    set of distinct odd primes below min(P, 32) with P * prod r_i >= N (so the CRT
+    window q + B of N integers holds exactly one representative)
+    that minimises the extra measurement rows sum_i (r_i - 1) per bucket; ties ->
+    fewer primes, then the lexicographically smallest ascending list.  At least one."""
+    need = -(-N // P)
+    cands = [r for r in odd_primes() if r <= RESIDUE_PRIME_MAX and r < P]
+    best = None
+    for k in range(1, len(cands) + 1):
+        for combo in itertools.combinations(cands, k):
+            if math.prod(combo) >= need:
+                key = (sum(r - 1 for r in combo), k, combo)
+                if best is None or key < best:
+                    best = key
+    if best is None:
+        raise ConfigError("no set of residue primes below the bucket prime reaches N")
+    return list(best[2])
+
+
 def derive_plan(N: int, s: int, params: OracleParams | None = None) -> Plan:
     """Derive every parameter Algorithm 1 needs."""
     p = params or OracleParams()
@@ -161,18 +185,7 @@ def derive_plan(N: int, s: int, params: OracleParams | None = None) -> Plan:
     if len(pool) < T:
         raise ConfigError(f"bucket-prime pool has {len(pool)} < T={T} primes")
     primes = draw_distinct(pool, T, p.seed)
-    rp = odd_primes()
-    residues = []
-    for P in primes:
-        rs = []
-        prod = P
-        while prod < N or not rs:          # R8: at least one residue prime
-            r = rp[len(rs)]
-            rs.append(r)
-            prod *= r
-        if rs[-1] >= P:
-            raise ConfigError("residue primes must be smaller than the bucket primes")
-        residues.append(rs)
+    residues = [residue_moduli(P, N) for P in primes]
     if not (1 <= p.vote_min <= T):
         raise ConfigError("vote_min must lie in [1, T]")
     budget = int(p.band_budget) if p.band_budget > 0 else s

@@ -344,18 +344,41 @@ static dsft_status derive(int64_t N, int64_t s, const dsft_params& prm, Plan& P)
   for (int t = 0; t < T; ++t) {
     Bucket& b = P.bk[t];
     b.P = primes[t];
-    // residue primes: smallest consecutive odd primes with P prod r >= N, at least one (R8)
-    int K = 0;
-    __int128 prod = b.P;
-    while (prod < N || K == 0) {
-      if (K >= DSFT_MAX_K) return fail(DSFT_ERR_UNSUPPORTED, "more than DSFT_MAX_K residue primes");
-      b.r[K] = (int)odd[K];
-      prod *= odd[K];
-      ++K;
+    // residue primes (reading R8): the set of distinct odd primes below min(P, 32) with
+    // P prod r >= N minimising sum (r - 1) (extra shift rows), ties -> fewer primes,
+    // then lexicographically smallest; at least one
+    {
+      std::vector<int64_t> cand;
+      for (int64_t pr : odd)
+        if (pr <= 31 && pr < b.P) cand.push_back(pr);
+      const int64_t need = (N + b.P - 1) / b.P;
+      const int nc = (int)cand.size();
+      std::vector<int64_t> best;
+      int64_t best_sum = -1;
+      for (uint32_t mask = 1; mask < (1u << nc); ++mask) {
+        __int128 prod = 1;
+        int64_t sum = 0;
+        std::vector<int64_t> set;
+        for (int i = 0; i < nc; ++i)
+          if (mask >> i & 1) {
+            prod *= cand[i];
+            sum += cand[i] - 1;
+            set.push_back(cand[i]);
+          }
+        if (prod < need) continue;
+        const bool better = best_sum < 0 || sum < best_sum ||
+                            (sum == best_sum && (set.size() < best.size() || (set.size() == best.size() && set < best)));
+        if (better) {
+          best = set;
+          best_sum = sum;
+        }
+      }
+      if (best.empty()) return fail(DSFT_ERR_CONFIG, "no set of residue primes below the bucket prime reaches N");
+      if ((int)best.size() > DSFT_MAX_K) return fail(DSFT_ERR_UNSUPPORTED, "more than DSFT_MAX_K residue primes");
+      b.K = (int)best.size();
+      for (int i = 0; i < b.K; ++i) b.r[i] = (int)best[i];
     }
-    b.K = K;
-    if (b.r[K - 1] >= b.P) return fail(DSFT_ERR_CONFIG, "residue primes must be smaller than the bucket primes");
-    if (b.r[K - 1] > 31) return fail(DSFT_ERR_UNSUPPORTED, "residue prime > 31");
+    const int K = b.K;
     // shifts: sigma 0 = P-subgrid (n2 = 0 of every residue grid), then (i, n2 >= 1)
     int S = 1;
     b.shift_r[0] = 1;

@@ -117,15 +117,43 @@ def test_draw_is_distinct_sorted_seeded():
     assert a == sorted(work[:5])
 
 
-def test_residue_rule():
-    p = derive_plan(2**26, 1000, OracleParams(seed=3))
+def _brute_residues(P, N):
+    """Independent brute force of reading R8: depth-first over ascending subsets of
+    the odd primes below min(P, 32); minimise (sum(r - 1), count, lexicographic)."""
+    ps = [r for r in range(3, 32) if all(r % d for d in range(2, r)) and r < P]
+    best = []
+
+    def dfs(i, chosen, prod):
+        if prod * P >= N and chosen:
+            key = (sum(r - 1 for r in chosen), len(chosen), tuple(chosen))
+            if not best or key < best[0]:
+                best[:] = [key]
+        for k in range(i, len(ps)):
+            dfs(k + 1, chosen + [ps[k]], prod * ps[k])
+
+    dfs(0, [], 1)
+    return list(best[0][2]) if best else None
+
+
+@pytest.mark.parametrize("N,s,seed", [(2**26, 1000, 3), (2**26, 1000, 0), (2**22, 50, 1), (4096, 8, 0),
+                                      (6000011, 100, 2), (2**24, 256, 5), (2**21, 4000, 1), (64, 4, 0)])
+def test_residue_rule(N, s, seed):
+    """Reading R8: the CRT window is unique (P prod r >= N) with the fewest extra
+    measurement rows sum (r - 1); checked against an independent brute force."""
+    p = derive_plan(N, s, OracleParams(seed=seed))
     for P, rs in zip(p.primes, p.residues):
-        prod = P
-        for r in rs:
-            prod *= r
-        assert prod >= p.N and prod // rs[-1] < p.N  # smallest such K
-        assert rs == [3, 5, 7, 11, 13, 17, 19, 23][:len(rs)]
-        assert all(r < P for r in rs)
+        assert math.prod(rs) * P >= N
+        assert rs == sorted(rs) and all(r < P for r in rs) and len(set(rs)) == len(rs)
+        assert rs == _brute_residues(P, N)
+
+
+def test_residue_rule_headline_values():
+    """BASELINE config 2 (N = 2^26, s = 1000, seed 0): P = 4051, 4057, 4357 need
+    prod r >= 16567, 16542, 15403 -> {3,5,7,11,17} (38 extra rows) rather than the
+    consecutive {3,...,17} (50); P = 4951, 7561 -> {3,5,7,11,13}."""
+    p = derive_plan(2**26, 1000, OracleParams(seed=0))
+    assert p.primes == [4051, 4057, 4357, 4951, 7561]
+    assert p.residues == [[3, 5, 7, 11, 17]] * 3 + [[3, 5, 7, 11, 13]] * 2
 
 
 @pytest.mark.parametrize("bad", [
