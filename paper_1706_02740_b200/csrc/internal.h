@@ -32,7 +32,10 @@ namespace dsft {
 constexpr int kMaxShifts = 160;  // 1 + sum_i (r_i - 1) for up to 10 residue primes
 constexpr int kK1TabMax = 32 * 6 * 2;  // J <= 32 with kappa <= 6 in kernel params
 constexpr int64_t kSentinel = INT64_MIN;
-constexpr int kZBufs = 2;        // Z buffers the bucket-prime pipeline rotates through (3: measured worse, L2)
+#ifndef DSFT_ZBUFS
+#define DSFT_ZBUFS 2
+#endif
+constexpr int kZBufs = DSFT_ZBUFS;        // Z buffers the bucket-prime pipeline rotates through (3: measured worse, L2)
 constexpr int kMaxRadix = 16;    // largest in-register FFT stage radix in K2
 
 // Per-bucket-prime tables (host copy + device pointers into plan->dev_tables).

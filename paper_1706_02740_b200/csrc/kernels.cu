@@ -1048,7 +1048,10 @@ __device__ void merge_range(const K6Params& p, int v, int64_t e_lo, int64_t e_hi
   const int64_t hi = e_hi < (n > p.s ? n : p.s) ? e_hi : (n > p.s ? n : p.s);
   const bool staged = n <= kK6Stage && e_lo < n;  // CTA-uniform
   if (staged) {
-    for (int64_t i = threadIdx.x; i < n; i += kK6Threads) {
+#pragma unroll
+    for (int it = 0; it < kK6Stage / kK6Threads; ++it) {  // fixed trip: loads in flight together
+      const int64_t i = threadIdx.x + it * kK6Threads;
+      if (i >= n) continue;
       int lo = 0, hb = p.nb;  // block of flat entry i: largest b with pre[b] <= i
       while (hb - lo > 1) {
         const int mid = (lo + hb) >> 1;
