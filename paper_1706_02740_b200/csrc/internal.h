@@ -83,6 +83,7 @@ struct Plan {
   bool any_split = false;            // some bucket uses the K2 split mode
   int64_t sumP = 0, maxSP = 0;
   Bucket bk[DSFT_MAX_T];
+  int order[DSFT_MAX_T] = {};   // processing order of the bucket primes (plan.cpp choose_order)
   std::vector<double> k1tab;   // [J][kappa][2] cos/sin(q_j u 2pi/N), u = 1..kappa
   std::vector<double> ctab;    // [kappa+1] exp(-u^2 h^2 / (2 c1^2)), h = 2 pi / N
   double* k1tab_dev = nullptr;
@@ -129,7 +130,7 @@ cudaError_t launch_k1(const Plan& p, int t, int zb, const double2* f, int64_t ld
 cudaError_t launch_k2(const Plan& p, int t, int zb, int nvec, void* ws, const int* band_list, int nbands,
                       cudaStream_t st);
 cudaError_t launch_k3(const Plan& p, int t, int zb, int nvec, void* ws, const int* band_list, int nbands,
-                      cudaStream_t st);
+                      cudaStream_t st, const int* prev, int nprev);
 // K4..K6 in one cooperative launch; freqs == nullptr: no merge (sharded path merges
 // after the allgather with launch_k6_blocks)
 cudaError_t launch_k45(const Plan& p, int nvec, void* ws, const int* band_list, int nbands, cudaStream_t st,

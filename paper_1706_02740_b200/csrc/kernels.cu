@@ -641,6 +641,8 @@ struct K3Params {
   int64_t cw_vec_stride;  // elements per vector in cand_w (nb * sumP)
   int64_t sumP, off;
   int t;                  // this bucket prime's index
+  int nprev;              // bucket primes processed before this one (plan order) ...
+  int prev[DSFT_MAX_T];   // ... in processing order
   int64_t Pt[DSFT_MAX_T], offt[DSFT_MAX_T];  // all bucket primes and their slot offsets
   int32_t* vmask;         // [vec][band][sum_t P_t] vote mask per candidate slot (reading R9)
 };
@@ -712,17 +714,20 @@ __global__ void __launch_bounds__(256) k3_identify(const __grid_constant__ K3Par
   if (ok) {
     double2* cv = p.cand_v + slot * p.Kmax;
     for (int i = 0; i < p.K; ++i) cv[i] = yv[i];
-    // Vote (reading R9), incrementally over the bucket primes in order: the owner
-    // of omega in this band is the smallest prime that produced it; K3 of every
-    // later producing prime ORs its bit into the owner's mask (K3 launches are
-    // sequential, so the earlier primes' candidates are final here).
+    // Vote (reading R9), incrementally over the bucket primes in processing order:
+    // the mask of omega in this band lives on the slot of the first processed prime
+    // that produced it; K3 of every later producing prime ORs its bit into that
+    // mask (K3 launches are sequential, so the earlier primes' candidates are final
+    // here).  The accepted set and the masks do not depend on the order.
     const int64_t bb = (int64_t)v * p.cw_vec_stride + (int64_t)j * p.sumP;
     int t0 = p.t;
-    for (int t2 = 0; t2 < p.t; ++t2)
+    for (int k = 0; k < p.nprev; ++k) {
+      const int t2 = p.prev[k];
       if (__ldcg(p.cand_w + bb + p.offt[t2] + pmod(om, p.Pt[t2])) == om) {
         t0 = t2;
         break;
       }
+    }
     if (t0 == p.t) mk = 1 << p.t;
     else atomicOr(p.vmask + bb + p.offt[t0] + pmod(om, p.Pt[t0]), 1 << p.t);
   }
@@ -1370,7 +1375,8 @@ cudaError_t launch_k2(const Plan& p, int t, int zb, int nvec, void* ws, const in
   return cudaGetLastError();
 }
 
-cudaError_t launch_k3(const Plan& p, int t, int zb, int nvec, void* ws, const int* bands, int nbands, cudaStream_t st) {
+cudaError_t launch_k3(const Plan& p, int t, int zb, int nvec, void* ws, const int* bands, int nbands, cudaStream_t st,
+                      const int* prev, int nprev) {
   const Bucket& b = p.bk[t];
   const WsLayout L = ws_layout(p, p.ws_batch);
   K3Params k{};
@@ -1398,6 +1404,8 @@ cudaError_t launch_k3(const Plan& p, int t, int zb, int nvec, void* ws, const in
   k.B_hi = p.B_hi;
   k.gpow = b.gpow;
   k.t = t;
+  k.nprev = nprev;
+  for (int i = 0; i < nprev; ++i) k.prev[i] = prev[i];
   for (int t2 = 0; t2 < p.T; ++t2) {
     k.Pt[t2] = p.bk[t2].P;
     k.offt[t2] = p.bk[t2].off;

@@ -594,6 +594,38 @@ static void specialise_k2(Plan& P) {
     }
 }
 
+// Processing order of the bucket primes (results do not depend on it: K3's vote is
+// order-free): by K1/K3 work S_t P_t ascending.  (Measured at BASELINE config 2,
+// six orders: ascending is best; moving the largest prime, whose K2 runs one CTA
+// per SM, next to the concurrent K1/K3 work slowed it by up to 37 %.)
+// DSFT_ORDER="i,j,..." overrides (experiments).
+static void choose_order(Plan& P) {
+  std::vector<int> ord(P.T);
+  for (int t = 0; t < P.T; ++t) ord[t] = t;
+  std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) {
+    return (int64_t)P.bk[a].S * P.bk[a].P < (int64_t)P.bk[b].S * P.bk[b].P;
+  });
+  if (const char* env = getenv("DSFT_ORDER")) {
+    std::vector<int> o;
+    std::string tok;
+    for (const char* c = env;; ++c) {
+      if (*c == ',' || *c == 0) {
+        if (!tok.empty()) o.push_back(atoi(tok.c_str()));
+        tok.clear();
+        if (!*c) break;
+      } else {
+        tok += *c;
+      }
+    }
+    std::vector<int> chk = o;
+    std::sort(chk.begin(), chk.end());
+    bool ok = (int)o.size() == P.T;
+    for (int i = 0; ok && i < P.T; ++i) ok = chk[i] == i;
+    if (ok) ord = o;
+  }
+  for (int k = 0; k < P.T; ++k) P.order[k] = ord[k];
+}
+
 // =============================================================== ABI: basics
 extern "C" {
 
@@ -646,6 +678,7 @@ dsft_status dsft_plan_create(int64_t N, int64_t s, const dsft_params* params, ds
     delete pl;
     return cuda_fail(e, "kernels_init");
   }
+  choose_order(pl->p);
 
   st = upload_tables(pl->p);
   if (st != DSFT_OK) {
@@ -840,22 +873,26 @@ static dsft_status run_bands(Plan& p, const double2* f, int64_t ld, int nv, cons
   CU(cudaEventRecord(evFork, st), "pipeline fork");
   CU(cudaStreamWaitEvent(a1, evFork, 0), "pipeline fork wait");
   CU(cudaStreamWaitEvent(a3, evFork, 0), "pipeline fork wait");
-  auto k1 = [&](int t) -> dsft_status {
-    if (t >= kZBufs) CU(cudaStreamWaitEvent(a1, evK3[t - kZBufs], 0), "K1 waits K3");
-    CU(timed(p, 0, a1, [&] { return launch_k1(p, t, t % kZBufs, f, ld, nv, p.ws, bands, nb, a1); }),
+  // k: processing position; t = p.order[k]: bucket prime; Z buffer k % kZBufs
+  auto k1 = [&](int k) -> dsft_status {
+    const int t = p.order[k];
+    if (k >= kZBufs) CU(cudaStreamWaitEvent(a1, evK3[k - kZBufs], 0), "K1 waits K3");
+    CU(timed(p, 0, a1, [&] { return launch_k1(p, t, k % kZBufs, f, ld, nv, p.ws, bands, nb, a1); }),
        "K1 gather_mix launch");
-    CU(cudaEventRecord(evK1[t], a1), "K1 event");
+    CU(cudaEventRecord(evK1[k], a1), "K1 event");
     return DSFT_OK;
   };
   if ((stt = k1(0)) != DSFT_OK) return stt;
-  for (int t = 0; t < p.T; ++t) {
-    if (t + 1 < p.T && (stt = k1(t + 1)) != DSFT_OK) return stt;
-    CU(cudaStreamWaitEvent(st, evK1[t], 0), "K2 waits K1");
-    CU(timed(p, 1, st, [&] { return launch_k2(p, t, t % kZBufs, nv, p.ws, bands, nb, st); }), "K2 prime_dft launch");
-    CU(cudaEventRecord(evK2[t], st), "K2 event");
-    CU(cudaStreamWaitEvent(a3, evK2[t], 0), "K3 waits K2");
-    CU(timed(p, 2, a3, [&] { return launch_k3(p, t, t % kZBufs, nv, p.ws, bands, nb, a3); }), "K3 identify launch");
-    CU(cudaEventRecord(evK3[t], a3), "K3 event");
+  for (int k = 0; k < p.T; ++k) {
+    const int t = p.order[k];
+    if (k + 1 < p.T && (stt = k1(k + 1)) != DSFT_OK) return stt;
+    CU(cudaStreamWaitEvent(st, evK1[k], 0), "K2 waits K1");
+    CU(timed(p, 1, st, [&] { return launch_k2(p, t, k % kZBufs, nv, p.ws, bands, nb, st); }), "K2 prime_dft launch");
+    CU(cudaEventRecord(evK2[k], st), "K2 event");
+    CU(cudaStreamWaitEvent(a3, evK2[k], 0), "K3 waits K2");
+    CU(timed(p, 2, a3, [&] { return launch_k3(p, t, k % kZBufs, nv, p.ws, bands, nb, a3, p.order, k); }),
+       "K3 identify launch");
+    CU(cudaEventRecord(evK3[k], a3), "K3 event");
   }
   CU(cudaEventRecord(evJoin1, a1), "pipeline join");
   CU(cudaEventRecord(evJoin3, a3), "pipeline join");
