@@ -66,6 +66,9 @@ struct Bucket {
   // device pointers
   uint16_t* dlog = nullptr;     // [P] discrete log base g (dlog[0] unused; parity hooks)
   uint16_t* gpow = nullptr;     // [M] g^q mod P: node / bin of Rader position q
+  int* shift_r_dev = nullptr;   // [S] K1 shift tables (copies of shift_r, shift_n2, 2 pi / (N P r))
+  int* shift_n2_dev = nullptr;
+  double* shift_scale_dev = nullptr;
   double2* bhat = nullptr;      // [R_last][M/R_last] FFT_M(b)/M, DIF output position blk*R_last + c stored
                                 // at c*(M/R_last) + blk; b_m = exp(-2 pi i g^-m / P)
   double2* tw = nullptr;        // [ntw] per DIF stage s (span n_s, m_s = n_s/R_s): exp(-2 pi i k / n_s), k < m_s;
@@ -84,6 +87,13 @@ struct Plan {
   int64_t sumP = 0, maxSP = 0;
   Bucket bk[DSFT_MAX_T];
   int order[DSFT_MAX_T] = {};   // processing order of the bucket primes (plan.cpp choose_order)
+  // K1 schedule: k1_groups[g] consecutive primes (in processing order) per K1 launch.
+  // One group per prime = the two-buffer pipeline (Z buffer k mod 2); otherwise every
+  // prime has its own Z region (z_off) and K1 launches need not wait for K3.
+  int n_k1_groups = 0;
+  int k1_groups[DSFT_MAX_T] = {};
+  int64_t z_off[DSFT_MAX_T] = {};  // per-prime Z region offsets (elements per vector) when grouped
+  int64_t z_tot = 0;
   std::vector<double> k1tab;   // [J][kappa][2] cos/sin(q_j u 2pi/N), u = 1..kappa
   std::vector<double> ctab;    // [kappa+1] exp(-u^2 h^2 / (2 c1^2)), h = 2 pi / N
   double* k1tab_dev = nullptr;
@@ -125,20 +135,22 @@ struct WsLayout {
 WsLayout ws_layout(const Plan& p, int64_t nvec);
 
 // ---- kernel launchers (kernels.cu); all stream-ordered, return cudaError_t
-cudaError_t launch_k1(const Plan& p, int t, int zb, const double2* f, int64_t ld, int nvec, void* ws,
-                      const int* band_list, int nbands, cudaStream_t st);
-cudaError_t launch_k2(const Plan& p, int t, int zb, int nvec, void* ws, const int* band_list, int nbands,
+// K1 over the nodes of nprime bucket primes ts[] (one launch), prime i writing Zs[i]
+cudaError_t launch_k1(const Plan& p, int nprime, const int* ts, double2* const* Zs, const int64_t* zstrides,
+                      const int* keep_l2, const double2* f, int64_t ld, int nvec, const int* band_list, int nbands,
                       cudaStream_t st);
-cudaError_t launch_k3(const Plan& p, int t, int zb, int nvec, void* ws, const int* band_list, int nbands,
-                      cudaStream_t st, const int* prev, int nprev);
+cudaError_t launch_k2(const Plan& p, int t, double2* Z, int64_t zstride, int nvec, void* ws, const int* band_list,
+                      int nbands, cudaStream_t st);
+cudaError_t launch_k3(const Plan& p, int t, const double2* Z, int64_t zstride, int nvec, void* ws,
+                      const int* band_list, int nbands, cudaStream_t st, const int* prev, int nprev);
 // K4..K6 in one cooperative launch; freqs == nullptr: no merge (sharded path merges
 // after the allgather with launch_k6_blocks)
 cudaError_t launch_k45(const Plan& p, int nvec, void* ws, const int* band_list, int nbands, cudaStream_t st,
                        int64_t* freqs, double2* coeffs);
 cudaError_t launch_k6(const Plan& p, int nvec, void* ws, int64_t* freqs, double2* coeffs,
                       cudaStream_t st);
-cudaError_t launch_debug_grid(const Plan& p, int t, int zb, int i, int band, int what, const void* ws,
-                              double2* out, cudaStream_t st);
+cudaError_t launch_debug_grid(const Plan& p, int t, const double2* Z, int i, int band, int what, double2* out,
+                              cudaStream_t st);
 cudaError_t kernels_init();  // one-time attribute setup (dynamic smem limits)
 // jit.cpp: k2_ct<nt, minb, fac...> compiled with NVRTC (cudaKernel_t), or nullptr + *why
 const void* jit_k2(int nt, int minb, const int* fac, int nfac, size_t smem_bytes, std::string* why);

@@ -31,15 +31,25 @@ namespace dsft {
 namespace cg = cooperative_groups;
 
 // =============================================================== K1 gather_mix
+// One launch covers the nodes of one or several bucket primes (all of them when
+// the plan runs K1 once up front): CTAs [cta_off[i], cta_off[i+1]) take prime i.
+struct K1Prime {
+  double2* Z;
+  int64_t z_vec_stride;  // elements per vector in Z
+  int P, S;
+  const uint16_t* gpow;  // [P-1] node n1 = g^q of Rader position q (position P-1: node 0)
+  int keep_l2;           // Z stores with the L2 evict_last policy (consumed next) or evict_first
+  const int* shift_r;    // [S] residue prime of shift sigma (1 for the P-subgrid)   (device tables)
+  const int* shift_n2;   // [S] n2 of shift sigma
+  const double* shift_scale;  // [S] 2 pi / (N L_sigma)
+};
+
 struct K1Params {
   const double2* f;
   int64_t ld;            // elements between vectors
   int64_t N;
-  double2* Z;
-  int64_t z_vec_stride;  // elements per vector in Z
-  int64_t P;
-  int S, nb, kappa, pad_;
-  const uint16_t* gpow;      // [P-1] node n1 = g^q of Rader position q (position P-1: node 0)
+  int nb, kappa, nprime, pad_;
+  int cta_off[DSFT_MAX_T + 1];
   double neg_half_inv_c1sq;  // -1 / (2 c1^2)
   double inv_c1N;            // 1 / (c1 N)
   double h_over_c1sq;        // (2 pi / N) / c1^2
@@ -47,35 +57,41 @@ struct K1Params {
   const double* tab_dev;     // rows of [J][kappa][2] (generic-kappa path)
   int64_t tab_stride;        // doubles between listed bands in tab_dev
   const double* ctab_dev;    // [kappa+1]
-  int shift_r[kMaxShifts];
-  int shift_n2[kMaxShifts];
-  double shift_scale[kMaxShifts];  // 2 pi / (N L_sigma)
   double ctab[8];
   double tab[kK1TabMax];     // [nb][kappa][2] cos/sin(q_j u 2 pi / N) (fast path)
+  K1Prime pr[DSFT_MAX_T];
 };
+
+// prime of this CTA and the CTA's index within that prime's range
+__device__ __forceinline__ int k1_prime(const K1Params& p, int& lb) {
+  int t = 0;
+  while (t + 1 < p.nprime && (int)blockIdx.x >= p.cta_off[t + 1]) ++t;
+  lb = (int)blockIdx.x - p.cta_off[t];
+  return t;
+}
 
 // Node geometry shared by both K1 variants: node (sigma, n1) of bucket prime P
 // is x = -pi + 2 pi k / L, L = P r_sigma, k = (r n1 + P n2) mod L (Good's
 // mapping of the residue grid; sigma = 0 is the P-subgrid).  Thread q of a row
 // computes node n1 = g^q (q < P-1) or n1 = 0 (q = P-1) and stores at q: the row
 // is then already in the Rader order K2 consumes.
-__device__ __forceinline__ int rader_node(const K1Params& p, int q) {
-  return q < (int)p.P - 1 ? (int)__ldg(p.gpow + q) : 0;
+__device__ __forceinline__ int rader_node(const K1Prime& p, int q) {
+  return q < p.P - 1 ? (int)__ldg(p.gpow + q) : 0;
 }
 struct NodeGeo {
   int64_t jp;   // j' = round(kN/L)
   double d0;    // x - y_j'
 };
 
-__device__ __forceinline__ NodeGeo node_geo(const K1Params& p, int sigma, int64_t n1) {
-  const int64_t r = p.shift_r[sigma];
-  const int64_t L = p.P * r;
-  int64_t k = r * n1 + p.P * (int64_t)p.shift_n2[sigma];
+__device__ __forceinline__ NodeGeo node_geo(const K1Prime& p, int64_t N, int sigma, int64_t n1) {
+  const int64_t r = __ldg(p.shift_r + sigma);
+  const int64_t L = (int64_t)p.P * r;
+  int64_t k = r * n1 + (int64_t)p.P * (int64_t)__ldg(p.shift_n2 + sigma);
   if (k >= L) k -= L;
   // j' = round(kN / L): L is odd, so 2kN + L is never an exact multiple tie (R3).
-  const int64_t jp = (2 * k * p.N + L) / (2 * L);
-  const int64_t num0 = k * p.N - jp * L;  // (x - y_j') N L / (2 pi), exact
-  return NodeGeo{jp, (double)num0 * p.shift_scale[sigma]};
+  const int64_t jp = (2 * k * N + L) / (2 * L);
+  const int64_t num0 = k * N - jp * L;  // (x - y_j') N L / (2 pi), exact
+  return NodeGeo{jp, (double)num0 * __ldg(p.shift_scale + sigma)};
 }
 
 // Fast path (KAPPA in {4, 6}): each warp stages the 32 windows of its nodes in
@@ -87,12 +103,12 @@ constexpr int kK1FastThreads = 128;
 
 // j' = round(kN/L) from a double estimate, corrected exactly in integers so
 // that |kN - j'L| <= L/2 (no ties: L odd, R3); returns (j', d0 = x - y_j').
-__device__ __forceinline__ NodeGeo node_geo_fast(const K1Params& p, int sigma, int n1) {
-  const int r = p.shift_r[sigma];
-  const int64_t L = p.P * (int64_t)r;
-  int64_t k = (int64_t)r * n1 + p.P * (int64_t)p.shift_n2[sigma];
+__device__ __forceinline__ NodeGeo node_geo_fast(const K1Prime& p, int64_t N, int sigma, int n1) {
+  const int r = __ldg(p.shift_r + sigma);
+  const int64_t L = (int64_t)p.P * r;
+  int64_t k = (int64_t)r * n1 + (int64_t)p.P * (int64_t)__ldg(p.shift_n2 + sigma);
   if (k >= L) k -= L;
-  const int64_t kN = k * p.N;
+  const int64_t kN = k * N;
   int64_t jp = (int64_t)rint((double)kN / (double)L);
   int64_t num0 = kN - jp * L;
   if (2 * num0 > L) {
@@ -102,7 +118,7 @@ __device__ __forceinline__ NodeGeo node_geo_fast(const K1Params& p, int sigma, i
     --jp;
     num0 += L;
   }
-  return NodeGeo{jp, (double)num0 * p.shift_scale[sigma]};
+  return NodeGeo{jp, (double)num0 * __ldg(p.shift_scale + sigma)};
 }
 
 template <int KAPPA>
@@ -110,13 +126,15 @@ __global__ void __launch_bounds__(kK1FastThreads) k1_gather_mix_fast(const __gri
   constexpr int W = 2 * KAPPA + 1;
   __shared__ double2 s_win[kK1FastThreads / 32][32][W];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nodes = p.S * (int)p.P;
-  const int gid = blockIdx.x * kK1FastThreads + threadIdx.x;
+  int lb;
+  const K1Prime& pp = p.pr[k1_prime(p, lb)];
+  const int nodes = pp.S * pp.P;
+  const int gid = lb * kK1FastThreads + threadIdx.x;
   const bool active = gid < nodes;
   const int v = blockIdx.y;
-  const int sigma = active ? gid / (int)p.P : 0;
-  const int q = active ? gid - sigma * (int)p.P : 0;
-  const NodeGeo g = active ? node_geo_fast(p, sigma, rader_node(p, q)) : NodeGeo{0, 0.0};
+  const int sigma = active ? gid / pp.P : 0;
+  const int q = active ? gid - sigma * pp.P : 0;
+  const NodeGeo g = active ? node_geo_fast(pp, p.N, sigma, rader_node(pp, q)) : NodeGeo{0, 0.0};
   const int N = (int)p.N;
   // window start j' - kappa, or -1 - start for windows that wrap mod N
   int st = (int)g.jp - KAPPA;
@@ -125,7 +143,7 @@ __global__ void __launch_bounds__(kK1FastThreads) k1_gather_mix_fast(const __gri
   {
     const int h = lane >> 4, u = lane & 15;
     const bool lane_on = u < W;
-    const int first = (blockIdx.x * kK1FastThreads + warp * 32);
+    const int first = (lb * kK1FastThreads + warp * 32);
     double2 buf[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
@@ -175,9 +193,9 @@ __global__ void __launch_bounds__(kK1FastThreads) k1_gather_mix_fast(const __gri
   double2 ph = make_double2(cs, sn);
   sincos(p.qstep * d0, &sn, &cs);
   const double2 step = make_double2(cs, sn);
-  const uint64_t pol_z = l2_evict_last();
-  double2* zo = p.Z + (int64_t)v * p.z_vec_stride + (int64_t)sigma * p.P + q;
-  const int64_t band_stride = (int64_t)p.S * p.P;
+  const uint64_t pol_z = pp.keep_l2 ? l2_evict_last() : l2_evict_first();
+  double2* zo = pp.Z + (int64_t)v * pp.z_vec_stride + (int64_t)sigma * pp.P + q;
+  const int64_t band_stride = (int64_t)pp.S * pp.P;
   // two bands per iteration, cos and sin parts in separate accumulators:
   // 8 independent DFMA chains instead of 2 (the FP64 latency, not its
   // throughput, bounded the single-chain loop)
@@ -227,22 +245,24 @@ template <int KAPPA>
 __global__ void __launch_bounds__(256) k1_gather_mix(const __grid_constant__ K1Params p) {
   constexpr int KM = KAPPA > 0 ? KAPPA : 32;
   const int kappa = KAPPA > 0 ? KAPPA : p.kappa;
-  const int64_t nodes = (int64_t)p.S * p.P;
-  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int lb;
+  const K1Prime& pp = p.pr[k1_prime(p, lb)];
+  const int64_t nodes = (int64_t)pp.S * pp.P;
+  const int64_t gid = (int64_t)lb * blockDim.x + threadIdx.x;
   if (gid >= nodes) return;
   const int v = blockIdx.y;
-  const int sigma = (int)(gid / p.P);
-  const int64_t q = gid - (int64_t)sigma * p.P;
-  const int64_t n1 = rader_node(p, (int)q);
-  const int64_t r = p.shift_r[sigma];
-  const int64_t L = p.P * r;
-  int64_t k = r * n1 + p.P * (int64_t)p.shift_n2[sigma];
+  const int sigma = (int)(gid / pp.P);
+  const int64_t q = gid - (int64_t)sigma * pp.P;
+  const int64_t n1 = rader_node(pp, (int)q);
+  const int64_t r = __ldg(pp.shift_r + sigma);
+  const int64_t L = (int64_t)pp.P * r;
+  int64_t k = r * n1 + (int64_t)pp.P * (int64_t)__ldg(pp.shift_n2 + sigma);
   if (k >= L) k -= L;
   const int64_t N = p.N;
   // j' = round(kN / L): L is odd, so 2kN + L is never an exact multiple tie (R3).
   const int64_t jp = (2 * k * N + L) / (2 * L);
   const int64_t num0 = k * N - jp * L;            // (x - y_j') N L / (2 pi), exact
-  const double d0 = (double)num0 * p.shift_scale[sigma];
+  const double d0 = (double)num0 * __ldg(pp.shift_scale + sigma);
 
   // window f_{j'-kappa .. j'+kappa} (indices mod N)
   const double2* fv = p.f + (int64_t)v * p.ld;
@@ -290,8 +310,8 @@ __global__ void __launch_bounds__(256) k1_gather_mix(const __grid_constant__ K1P
   sincos(p.qstep * d0, &sn, &cs);
   const double2 step = make_double2(cs, sn);
 
-  double2* zo = p.Z + (int64_t)v * p.z_vec_stride + (int64_t)sigma * p.P + q;
-  const int64_t band_stride = (int64_t)p.S * p.P;
+  double2* zo = pp.Z + (int64_t)v * pp.z_vec_stride + (int64_t)sigma * pp.P + q;
+  const int64_t band_stride = (int64_t)pp.S * pp.P;
   for (int j = 0; j < p.nb; ++j) {
     double re = P0.x, im = P0.y;
     const double* tb = KAPPA > 0 ? (p.tab + j * KAPPA * 2) : (p.tab_dev + (int64_t)j * p.tab_stride);
@@ -1267,21 +1287,16 @@ cudaError_t kernels_init() {
 
 static int64_t band_q(const Plan& p, int j) { return p.q1 + 2 * p.w * (int64_t)j; }
 
-cudaError_t launch_k1(const Plan& p, int t, int zb, const double2* f, int64_t ld, int nvec, void* ws,
-                      const int* bands, int nbands, cudaStream_t st) {
-  const Bucket& b = p.bk[t];
-  const WsLayout L = ws_layout(p, p.ws_batch);
+cudaError_t launch_k1(const Plan& p, int nprime, const int* ts, double2* const* Zs, const int64_t* zstrides,
+                      const int* keep_l2, const double2* f, int64_t ld, int nvec, const int* bands, int nbands,
+                      cudaStream_t st) {
   K1Params k{};
   k.f = f;
   k.ld = ld;
   k.N = p.N;
-  k.Z = (double2*)((char*)ws + L.z) + zb * L.z_buf;
-  k.z_vec_stride = L.z_vec;
-  k.P = b.P;
-  k.S = b.S;
   k.nb = nbands;
   k.kappa = p.kappa;
-  k.gpow = b.gpow;
+  k.nprime = nprime;
   k.neg_half_inv_c1sq = -1.0 / (2.0 * p.c1 * p.c1);
   k.inv_c1N = 1.0 / (p.c1 * (double)p.N);
   const double h = 2.0 * M_PI / (double)p.N;
@@ -1289,11 +1304,6 @@ cudaError_t launch_k1(const Plan& p, int t, int zb, const double2* f, int64_t ld
   k.qfirst = (double)band_q(p, bands[0]);
   const int stride = nbands > 1 ? bands[1] - bands[0] : 1;
   k.qstep = (double)(2 * p.w * (int64_t)stride);
-  for (int s = 0; s < b.S; ++s) {
-    k.shift_r[s] = b.shift_r[s];
-    k.shift_n2[s] = b.shift_n2[s];
-    k.shift_scale[s] = 2.0 * M_PI / ((double)p.N * (double)(b.P * b.shift_r[s]));
-  }
   // device table: [J][kappa][2] then ctab[kappa+1]; listed band jj is row bands[0] + jj*stride
   k.tab_dev = p.k1tab_dev + (size_t)bands[0] * p.kappa * 2;
   k.tab_stride = (int64_t)stride * p.kappa * 2;
@@ -1305,22 +1315,36 @@ cudaError_t launch_k1(const Plan& p, int t, int zb, const double2* f, int64_t ld
       for (int u = 0; u < p.kappa; ++u)
         for (int c = 0; c < 2; ++c) k.tab[(jj * p.kappa + u) * 2 + c] = p.k1tab[((size_t)bands[jj] * p.kappa + u) * 2 + c];
   }
-  const int64_t nodes = (int64_t)b.S * b.P;
-  if (fast && p.kappa == 6)
-    k1_gather_mix_fast<6><<<dim3(cdiv(nodes, kK1FastThreads), nvec), kK1FastThreads, 0, st>>>(k);
-  else if (fast && p.kappa == 4)
-    k1_gather_mix_fast<4><<<dim3(cdiv(nodes, kK1FastThreads), nvec), kK1FastThreads, 0, st>>>(k);
-  else
-    k1_gather_mix<0><<<dim3(cdiv(nodes, 256), nvec), 256, 0, st>>>(k);
+  const int cta = fast ? kK1FastThreads : 256;
+  k.cta_off[0] = 0;
+  for (int i = 0; i < nprime; ++i) {
+    const Bucket& b = p.bk[ts[i]];
+    K1Prime& q = k.pr[i];
+    q.Z = Zs[i];
+    q.z_vec_stride = zstrides[i];
+    q.P = (int)b.P;
+    q.S = b.S;
+    q.gpow = b.gpow;
+    q.keep_l2 = keep_l2[i];
+    q.shift_r = b.shift_r_dev;
+    q.shift_n2 = b.shift_n2_dev;
+    q.shift_scale = b.shift_scale_dev;
+    k.cta_off[i + 1] = k.cta_off[i] + (int)cdiv((int64_t)b.S * b.P, cta);
+  }
+  const dim3 grid((unsigned)k.cta_off[nprime], nvec);
+  if (fast && p.kappa == 6) k1_gather_mix_fast<6><<<grid, kK1FastThreads, 0, st>>>(k);
+  else if (fast && p.kappa == 4) k1_gather_mix_fast<4><<<grid, kK1FastThreads, 0, st>>>(k);
+  else k1_gather_mix<0><<<grid, 256, 0, st>>>(k);
   return cudaGetLastError();
 }
 
-cudaError_t launch_k2(const Plan& p, int t, int zb, int nvec, void* ws, const int* /*bands*/, int nbands, cudaStream_t st) {
+cudaError_t launch_k2(const Plan& p, int t, double2* Z, int64_t zstride, int nvec, void* ws, const int* /*bands*/,
+                      int nbands, cudaStream_t st) {
   const Bucket& b = p.bk[t];
   const WsLayout L = ws_layout(p, p.ws_batch);
   K2Params k{};
-  k.Z = (double2*)((char*)ws + L.z) + zb * L.z_buf;
-  k.z_vec_stride = L.z_vec;
+  k.Z = Z;
+  k.z_vec_stride = zstride;
   k.P = (int)b.P;
   k.M = b.M;
   k.nfac = b.nfac;
@@ -1375,13 +1399,13 @@ cudaError_t launch_k2(const Plan& p, int t, int zb, int nvec, void* ws, const in
   return cudaGetLastError();
 }
 
-cudaError_t launch_k3(const Plan& p, int t, int zb, int nvec, void* ws, const int* bands, int nbands, cudaStream_t st,
-                      const int* prev, int nprev) {
+cudaError_t launch_k3(const Plan& p, int t, const double2* Z, int64_t zstride, int nvec, void* ws, const int* bands,
+                      int nbands, cudaStream_t st, const int* prev, int nprev) {
   const Bucket& b = p.bk[t];
   const WsLayout L = ws_layout(p, p.ws_batch);
   K3Params k{};
-  k.Z = (const double2*)((char*)ws + L.z) + zb * L.z_buf;
-  k.z_vec_stride = L.z_vec;
+  k.Z = Z;
+  k.z_vec_stride = zstride;
   k.P = b.P;
   k.S = b.S;
   k.nb = nbands;
@@ -1532,12 +1556,12 @@ static int64_t modinv(int64_t a, int64_t m) {
   return 0;
 }
 
-cudaError_t launch_debug_grid(const Plan& p, int t, int zb, int i, int band, int what, const void* ws, double2* out,
+cudaError_t launch_debug_grid(const Plan& p, int t, const double2* Z, int i, int band, int what, double2* out,
                               cudaStream_t st) {
   const Bucket& b = p.bk[t];
   const WsLayout L = ws_layout(p, p.ws_batch);
   DbgParams k{};
-  k.Z = (const double2*)((const char*)ws + L.z) + zb * L.z_buf;
+  k.Z = Z;
   k.dlog = b.dlog;
   k.P = b.P;
   k.r = b.r[i];

@@ -235,7 +235,8 @@ WsLayout ws_layout(const Plan& p, int64_t nvec) {
     return at;
   };
   L.z_buf = nvec * L.z_vec;
-  L.z = take((size_t)kZBufs * L.z_buf * 16);
+  const bool grouped = p.n_k1_groups > 0 && p.n_k1_groups < p.T;
+  L.z = take(grouped ? (size_t)nvec * p.z_tot * 16 : (size_t)kZBufs * L.z_buf * 16);
   L.zs = take(p.any_split ? (size_t)L.z_buf * 16 : 0);
   L.cand_w = take((size_t)nvec * L.cw_vec * 8);
   L.cand_v = take((size_t)nvec * L.cw_vec * p.Kmax * 16);
@@ -338,6 +339,7 @@ static dsft_status derive(int64_t N, int64_t s, const dsft_params& prm, Plan& P)
   P.Kmax = 0;
   P.Smax = 0;
   P.any_split = false;
+  P.z_tot = 0;
   P.sumP = 0;
   P.maxSP = 0;
   int64_t grid_points = 0, nodes = 0;
@@ -410,6 +412,8 @@ static dsft_status derive(int64_t N, int64_t s, const dsft_params& prm, Plan& P)
     b.off = P.sumP;
     P.sumP += b.P;
     P.maxSP = std::max<int64_t>(P.maxSP, (int64_t)S * b.P);
+    P.z_off[t] = P.z_tot;
+    P.z_tot += (int64_t)J * S * b.P;
     P.Kmax = std::max(P.Kmax, K);
     P.Rmax = std::max(P.Rmax, b.r[K - 1]);
     P.Smax = std::max(P.Smax, S);
@@ -491,9 +495,11 @@ static dsft_status upload_tables(Plan& P) {
   // one allocation; per t: dlog [P] uint16 | gpow [M] uint16 | bhat [M] | tw [ntw] (double2);
   // then the K1 tables k1tab [J][kappa][2], ctab [kappa+1]
   size_t bytes = 0;
-  std::vector<size_t> offs(P.T), goff(P.T), cpx(P.T);
+  std::vector<size_t> offs(P.T), goff(P.T), cpx(P.T), soff(P.T);
   for (int t = 0; t < P.T; ++t) {
     const Bucket& b = P.bk[t];
+    soff[t] = bytes;  // K1 shift tables: scale [S] double | r [S] int | n2 [S] int
+    bytes = align256(bytes + (size_t)b.S * 16);
     offs[t] = bytes;
     goff[t] = align256(bytes + (size_t)b.P * 2);
     cpx[t] = align256(goff[t] + (size_t)b.M * 2);
@@ -505,6 +511,16 @@ static dsft_status upload_tables(Plan& P) {
   for (int t = 0; t < P.T; ++t) {
     Bucket& b = P.bk[t];
     const int M = b.M;
+    {
+      double* sc = (double*)(host.data() + soff[t]);
+      int* sr = (int*)(sc + b.S);
+      int* sn = sr + b.S;
+      for (int sg = 0; sg < b.S; ++sg) {
+        sc[sg] = 2.0 * M_PI / ((double)P.N * (double)(b.P * b.shift_r[sg]));
+        sr[sg] = b.shift_r[sg];
+        sn[sg] = b.shift_n2[sg];
+      }
+    }
     uint16_t* dlog = (uint16_t*)(host.data() + offs[t]);
     uint16_t* gpow = (uint16_t*)(host.data() + goff[t]);
     double* bhat = (double*)(host.data() + cpx[t]);
@@ -553,6 +569,9 @@ static dsft_status upload_tables(Plan& P) {
   char* base = (char*)P.dev_tables;
   for (int t = 0; t < P.T; ++t) {
     Bucket& b = P.bk[t];
+    b.shift_scale_dev = (double*)(base + soff[t]);
+    b.shift_r_dev = (int*)(b.shift_scale_dev + b.S);
+    b.shift_n2_dev = b.shift_r_dev + b.S;
     b.dlog = (uint16_t*)(base + offs[t]);
     b.gpow = (uint16_t*)(base + goff[t]);
     b.bhat = (double2*)(base + cpx[t]);
@@ -624,6 +643,35 @@ static void choose_order(Plan& P) {
     if (ok) ord = o;
   }
   for (int k = 0; k < P.T; ++k) P.order[k] = ord[k];
+  // K1 schedule: one launch per prime (two reused Z buffers) unless DSFT_K1GROUPS =
+  // "a,b,..." (consecutive group sizes summing to T; experiments)
+  P.n_k1_groups = P.T;
+  for (int g = 0; g < P.T; ++g) P.k1_groups[g] = 1;
+  if (const char* env = getenv("DSFT_K1GROUPS")) {
+    std::vector<int> gs;
+    int sum = 0, cur = 0;
+    bool any = false;
+    for (const char* c = env;; ++c) {
+      if (*c >= '0' && *c <= '9') {
+        cur = cur * 10 + (*c - '0');
+        any = true;
+      } else {
+        if (any) {
+          gs.push_back(cur);
+          sum += cur;
+        }
+        cur = 0;
+        any = false;
+        if (!*c) break;
+      }
+    }
+    bool ok = sum == P.T && !gs.empty();
+    for (int g : gs) ok = ok && g >= 1;
+    if (ok) {
+      P.n_k1_groups = (int)gs.size();
+      for (size_t g = 0; g < gs.size(); ++g) P.k1_groups[g] = gs[g];
+    }
+  }
 }
 
 // =============================================================== ABI: basics
@@ -873,24 +921,54 @@ static dsft_status run_bands(Plan& p, const double2* f, int64_t ld, int nv, cons
   CU(cudaEventRecord(evFork, st), "pipeline fork");
   CU(cudaStreamWaitEvent(a1, evFork, 0), "pipeline fork wait");
   CU(cudaStreamWaitEvent(a3, evFork, 0), "pipeline fork wait");
-  // k: processing position; t = p.order[k]: bucket prime; Z buffer k % kZBufs
-  auto k1 = [&](int k) -> dsft_status {
-    const int t = p.order[k];
-    if (k >= kZBufs) CU(cudaStreamWaitEvent(a1, evK3[k - kZBufs], 0), "K1 waits K3");
-    CU(timed(p, 0, a1, [&] { return launch_k1(p, t, k % kZBufs, f, ld, nv, p.ws, bands, nb, a1); }),
+  // k: processing position; t = p.order[k]: bucket prime.  Two-buffer pipeline (one
+  // K1 launch per prime): Z buffer k % kZBufs, K1(k) waits for K3(k - kZBufs).
+  // Grouped K1 (every prime its own Z region): one launch per group, no K3 wait.
+  const WsLayout L = ws_layout(p, p.ws_batch);
+  const bool grouped = p.n_k1_groups < p.T;
+  auto zfor = [&](int k, int t, double2*& Z, int64_t& zs) {
+    if (grouped) {
+      Z = (double2*)((char*)p.ws + L.z) + (int64_t)p.ws_batch * p.z_off[t];
+      zs = (int64_t)p.J * p.bk[t].S * p.bk[t].P;
+    } else {
+      Z = (double2*)((char*)p.ws + L.z) + (int64_t)(k % kZBufs) * L.z_buf;
+      zs = L.z_vec;
+    }
+  };
+  int gfirst[DSFT_MAX_T + 1], gof[DSFT_MAX_T];  // first position of group g; group of position k
+  gfirst[0] = 0;
+  for (int g = 0; g < p.n_k1_groups; ++g) {
+    gfirst[g + 1] = gfirst[g] + p.k1_groups[g];
+    for (int k = gfirst[g]; k < gfirst[g + 1]; ++k) gof[k] = g;
+  }
+  auto k1 = [&](int g) -> dsft_status {
+    const int k0 = gfirst[g], n = p.k1_groups[g];
+    if (!grouped && k0 >= kZBufs) CU(cudaStreamWaitEvent(a1, evK3[k0 - kZBufs], 0), "K1 waits K3");
+    int ts[DSFT_MAX_T], keep[DSFT_MAX_T];
+    double2* Zs[DSFT_MAX_T];
+    int64_t zst[DSFT_MAX_T];
+    for (int i = 0; i < n; ++i) {
+      ts[i] = p.order[k0 + i];
+      zfor(k0 + i, ts[i], Zs[i], zst[i]);
+      keep[i] = (!grouped || n == 1) ? 1 : 0;  // a group's Z is read later: do not pin it in L2
+    }
+    CU(timed(p, 0, a1, [&] { return launch_k1(p, n, ts, Zs, zst, keep, f, ld, nv, bands, nb, a1); }),
        "K1 gather_mix launch");
-    CU(cudaEventRecord(evK1[k], a1), "K1 event");
+    CU(cudaEventRecord(evK1[g], a1), "K1 event");
     return DSFT_OK;
   };
   if ((stt = k1(0)) != DSFT_OK) return stt;
   for (int k = 0; k < p.T; ++k) {
     const int t = p.order[k];
-    if (k + 1 < p.T && (stt = k1(k + 1)) != DSFT_OK) return stt;
-    CU(cudaStreamWaitEvent(st, evK1[k], 0), "K2 waits K1");
-    CU(timed(p, 1, st, [&] { return launch_k2(p, t, k % kZBufs, nv, p.ws, bands, nb, st); }), "K2 prime_dft launch");
+    if (k == gfirst[gof[k]] && gof[k] + 1 < p.n_k1_groups && (stt = k1(gof[k] + 1)) != DSFT_OK) return stt;
+    double2* Z;
+    int64_t zs;
+    zfor(k, t, Z, zs);
+    CU(cudaStreamWaitEvent(st, evK1[gof[k]], 0), "K2 waits K1");
+    CU(timed(p, 1, st, [&] { return launch_k2(p, t, Z, zs, nv, p.ws, bands, nb, st); }), "K2 prime_dft launch");
     CU(cudaEventRecord(evK2[k], st), "K2 event");
     CU(cudaStreamWaitEvent(a3, evK2[k], 0), "K3 waits K2");
-    CU(timed(p, 2, a3, [&] { return launch_k3(p, t, k % kZBufs, nv, p.ws, bands, nb, a3, p.order, k); }),
+    CU(timed(p, 2, a3, [&] { return launch_k3(p, t, Z, zs, nv, p.ws, bands, nb, a3, p.order, k); }),
        "K3 identify launch");
     CU(cudaEventRecord(evK3[k], a3), "K3 event");
   }
@@ -1014,9 +1092,13 @@ dsft_status dsft_debug_grid(dsft_plan* pl, const dsft_c128* f_dev, int32_t band,
   if (stt != DSFT_OK) return stt;
   cudaStream_t st = (cudaStream_t)stream;
   int b = band;
-  CU(launch_k1(p, t, 0, (const double2*)f_dev, p.N, 1, p.ws, &b, 1, st), "K1 launch");
-  if (what == 1) CU(launch_k2(p, t, 0, 1, p.ws, &b, 1, st), "K2 launch");
-  CU(launch_debug_grid(p, t, 0, i, 0, what, p.ws, (double2*)out_dev, st), "debug grid launch");
+  const WsLayout L = ws_layout(p, p.ws_batch);
+  double2* Z = (double2*)((char*)p.ws + L.z);  // buffer 0 / prime region 0 (one vector, one band)
+  const int64_t zs = (int64_t)p.bk[t].S * p.bk[t].P;
+  const int keep = 1;
+  CU(launch_k1(p, 1, &t, &Z, &zs, &keep, (const double2*)f_dev, p.N, 1, &b, 1, st), "K1 launch");
+  if (what == 1) CU(launch_k2(p, t, Z, zs, 1, p.ws, &b, 1, st), "K2 launch");
+  CU(launch_debug_grid(p, t, Z, i, 0, what, (double2*)out_dev, st), "debug grid launch");
   return DSFT_OK;
 }
 
