@@ -21,6 +21,7 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <climits>
 #include <cmath>
 
 #include "internal.h"
@@ -121,57 +122,19 @@ __device__ __forceinline__ NodeGeo node_geo_fast(const K1Prime& p, int64_t N, in
   return NodeGeo{jp, (double)num0 * __ldg(p.shift_scale + sigma)};
 }
 
+// Band mix of one node from its window (2 kappa + 1 values at `win`, shared
+// memory): Gaussian taps g(d_u)/N, d_u = d0 - u h, by the recurrence G_u = G_0 E^u
+// C_u (DESIGN.md §6 K1), u <-> -u folded (A_u, D_u), all listed bands, phase
+// e^{i q d0} advanced between bands; stores the node's sample of every band.
 template <int KAPPA>
-__global__ void __launch_bounds__(kK1FastThreads) k1_gather_mix_fast(const __grid_constant__ K1Params p) {
+__device__ __forceinline__ void k1_mix_node(const K1Params& p, const K1Prime& pp, int v, int sigma, int q, double d0,
+                                            const double2* win) {
   constexpr int W = 2 * KAPPA + 1;
-  __shared__ double2 s_win[kK1FastThreads / 32][32][W];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  int lb;
-  const K1Prime& pp = p.pr[k1_prime(p, lb)];
-  const int nodes = pp.S * pp.P;
-  const int gid = lb * kK1FastThreads + threadIdx.x;
-  const bool active = gid < nodes;
-  const int v = blockIdx.y;
-  const int sigma = active ? gid / pp.P : 0;
-  const int q = active ? gid - sigma * pp.P : 0;
-  const NodeGeo g = active ? node_geo_fast(pp, p.N, sigma, rader_node(pp, q)) : NodeGeo{0, 0.0};
-  const int N = (int)p.N;
-  // window start j' - kappa, or -1 - start for windows that wrap mod N (PAPER.md:477)
-  int st = (int)g.jp - KAPPA;
-  if (st < 0 || st + W > N) st = -1 - ((st % N) + N) % N;
-  const double2* fv = p.f + (int64_t)v * p.ld;
-  {
-    const int h = lane >> 4, u = lane & 15;
-    const bool lane_on = u < W;
-    const int first = (lb * kK1FastThreads + warp * 32);
-    double2 buf[16];
-#pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      const int m = 2 * i + h;
-      const int stm = __shfl_sync(0xffffffffu, st, m);
-      if (lane_on && first + m < nodes) {
-        int idx;
-        if (stm >= 0) {
-          idx = stm + u;
-        } else {
-          idx = -1 - stm + u;
-          if (idx >= N) idx -= N;
-        }
-        buf[i] = ld_stream(fv + idx);
-      }
-    }
-#pragma unroll
-    for (int i = 0; i < 16; ++i)
-      if (lane_on) s_win[warp][2 * i + h][u] = buf[i];
-  }
-  __syncwarp();
-  if (!active) return;
   double2 fw[W];
 #pragma unroll
-  for (int u = 0; u < W; ++u) fw[u] = s_win[warp][lane][u];
+  for (int u = 0; u < W; ++u) fw[u] = win[u];
 
   // Gaussian taps g(d_u)/N, d_u = d0 - u h, via G_u = G_0 E^u C_u (DESIGN.md §6 K1)
-  const double d0 = g.d0;
   const double G0 = exp(d0 * d0 * p.neg_half_inv_c1sq) * p.inv_c1N;
   const double E = exp(d0 * p.h_over_c1sq);
   const double Ei = 1.0 / E;
@@ -183,10 +146,10 @@ __global__ void __launch_bounds__(kK1FastThreads) k1_gather_mix_fast(const __gri
     ep *= E;
     em *= Ei;
     const double cu = p.ctab[u];
-    const double2 pp = cscale(fw[KAPPA + u], ep * cu);
-    const double2 pm = cscale(fw[KAPPA - u], em * cu);
-    A[u - 1] = cadd(pp, pm);
-    D[u - 1] = csub(pp, pm);
+    const double2 pu = cscale(fw[KAPPA + u], ep * cu);
+    const double2 mu = cscale(fw[KAPPA - u], em * cu);
+    A[u - 1] = cadd(pu, mu);
+    D[u - 1] = csub(pu, mu);
   }
   double sn, cs;
   sincos(p.qfirst * d0, &sn, &cs);
@@ -237,6 +200,54 @@ __global__ void __launch_bounds__(kK1FastThreads) k1_gather_mix_fast(const __gri
     }
     st_keep(zo + j * band_stride, cmul(make_double2(rc + rs, ic - is), ph), pol_z);
   }
+}
+
+template <int KAPPA>
+__global__ void __launch_bounds__(kK1FastThreads) k1_gather_mix_fast(const __grid_constant__ K1Params p) {
+  constexpr int W = 2 * KAPPA + 1;
+  __shared__ double2 s_win[kK1FastThreads / 32][32][W];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int lb;
+  const K1Prime& pp = p.pr[k1_prime(p, lb)];
+  const int nodes = pp.S * pp.P;
+  const int gid = lb * kK1FastThreads + threadIdx.x;
+  const bool active = gid < nodes;
+  const int v = blockIdx.y;
+  const int sigma = active ? gid / pp.P : 0;
+  const int q = active ? gid - sigma * pp.P : 0;
+  const NodeGeo g = active ? node_geo_fast(pp, p.N, sigma, rader_node(pp, q)) : NodeGeo{0, 0.0};
+  const int N = (int)p.N;
+  // window start j' - kappa, or -1 - start for windows that wrap mod N (PAPER.md:477)
+  int st = (int)g.jp - KAPPA;
+  if (st < 0 || st + W > N) st = -1 - ((st % N) + N) % N;
+  const double2* fv = p.f + (int64_t)v * p.ld;
+  {
+    const int h = lane >> 4, u = lane & 15;
+    const bool lane_on = u < W;
+    const int first = (lb * kK1FastThreads + warp * 32);
+    double2 buf[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int m = 2 * i + h;
+      const int stm = __shfl_sync(0xffffffffu, st, m);
+      if (lane_on && first + m < nodes) {
+        int idx;
+        if (stm >= 0) {
+          idx = stm + u;
+        } else {
+          idx = -1 - stm + u;
+          if (idx >= N) idx -= N;
+        }
+        buf[i] = ld_stream(fv + idx);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 16; ++i)
+      if (lane_on) s_win[warp][2 * i + h][u] = buf[i];
+  }
+  __syncwarp();
+  if (!active) return;
+  k1_mix_node<KAPPA>(p, pp, v, sigma, q, g.d0, &s_win[warp][lane][0]);
 }
 
 // KAPPA > 0: compile-time window, table in kernel parameters (constant bank).

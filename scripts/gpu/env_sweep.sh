@@ -1,7 +1,7 @@
 # Bench a list of environment settings (e.g. "DSFT_K1GROUPS=1,4").  Usage: bash scripts/gpu/env_sweep.sh "A=1" "B=2" ...
 cd "$GRAFT_REPO_ROOT"; mkdir -p gpurun_out
 for rep in 1 2; do for e in "NONE=0" "$@"; do
-env "$e" timeout 600 python bench.py --steps 30 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/envsw.json 2>&1
+env $e timeout 600 python bench.py --steps 30 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/envsw.json 2>&1
 python - "gpurun_out/envsw.json" "$e" <<'PY'
 import json,sys
 l=[x for x in open(sys.argv[1]) if x.startswith('{')]
