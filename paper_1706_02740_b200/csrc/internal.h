@@ -59,6 +59,7 @@ struct Bucket {
   int fft_variant = 0;           // K2 instantiation: 0 <64,8>, 1 <288,2>, 2 <512,1>
   int fft_group = 1;             // reserved (warp-group sub-FFT layout, not used)
   const void* k2_jit = nullptr;  // plan-time NVRTC specialisation of K2 (cudaKernel_t), or null
+  int jit_threads = 0;           // its CTA size (default fft_threads)
   int split = 0;                 // > 1: row too large for one CTA's shared memory; K2a/K2b split
                                  // mode with R0 = fac[0] = split output blocks of M/R0 elements
   int toff[kMaxFac] = {};       // offset of stage s's twiddle base table in tw

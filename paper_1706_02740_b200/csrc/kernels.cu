@@ -1382,7 +1382,7 @@ cudaError_t launch_k2(const Plan& p, int t, double2* Z, int64_t zstride, int nve
   const size_t smem = (size_t)b.M * sizeof(double2);
   if (b.k2_jit) {  // plan-time specialisation (jit.cpp): same arguments, compile-time radices
     void* args[] = {(void*)&k};
-    return cudaLaunchKernel(b.k2_jit, grid, dim3(b.fft_threads), args, smem, st);
+    return cudaLaunchKernel(b.k2_jit, grid, dim3(b.jit_threads), args, smem, st);
   }
   // Shared-memory carveout: just enough for the resident rows, so the rest of
   // the unified 256 KB stays L1 for bhat and the twiddle tables (read by every

@@ -600,8 +600,17 @@ static void specialise_k2(Plan& P) {
     th.emplace_back([&, t, dev] {
       cudaSetDevice(dev);
       Bucket& bb = P.bk[t];
-      const int minb = bb.fft_variant == 1 ? 2 : 1;
-      bb.k2_jit = jit_k2(bb.fft_threads, minb, bb.fac, bb.nfac, (size_t)bb.M * 16, &why[t]);
+      int nt = bb.fft_threads, minb = bb.fft_variant == 1 ? 2 : 1;
+      // DSFT_K2_JIT="threads,ctas_per_sm" (experiments): other occupancy for the rows
+      // that run two CTAs per SM, when that many rows fit in shared memory
+      if (const char* o = getenv("DSFT_K2_JIT")) {
+        int a = 0, c = 0;
+        if (sscanf(o, "%d,%d", &a, &c) == 2 && bb.fft_variant == 1 && a % 32 == 0 && a >= 64 && a <= 1024 &&
+            c >= 1 && (size_t)c * ((size_t)bb.M * 16 + 1088) <= 228 * 1024)
+          nt = a, minb = c;
+      }
+      bb.jit_threads = nt;
+      bb.k2_jit = jit_k2(nt, minb, bb.fac, bb.nfac, (size_t)bb.M * 16, &why[t]);
     });
   }
   for (auto& x : th) x.join();
