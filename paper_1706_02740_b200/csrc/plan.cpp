@@ -815,9 +815,14 @@ dsft_status dsft_plan_get_info(const dsft_plan* pl, dsft_plan_info* info) {
 }
 
 static int64_t choose_wave(const Plan& p, int64_t batch) {
-  // vectors per wave: keep the Z working set near L2 size (126 MB) when several fit
+  // vectors per wave (batched execute): ~1 GB of Z per wave, at most 64 vectors.  Each
+  // wave pays the pipeline's fill and drain (first K1, last K3, the K5/K6 tail) once;
+  // measured at config 4 (256 x 2^24): 64 MB waves (Z in L2) 8587 transforms/s,
+  // 512 MB 10470, 1 GB 10718, 2 GB 10681 -- K2 is FP64-bound, Z may come from DRAM.
   const double zbytes = (double)p.J * p.maxSP * 16.0;
-  int64_t vb = (int64_t)(64.0e6 / std::max(zbytes, 1.0));
+  double budget = 1.0e9;
+  if (const char* e = getenv("DSFT_WAVE_MB")) budget = std::max(1.0, atof(e)) * 1e6;  // experiments
+  int64_t vb = (int64_t)(budget / std::max(zbytes, 1.0));
   vb = std::max<int64_t>(1, std::min<int64_t>(vb, 64));
   return std::min<int64_t>(vb, std::max<int64_t>(batch, 1));
 }
