@@ -137,13 +137,17 @@ WsLayout ws_layout(const Plan& p, int64_t nvec);
 
 // ---- kernel launchers (kernels.cu); all stream-ordered, return cudaError_t
 // K1 over the nodes of nprime bucket primes ts[] (one launch), prime i writing Zs[i]
+// sig_range (optional): per prime [s0, s1) shift rows of the launch
 cudaError_t launch_k1(const Plan& p, int nprime, const int* ts, double2* const* Zs, const int64_t* zstrides,
                       const int* keep_l2, const double2* f, int64_t ld, int nvec, const int* band_list, int nbands,
-                      cudaStream_t st);
+                      cudaStream_t st, const int* sig_range = nullptr);
+// rows: bands [band0, band0 + nb_launch) x shifts [sig0, sig0 + nsig) (<= 0: all)
 cudaError_t launch_k2(const Plan& p, int t, double2* Z, int64_t zstride, int nvec, void* ws, const int* band_list,
-                      int nbands, cudaStream_t st);
+                      int nbands, cudaStream_t st, int band0 = 0, int nb_launch = 0, int sig0 = 0, int nsig = 0);
+// bands [j0, j0 + nb_launch) of the band list (<= 0: all)
 cudaError_t launch_k3(const Plan& p, int t, const double2* Z, int64_t zstride, int nvec, void* ws,
-                      const int* band_list, int nbands, cudaStream_t st, const int* prev, int nprev);
+                      const int* band_list, int nbands, cudaStream_t st, const int* prev, int nprev, int j0 = 0,
+                      int nb_launch = 0);
 // K4..K6 in one cooperative launch; freqs == nullptr: no merge (sharded path merges
 // after the allgather with launch_k6_blocks)
 cudaError_t launch_k45(const Plan& p, int nvec, void* ws, const int* band_list, int nbands, cudaStream_t st,

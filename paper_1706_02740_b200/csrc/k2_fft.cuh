@@ -16,10 +16,17 @@ struct K2Params {
   int P, M, nfac, t;     // t: bucket-prime index (trace builds only)
   int fac[kMaxFac];
   int toff[kMaxFac];
+  int S, sig0, nsig, band0;  // rows of this launch: bands band0 + blockIdx.x / nsig, shifts sig0 + blockIdx.x % nsig
   const double2* bhat;   // [R_last][M/R_last] (see internal.h)
   const double2* tw;     // per-stage twiddle base tables
   double2* Zs;           // split mode: scratch rows (same layout and strides as Z)
 };
+
+// global row index (band * S + shift) of the launch's local block b
+__device__ __forceinline__ int k2_row(const K2Params& p, int b) {
+  const int bl = b / p.nsig;
+  return (p.band0 + bl) * p.S + p.sig0 + (b - bl * p.nsig);
+}
 
 template <int NT, int M, int N, int R, bool GSRC>
 __device__ __forceinline__ void dif_ct(const double2* __restrict__ src, double2* s, const double2* __restrict__ tw) {
@@ -150,7 +157,7 @@ __global__ void __launch_bounds__(NT) __maxnreg__(((65536 / (NT * MINB)) & ~7) >
   constexpr int M = L::M, F = L::F;
   extern __shared__ double2 sm[];
   __shared__ double2 sX0;
-  double2* row = p.Z + (int64_t)blockIdx.y * p.z_vec_stride + (int64_t)blockIdx.x * p.P;
+  double2* row = p.Z + (int64_t)blockIdx.y * p.z_vec_stride + (int64_t)k2_row(p, blockIdx.x) * p.P;
   const double2 x0 = ldcg2(row + M);
   if constexpr (F == 1) {
     for (int i = threadIdx.x; i < M; i += NT) sm[i] = ldcg2(row + i);

@@ -40,6 +40,7 @@ struct K1Prime {
   int P, S;
   const uint16_t* gpow;  // [P-1] node n1 = g^q of Rader position q (position P-1: node 0)
   int keep_l2;           // Z stores with the L2 evict_last policy (consumed next) or evict_first
+  int node0, nnode;      // this launch covers nodes [node0, node0 + nnode) of the prime (node = sigma P + q)
   const int* shift_r;    // [S] residue prime of shift sigma (1 for the P-subgrid)   (device tables)
   const int* shift_n2;   // [S] n2 of shift sigma
   const double* shift_scale;  // [S] 2 pi / (N L_sigma)
@@ -209,8 +210,8 @@ __global__ void __launch_bounds__(kK1FastThreads) k1_gather_mix_fast(const __gri
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int lb;
   const K1Prime& pp = p.pr[k1_prime(p, lb)];
-  const int nodes = pp.S * pp.P;
-  const int gid = lb * kK1FastThreads + threadIdx.x;
+  const int nodes = pp.node0 + pp.nnode;
+  const int gid = pp.node0 + lb * kK1FastThreads + threadIdx.x;
   const bool active = gid < nodes;
   const int v = blockIdx.y;
   const int sigma = active ? gid / pp.P : 0;
@@ -224,7 +225,7 @@ __global__ void __launch_bounds__(kK1FastThreads) k1_gather_mix_fast(const __gri
   {
     const int h = lane >> 4, u = lane & 15;
     const bool lane_on = u < W;
-    const int first = (lb * kK1FastThreads + warp * 32);
+    const int first = (pp.node0 + lb * kK1FastThreads + warp * 32);
     double2 buf[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
@@ -258,8 +259,8 @@ __global__ void __launch_bounds__(256) k1_gather_mix(const __grid_constant__ K1P
   const int kappa = KAPPA > 0 ? KAPPA : p.kappa;
   int lb;
   const K1Prime& pp = p.pr[k1_prime(p, lb)];
-  const int64_t nodes = (int64_t)pp.S * pp.P;
-  const int64_t gid = (int64_t)lb * blockDim.x + threadIdx.x;
+  const int64_t nodes = (int64_t)pp.node0 + pp.nnode;
+  const int64_t gid = (int64_t)pp.node0 + (int64_t)lb * blockDim.x + threadIdx.x;
   if (gid >= nodes) return;
   const int v = blockIdx.y;
   const int sigma = (int)(gid / pp.P);
@@ -521,7 +522,7 @@ __global__ void __launch_bounds__(MAXT) __maxnreg__(((65536 / (MAXT * MINB)) & ~
   K2T();
   const int M = p.M, F = p.nfac;
   const int NT = blockDim.x, tid = threadIdx.x;
-  double2* row = p.Z + (int64_t)blockIdx.y * p.z_vec_stride + (int64_t)blockIdx.x * p.P;
+  double2* row = p.Z + (int64_t)blockIdx.y * p.z_vec_stride + (int64_t)k2_row(p, blockIdx.x) * p.P;
   const double2 x0 = ldcg2(row + M);
   int n = M;
   if (F >= 2) {
@@ -578,7 +579,8 @@ __global__ void __launch_bounds__(MAXT) __maxnreg__(((65536 / (MAXT * MINB)) & ~
   const int M = p.M, F = p.nfac, R0 = p.fac[0], RL = p.fac[F - 1];
   const int Msub = M / R0;
   const int NT = blockDim.x, tid = threadIdx.x;
-  const int rowi = blockIdx.x / R0, c = blockIdx.x - rowi * R0;
+  const int rowl = blockIdx.x / R0, c = blockIdx.x - rowl * R0;
+  const int rowi = k2_row(p, rowl);
   const int64_t roff = (int64_t)blockIdx.y * p.z_vec_stride + (int64_t)rowi * p.P;
   const double2* row = p.Z + roff;
   double2* srow = p.Zs + roff;
@@ -624,7 +626,8 @@ __global__ void __launch_bounds__(256) k2b_split(const __grid_constant__ K2Param
   const int M = p.M, R0 = p.fac[0];
   const int Msub = M / R0;
   const int nchunk = (Msub + 255) / 256;
-  const int rowi = blockIdx.x / nchunk, k = (blockIdx.x - rowi * nchunk) * 256 + threadIdx.x;
+  const int rowl = blockIdx.x / nchunk, k = (blockIdx.x - rowl * nchunk) * 256 + threadIdx.x;
+  const int rowi = k2_row(p, rowl);
   if (k >= Msub) return;
   const int64_t roff = (int64_t)blockIdx.y * p.z_vec_stride + (int64_t)rowi * p.P;
   double2* row = p.Z + roff;
@@ -672,6 +675,7 @@ struct K3Params {
   int64_t cw_vec_stride;  // elements per vector in cand_w (nb * sumP)
   int64_t sumP, off;
   int t;                  // this bucket prime's index
+  int j0;                 // first band (list index) of this launch; nb bands
   int nprev;              // bucket primes processed before this one (plan order) ...
   int prev[DSFT_MAX_T];   // ... in processing order
   int64_t Pt[DSFT_MAX_T], offt[DSFT_MAX_T];  // all bucket primes and their slot offsets
@@ -708,8 +712,9 @@ __global__ void __launch_bounds__(256) k3_identify(const __grid_constant__ K3Par
   const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (gid >= (int64_t)p.nb * p.P) return;
   const int v = blockIdx.y;
-  const int j = (int)(gid / p.P);
-  const int64_t pos = gid - (int64_t)j * p.P;  // Rader position: bucket a = g^-pos (pos < P-1), 0 (pos = P-1)
+  const int jl = (int)(gid / p.P);
+  const int64_t pos = gid - (int64_t)jl * p.P;  // Rader position: bucket a = g^-pos (pos < P-1), 0 (pos = P-1)
+  const int j = p.j0 + jl;
   const int64_t Mr = p.P - 1;
   const int64_t a = pos == Mr ? 0 : (int64_t)__ldg(p.gpow + (pos == 0 ? 0 : Mr - pos));
   const double2* col = p.Z + (int64_t)v * p.z_vec_stride + (int64_t)j * p.S * p.P + pos;
@@ -1300,7 +1305,7 @@ static int64_t band_q(const Plan& p, int j) { return p.q1 + 2 * p.w * (int64_t)j
 
 cudaError_t launch_k1(const Plan& p, int nprime, const int* ts, double2* const* Zs, const int64_t* zstrides,
                       const int* keep_l2, const double2* f, int64_t ld, int nvec, const int* bands, int nbands,
-                      cudaStream_t st) {
+                      cudaStream_t st, const int* sig_range) {
   K1Params k{};
   k.f = f;
   k.ld = ld;
@@ -1337,10 +1342,13 @@ cudaError_t launch_k1(const Plan& p, int nprime, const int* ts, double2* const* 
     q.S = b.S;
     q.gpow = b.gpow;
     q.keep_l2 = keep_l2[i];
+    const int s0 = sig_range ? sig_range[2 * i] : 0, s1 = sig_range ? sig_range[2 * i + 1] : b.S;
+    q.node0 = s0 * (int)b.P;
+    q.nnode = (s1 - s0) * (int)b.P;
     q.shift_r = b.shift_r_dev;
     q.shift_n2 = b.shift_n2_dev;
     q.shift_scale = b.shift_scale_dev;
-    k.cta_off[i + 1] = k.cta_off[i] + (int)cdiv((int64_t)b.S * b.P, cta);
+    k.cta_off[i + 1] = k.cta_off[i] + (int)cdiv((int64_t)q.nnode, cta);
   }
   const dim3 grid((unsigned)k.cta_off[nprime], nvec);
   if (fast && p.kappa == 6) k1_gather_mix_fast<6><<<grid, kK1FastThreads, 0, st>>>(k);
@@ -1350,7 +1358,7 @@ cudaError_t launch_k1(const Plan& p, int nprime, const int* ts, double2* const* 
 }
 
 cudaError_t launch_k2(const Plan& p, int t, double2* Z, int64_t zstride, int nvec, void* ws, const int* /*bands*/,
-                      int nbands, cudaStream_t st) {
+                      int nbands, cudaStream_t st, int band0, int nb_launch, int sig0, int nsig) {
   const Bucket& b = p.bk[t];
   const WsLayout L = ws_layout(p, p.ws_batch);
   K2Params k{};
@@ -1360,6 +1368,12 @@ cudaError_t launch_k2(const Plan& p, int t, double2* Z, int64_t zstride, int nve
   k.M = b.M;
   k.nfac = b.nfac;
   k.t = t;
+  k.S = b.S;
+  if (nb_launch <= 0) band0 = 0, nb_launch = nbands;
+  if (nsig <= 0) sig0 = 0, nsig = b.S;
+  k.band0 = band0;
+  k.sig0 = sig0;
+  k.nsig = nsig;
   for (int i = 0; i < b.nfac; ++i) {
     k.fac[i] = b.fac[i];
     k.toff[i] = b.toff[i];
@@ -1372,13 +1386,13 @@ cudaError_t launch_k2(const Plan& p, int t, double2* Z, int64_t zstride, int nve
     const size_t smem_s = (size_t)msub * sizeof(double2);
     cudaError_t e = cudaFuncSetAttribute((const void*)k2a_split<512, 1>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (e != cudaSuccess) return e;
-    k2a_split<512, 1><<<dim3((unsigned)(nbands * b.S * b.split), nvec), 512, smem_s, st>>>(k);
+    k2a_split<512, 1><<<dim3((unsigned)(nb_launch * nsig * b.split), nvec), 512, smem_s, st>>>(k);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     const unsigned nchunk = (unsigned)((msub + 255) / 256);
-    k2b_split<<<dim3((unsigned)(nbands * b.S) * nchunk, nvec), 256, 0, st>>>(k);
+    k2b_split<<<dim3((unsigned)(nb_launch * nsig) * nchunk, nvec), 256, 0, st>>>(k);
     return cudaGetLastError();
   }
-  dim3 grid((unsigned)(nbands * b.S), nvec);
+  dim3 grid((unsigned)(nb_launch * nsig), nvec);
   const size_t smem = (size_t)b.M * sizeof(double2);
   if (b.k2_jit) {  // plan-time specialisation (jit.cpp): same arguments, compile-time radices
     void* args[] = {(void*)&k};
@@ -1411,7 +1425,7 @@ cudaError_t launch_k2(const Plan& p, int t, double2* Z, int64_t zstride, int nve
 }
 
 cudaError_t launch_k3(const Plan& p, int t, const double2* Z, int64_t zstride, int nvec, void* ws, const int* bands,
-                      int nbands, cudaStream_t st, const int* prev, int nprev) {
+                      int nbands, cudaStream_t st, const int* prev, int nprev, int j0, int nb_launch) {
   const Bucket& b = p.bk[t];
   const WsLayout L = ws_layout(p, p.ws_batch);
   K3Params k{};
@@ -1419,7 +1433,7 @@ cudaError_t launch_k3(const Plan& p, int t, const double2* Z, int64_t zstride, i
   k.z_vec_stride = zstride;
   k.P = b.P;
   k.S = b.S;
-  k.nb = nbands;
+  k.nb = nb_launch > 0 ? nb_launch : nbands;  // bands of this launch (j0 + 0 .. nb-1)
   k.K = b.K;
   k.Kmax = p.Kmax;
   for (int i = 0; i < b.K; ++i) {
@@ -1439,6 +1453,8 @@ cudaError_t launch_k3(const Plan& p, int t, const double2* Z, int64_t zstride, i
   k.B_hi = p.B_hi;
   k.gpow = b.gpow;
   k.t = t;
+  if (nb_launch <= 0) j0 = 0, nb_launch = nbands;
+  k.j0 = j0;
   k.nprev = nprev;
   for (int i = 0; i < nprev; ++i) k.prev[i] = prev[i];
   for (int t2 = 0; t2 < p.T; ++t2) {
@@ -1451,7 +1467,7 @@ cudaError_t launch_k3(const Plan& p, int t, const double2* Z, int64_t zstride, i
   k.cw_vec_stride = L.cw_vec;
   k.sumP = p.sumP;
   k.off = b.off;
-  dim3 grid(cdiv((int64_t)nbands * b.P, 256), nvec);
+  dim3 grid(cdiv((int64_t)k.nb * b.P, 256), nvec);
   if (p.Rmax <= 7) k3_identify<7><<<grid, 256, 0, st>>>(k);
   else if (p.Rmax <= 13) k3_identify<13><<<grid, 256, 0, st>>>(k);
   else if (p.Rmax <= 17) k3_identify<17><<<grid, 256, 0, st>>>(k);
