@@ -256,13 +256,15 @@ def run_ours(a):
         e2e = {"value": world / (ems / 1e3), "unit": UNIT, "h2d_bytes_per_step": N * 16,
                "d2h_bytes_per_step": s * 24, "ms_per_step": ems}
 
-    # ---- roofline of the dominant kernel: K2 (length-P DFTs), FP64-bound.  Algorithmic
-    # flops per launch = rows x 5 P log2 P; peak = measured DFMA peak
-    # (profiles/r1_fp64_peak.md: 36.6 TFLOP/s, 64 lanes x 2 flop x 148 SMs x 1.93 GHz)
+    # ---- roofline of the dominant kernel: K2 (the aliasing DFTs), FP64-bound.  Algorithmic
+    # flops = SURVEY §8(d)'s 5 L log2 L per residue grid L = P_t r_{t,i} per band (the grid
+    # DFT that K2's length-P DFTs and K3's length-r fold implement together, Good-Thomas);
+    # peak = measured DFMA peak (profiles/r1_fp64_peak.md: 36.6 TFLOP/s)
     peaks = measured_peaks()
     fp64_peak_tflops = 36.62
-    k2_flops = sum(info.J * info.n_shifts[t] * 5.0 * info.primes[t] * math.log2(info.primes[t])
-                   for t in range(info.T))  # per transform = sum over the T launches
+    k2_flops = sum(info.J * 5.0 * L * math.log2(L)
+                   for t in range(info.T)
+                   for L in (info.primes[t] * r for r in info.residues[t][:info.n_residues[t]]))
     k2_ms, k2_n = kt["k2_prime_dft"]
     k2_avg_ms = k2_ms / max(k2_n, 1)
     k2_achieved = (k2_flops / info.T / 1e12) / (k2_avg_ms / 1e3)
@@ -324,7 +326,8 @@ def run_ours(a):
                      "unit": "TFLOP/s", "frac": k2_achieved / fp64_peak_tflops, "traffic": k2_traffic,
                      "peak_source": "measured FP64 DFMA peak (profiles/r1_fp64_peak.md); FP64, no tensor path",
                      "algorithmic_flops_per_launch": k2_flops / info.T, "avg_launch_ms": k2_avg_ms,
-                     "algorithmic": "5 P log2 P per length-P DFT x J x S_t rows (Rader executes 2 FFTs of P-1)"},
+                     "algorithmic": "SURVEY 8(d): 5 L log2 L per residue grid L = P_t r_ti, x J bands (K2 + K3 fold; "
+                                    "Rader executes 2 FFTs of P-1 per row)"},
         "roofline_gather": {"kernel": "k1_gather_mix", "bound": "hbm", "achieved": achieved, "peak": peak_gbs,
                             "unit": "GB/s", "frac": achieved / peak_gbs, "traffic": traffic,
                             "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if peaks else "fallback 6.65 TB/s",
