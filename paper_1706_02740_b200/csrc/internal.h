@@ -32,6 +32,7 @@ namespace dsft {
 constexpr int kMaxShifts = 160;  // 1 + sum_i (r_i - 1) for up to 10 residue primes
 constexpr int kK1TabMax = 32 * 6 * 2;  // J <= 32 with kappa <= 6 in kernel params
 constexpr int64_t kSentinel = INT64_MIN;
+constexpr int64_t kMaxWave = 4096;  // vectors processed concurrently by one batched wave
 #ifndef DSFT_ZBUFS
 #define DSFT_ZBUFS 2
 #endif

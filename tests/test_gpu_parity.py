@@ -169,6 +169,24 @@ def test_batched_equals_single():
         assert np.array_equal(co.cpu().numpy()[v * s:(v + 1) * s], c1)
 
 
+def test_large_batch_equals_single():
+    """A batch far larger than one pipeline wave of small vectors (BASELINE config 0
+    shape): every vector's result equals its single-vector execute bitwise."""
+    N, s, B = 4096, 8, 600
+    fs = np.stack([planted(N, s, cfg=39, trial=v % 7, vector=v).f for v in range(B)])
+    plan = d.Plan(N, s)
+    fdev = to_dev(fs.reshape(-1))
+    fr = torch.empty(B * s, dtype=torch.int64, device=DEV)
+    co = torch.empty(B * s, dtype=torch.complex128, device=DEV)
+    plan.dsft_execute_batched(fdev, B, N, fr, co)
+    torch.cuda.synchronize()
+    frn, con = fr.cpu().numpy().reshape(B, s), co.cpu().numpy().reshape(B, s)
+    single = d.Plan(N, s)
+    for v in (0, 1, 63, 64, 299, 599):
+        f1, c1 = run_gpu(single, fs[v])
+        assert np.array_equal(frn[v], f1) and np.array_equal(con[v], c1)
+
+
 def test_host_path_equals_device_path():
     N, s = 2**16, 50
     pl = planted(N, s, cfg=35, trial=0)
