@@ -192,11 +192,13 @@ bool choose_radices(int M, std::vector<int>& out) {
 bool choose_k2_layout(Bucket& b, std::vector<int>& rad) {
   const int M = b.M;
   b.split = 0;
-  if ((size_t)M * 16 + 2048 > 227 * 1024) {
+  size_t split_above = 227 * 1024;  // DSFT_SPLIT_KB: experiments (split rows above this many KB)
+  if (const char* e = getenv("DSFT_SPLIT_KB")) split_above = (size_t)std::max(1, atoi(e)) * 1024;
+  if ((size_t)M * 16 + 2048 > split_above) {
     // split mode: the smallest R0 | M whose blocks of M/R0 fit one CTA (K2a), final
     // radix-R0 stage across blocks in K2b
     for (int r0 = 2; r0 <= kMaxRadix; ++r0)
-      if (M % r0 == 0 && (size_t)(M / r0) * 16 + 2048 <= 227 * 1024) {
+      if (M % r0 == 0 && (size_t)(M / r0) * 16 + 2048 <= std::min<size_t>(split_above, 227 * 1024)) {
         std::vector<int> sub;
         if (!choose_radices(M / r0, sub)) return false;
         rad.assign(1, r0);
