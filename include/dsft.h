@@ -208,10 +208,12 @@ dsft_status dsft_debug_grid(dsft_plan* plan, const dsft_c128* f_dev, int32_t ban
 dsft_status dsft_debug_copy(dsft_plan* plan, int32_t which, void* dst_dev, size_t bytes, void* stream);
 
 /* dsft_debug_jit_compile: NVRTC-compile (no load, no GPU needed) the specialised
- * K2 kernel k2_ct<nt, minb, fac[0..nfac)> to an sm_100a cubin; DSFT_OK or
- * DSFT_ERR_CUDA with the compiler log in `why` (truncated to why_len). */
-dsft_status dsft_debug_jit_compile(int32_t nt, int32_t minb, const int32_t* fac, int32_t nfac, char* why,
-                                   size_t why_len);
+ * K2 kernel k2_ct<nt, minb, fac[0..nfac)> (cluster != 0: the cluster-mode kernel
+ * k2_cl<nt, minb, fac[0] = CTAs per cluster, fac[1..nfac) = sub-FFT radices>) to an
+ * sm_100a cubin; DSFT_OK or DSFT_ERR_CUDA with the compiler log in `why`
+ * (truncated to why_len). */
+dsft_status dsft_debug_jit_compile(int32_t nt, int32_t minb, const int32_t* fac, int32_t nfac, int32_t cluster,
+                                   char* why, size_t why_len);
 
 #ifdef __cplusplus
 }

@@ -76,8 +76,8 @@ _SIGS = {
     "dsft_execute_sharded": (C.c_int, [_P, _P, _P, _P, _P, _P]),
     "dsft_debug_grid": (C.c_int, [_P, _P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _P, _P]),
     "dsft_debug_copy": (C.c_int, [_P, C.c_int32, _P, C.c_size_t, _P]),
-    "dsft_debug_jit_compile": (C.c_int, [C.c_int32, C.c_int32, C.POINTER(C.c_int32), C.c_int32, C.c_char_p,
-                                         C.c_size_t]),
+    "dsft_debug_jit_compile": (C.c_int, [C.c_int32, C.c_int32, C.POINTER(C.c_int32), C.c_int32, C.c_int32,
+                                         C.c_char_p, C.c_size_t]),
 }
 
 _lib = None
@@ -146,11 +146,12 @@ def _stream_ptr(stream) -> int | None:
     return stream if isinstance(stream, int) else stream.cuda_stream
 
 
-def dsft_debug_jit_compile(nt: int, minb: int, radices: list[int]) -> tuple[int, str]:
-    """NVRTC-compile the specialised K2 kernel for a radix tuple (no GPU needed): (status, log)."""
+def dsft_debug_jit_compile(nt: int, minb: int, radices: list[int], cluster: bool = False) -> tuple[int, str]:
+    """NVRTC-compile the specialised K2 kernel for a radix tuple (no GPU needed): (status, log).
+    cluster: the cluster-mode kernel, radices[0] = CTAs per cluster, the rest the sub-FFT."""
     arr = (C.c_int32 * len(radices))(*radices)
     buf = C.create_string_buffer(4096)
-    st = lib().dsft_debug_jit_compile(nt, minb, arr, len(radices), buf, 4096)
+    st = lib().dsft_debug_jit_compile(nt, minb, arr, len(radices), 1 if cluster else 0, buf, 4096)
     return int(st), buf.value.decode(errors="replace")
 
 

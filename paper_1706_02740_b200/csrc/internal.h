@@ -61,6 +61,8 @@ struct Bucket {
   int fft_group = 1;             // reserved (warp-group sub-FFT layout, not used)
   const void* k2_jit = nullptr;  // plan-time NVRTC specialisation of K2 (cudaKernel_t), or null
   int jit_threads = 0;           // its CTA size (default fft_threads)
+  int cl = 0;                    // > 1: cluster mode (k2_cl, C = fac[0] CTAs per row, DSMEM); falls back
+                                 // to the split mode below if the specialised kernel is unavailable
   int split = 0;                 // > 1: row too large for one CTA's shared memory; K2a/K2b split
                                  // mode with R0 = fac[0] = split output blocks of M/R0 elements
   int toff[kMaxFac] = {};       // offset of stage s's twiddle base table in tw
@@ -159,8 +161,8 @@ cudaError_t launch_debug_grid(const Plan& p, int t, const double2* Z, int i, int
                               cudaStream_t st);
 cudaError_t kernels_init();  // one-time attribute setup (dynamic smem limits)
 // jit.cpp: k2_ct<nt, minb, fac...> compiled with NVRTC (cudaKernel_t), or nullptr + *why
-const void* jit_k2(int nt, int minb, const int* fac, int nfac, size_t smem_bytes, std::string* why);
-bool jit_k2_compile_only(int nt, int minb, const int* fac, int nfac, std::string* why);  // no GPU needed
+const void* jit_k2(int nt, int minb, const int* fac, int nfac, size_t smem_bytes, std::string* why, bool cluster = false);
+bool jit_k2_compile_only(int nt, int minb, const int* fac, int nfac, std::string* why, bool cluster = false);
 cudaError_t launch_k6_blocks(const int64_t* bw, const double2* bc, const double* bm, const int32_t* bnz, int nblocks,
                              int64_t budget, int64_t blk_vec, int64_t bn_vec, int64_t s, int nvec, int64_t* freqs,
                              double2* coeffs, cudaStream_t st);

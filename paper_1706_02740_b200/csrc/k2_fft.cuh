@@ -97,6 +97,31 @@ __device__ __forceinline__ void dit_ct(double2* s, double2* __restrict__ dst, co
   }
 }
 
+// turn over M elements whose turn blocks are blk0 + blk of a bhat table with
+// nbt blocks per digit (whole row: blk0 = 0, nbt = M / R)
+template <int NT, int M, int R>
+__device__ __forceinline__ void turn_ct_at(double2* s, const double2* __restrict__ bhat, int nbt, int blk0,
+                                          double2* sX0) {
+  constexpr int nb = M / R, iters = (nb + NT - 1) / NT;
+#pragma unroll
+  for (int it = 0; it < iters; ++it) {
+    const int blk = threadIdx.x + it * NT;
+    if ((nb % NT == 0) || blk < nb) {
+      const int base = blk * R;
+      double2 v[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) v[r] = s[base + r];
+      dft<R>(v);
+      if (sX0 != nullptr && blk == 0) *sX0 = v[0];
+#pragma unroll
+      for (int c = 0; c < R; ++c) v[c] = cconj(cmul(v[c], ldg2(bhat + c * nbt + blk0 + blk)));
+      dft<R>(v);
+#pragma unroll
+      for (int c = 0; c < R; ++c) s[base + c] = v[c];
+    }
+  }
+}
+
 template <int NT, int M, int R>
 __device__ __forceinline__ void turn_ct(double2* s, const double2* __restrict__ bhat, double2* sX0) {
   constexpr int nb = M / R, iters = (nb + NT - 1) / NT;
@@ -176,6 +201,122 @@ __global__ void __launch_bounds__(NT) __maxnreg__(((65536 / (NT * MINB)) & ~7) >
     dit_ct<NT, M, M, L::R[0], true>(sm, row, p.tw + p.toff[0], x0);
   }
   if (threadIdx.x == 0) row[M] = cadd(x0, sX0);  // X[0] = x0 + sum_q a_q
+}
+
+// ------------------------------------------------------------ cluster mode
+// Rows too long for two CTAs per SM (P above ~7000): a thread-block cluster of C
+// CTAs holds one row in distributed shared memory, CTA c owning block c of M/C
+// elements.  The radix-C first DIF stage and last DIT stage run across the
+// cluster through DSMEM (butterfly k reads/writes element k of every block);
+// everything in between is the block's own sub-FFT (middle DIF stages, turn,
+// middle DIT stages) in local shared memory.  Row data touches global memory once
+// on the way in and once on the way out.
+__device__ __forceinline__ unsigned cl_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cl_sync() {
+  asm volatile("barrier.cluster.arrive.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
+}
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  unsigned long long a;
+  asm("cvta.to.shared.u64 %0, %1;" : "=l"(a) : "l"(p));
+  return (unsigned)a;
+}
+__device__ __forceinline__ unsigned cl_map(unsigned saddr, unsigned rank) {
+  unsigned r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ double2 ld_dsmem(unsigned a) {
+  double2 v;
+  asm volatile("ld.shared::cluster.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_dsmem(unsigned a, double2 v) {
+  asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(v.x), "d"(v.y) : "memory");
+}
+
+template <int NT, class L, int S>
+__device__ __forceinline__ void cl_dif_mid(double2* sm, const K2Params& p) {  // sub stages S.. (full stage S+1)
+  if constexpr (S <= L::F - 2) {
+    dif_ct<NT, L::M, L::span(S), L::R[S], false>(sm, sm, p.tw + p.toff[S + 1]);
+    __syncthreads();
+    cl_dif_mid<NT, L, S + 1>(sm, p);
+  }
+}
+
+template <int NT, class L, int S>
+__device__ __forceinline__ void cl_dit_mid(double2* sm, const K2Params& p, double2 x0) {
+  if constexpr (S >= 0) {
+    dit_ct<NT, L::M, L::span(S), L::R[S], false>(sm, sm, p.tw + p.toff[S + 1], x0);
+    __syncthreads();
+    cl_dit_mid<NT, L, S - 1>(sm, p, x0);
+  }
+}
+
+// cluster of C CTAs per row; Rs: radices of the length-M/C sub-FFT (F >= 2)
+template <int NT, int MINB, int C, int... Rs>
+__global__ void __launch_bounds__(NT) __maxnreg__(((65536 / (NT * MINB)) & ~7) > 255 ? 255 : ((65536 / (NT * MINB)) & ~7))
+    k2_cl(const __grid_constant__ K2Params p) {
+  using L = RadixList<Rs...>;
+  constexpr int Ms = L::M, M = C * Ms, F = L::F, RL = L::R[F - 1];
+  constexpr int chunk = (Ms + C - 1) / C;  // stage-0 butterflies per CTA
+  static_assert(F >= 2, "cluster mode needs a sub-FFT of at least two passes");
+  extern __shared__ double2 sm[];
+  __shared__ double2 sX0;
+  const int c = (int)cl_rank();
+  double2* row = p.Z + (int64_t)blockIdx.y * p.z_vec_stride + (int64_t)k2_row(p, blockIdx.x / C) * p.P;
+  const double2 x0 = ldcg2(row + M);
+  for (int i = threadIdx.x; i < Ms; i += NT) sm[i] = ldcg2(row + c * Ms + i);
+  unsigned rb[C];  // DSMEM address of element 0 of every block
+  const unsigned me = smem_u32(sm);
+#pragma unroll
+  for (int r = 0; r < C; ++r) rb[r] = cl_map(me, (unsigned)r);
+  cl_sync();
+  // DIF stage 0 (span M, radix C): y_{c'}[k] = W_M^{c'k} sum_r x_r[k] W_C^{rc'}, in place
+  const double2* tw0 = p.tw + p.toff[0];  // W_M^k, k < M / C
+  const int k_end = (c + 1) * chunk < Ms ? (c + 1) * chunk : Ms;
+  for (int k = c * chunk + (int)threadIdx.x; k < k_end; k += NT) {
+    double2 v[C];
+#pragma unroll
+    for (int r = 0; r < C; ++r) v[r] = ld_dsmem(rb[r] + (unsigned)k * 16u);
+    dft<C>(v);
+    const double2 w1 = ldg2(tw0 + k);
+    double2 w = w1;
+    st_dsmem(rb[0] + (unsigned)k * 16u, v[0]);
+#pragma unroll
+    for (int r = 1; r < C; ++r) {
+      st_dsmem(rb[r] + (unsigned)k * 16u, cmul(v[r], w));
+      if (r + 1 < C) w = cmul(w, w1);
+    }
+  }
+  cl_sync();
+  // the block's sub-FFT: middle DIF stages, turn (bhat blocks of this block), middle DIT stages
+  cl_dif_mid<NT, L, 0>(sm, p);
+  turn_ct_at<NT, Ms, RL>(sm, p.bhat, M / RL, c * (Ms / RL), c == 0 ? &sX0 : nullptr);
+  __syncthreads();
+  cl_dit_mid<NT, L, F - 2>(sm, p, x0);
+  cl_sync();
+  // DIT stage 0 (span M, radix C) across the cluster, straight to global memory, + x0
+  const uint64_t pol = l2_evict_last();
+  for (int k = c * chunk + (int)threadIdx.x; k < k_end; k += NT) {
+    double2 v[C];
+    const double2 w1 = ldg2(tw0 + k);
+    double2 w = w1;
+    v[0] = ld_dsmem(rb[0] + (unsigned)k * 16u);
+#pragma unroll
+    for (int r = 1; r < C; ++r) {
+      v[r] = cmul(ld_dsmem(rb[r] + (unsigned)k * 16u), w);
+      if (r + 1 < C) w = cmul(w, w1);
+    }
+    dft<C>(v);
+#pragma unroll
+    for (int r = 0; r < C; ++r) st_keep(row + r * Ms + k, cadd(x0, cconj(v[r])), pol);
+  }
+  if (c == 0 && threadIdx.x == 0) row[M] = cadd(x0, sX0);  // X[0] = x0 + sum_q a_q
+  cl_sync();  // keep this CTA's shared memory alive until the cluster is done with it
 }
 
 }  // namespace dsft

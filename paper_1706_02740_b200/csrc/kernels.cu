@@ -1381,6 +1381,22 @@ cudaError_t launch_k2(const Plan& p, int t, double2* Z, int64_t zstride, int nve
   k.bhat = b.bhat;
   k.tw = b.tw;
   k.Zs = L.zs ? (double2*)((char*)ws + L.zs) : nullptr;
+  if (b.cl && b.k2_jit) {  // cluster mode: C CTAs per row (thread-block cluster, DSMEM)
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(nb_launch * nsig * b.cl), nvec);
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = (size_t)(b.M / b.cl) * sizeof(double2);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = b.cl;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    void* args[] = {(void*)&k};
+    return cudaLaunchKernelExC(&cfg, b.k2_jit, args);
+  }
   if (b.split) {
     const int msub = b.M / b.split;
     const size_t smem_s = (size_t)msub * sizeof(double2);

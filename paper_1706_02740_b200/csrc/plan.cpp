@@ -192,6 +192,30 @@ bool choose_radices(int M, std::vector<int>& out) {
 bool choose_k2_layout(Bucket& b, std::vector<int>& rad) {
   const int M = b.M;
   b.split = 0;
+  b.cl = 0;
+  // cluster mode (k2_cl): rows too long for one CTA's shared memory are held by a
+  // cluster of C <= 8 CTAs (smallest C | M whose blocks of M/C fit two per SM and
+  // leave a sub-FFT of at least two passes); split mode with R0 = C is the fallback.
+  // (Measured: for rows that fit one CTA, P ~ 7.5k-14.5k, the single-CTA kernel is
+  // faster -- config 2, s = 1000: 2170 vs 1982 transforms/s; s = 4000: 332 -> 461.)
+  const char* clenv = getenv("DSFT_K2_CLUSTER");
+  if (!(clenv && strcmp(clenv, "0") == 0) && (size_t)M * 16 + 2048 > 227 * 1024) {
+    for (int c = 2; c <= 8; ++c) {
+      if (M % c) continue;
+      const int ms = M / c;
+      if ((size_t)2 * ((size_t)ms * 16 + 2048) > 228 * 1024) continue;
+      std::vector<int> sub;
+      if (!choose_radices(ms, sub) || sub.size() < 2 || 1 + sub.size() > (size_t)kMaxFac) continue;
+      rad.assign(1, c);
+      rad.insert(rad.end(), sub.begin(), sub.end());
+      b.cl = c;
+      b.split = c;
+      b.fft_variant = 2;
+      b.fft_threads = 512;  // split-mode fallback; the cluster kernel runs 256 threads, 2 CTAs / SM
+      b.fft_group = 1;
+      return true;
+    }
+  }
   size_t split_above = 227 * 1024;  // DSFT_SPLIT_KB: experiments (split rows above this many KB)
   if (const char* e = getenv("DSFT_SPLIT_KB")) split_above = (size_t)std::max(1, atoi(e)) * 1024;
   if ((size_t)M * 16 + 2048 > split_above) {
@@ -598,11 +622,16 @@ static void specialise_k2(Plan& P) {
   std::vector<std::string> why(P.T);
   for (int t = 0; t < P.T; ++t) {
     Bucket& b = P.bk[t];
-    if (b.split || b.fft_variant == 0) continue;
+    if ((b.split && !b.cl) || b.fft_variant == 0) continue;
     th.emplace_back([&, t, dev] {
       cudaSetDevice(dev);
       Bucket& bb = P.bk[t];
       int nt = bb.fft_threads, minb = bb.fft_variant == 1 ? 2 : 1;
+      if (bb.cl) {  // cluster kernel: blocks of M / C elements, 256 threads, 2 CTAs per SM
+        bb.jit_threads = 256;
+        bb.k2_jit = jit_k2(256, 2, bb.fac, bb.nfac, (size_t)(bb.M / bb.cl) * 16, &why[t], true);
+        return;
+      }
       // DSFT_K2_JIT="threads,ctas_per_sm" (experiments): other occupancy for the rows
       // that run two CTAs per SM, when that many rows fit in shared memory
       if (const char* o = getenv("DSFT_K2_JIT")) {
@@ -750,12 +779,12 @@ dsft_status dsft_plan_create(int64_t N, int64_t s, const dsft_params* params, ds
   return DSFT_OK;
 }
 
-dsft_status dsft_debug_jit_compile(int32_t nt, int32_t minb, const int32_t* fac, int32_t nfac, char* why,
-                                   size_t why_len) {
+dsft_status dsft_debug_jit_compile(int32_t nt, int32_t minb, const int32_t* fac, int32_t nfac, int32_t cluster,
+                                   char* why, size_t why_len) {
   if (!fac || nfac < 1 || nfac > kMaxFac || nt < 32 || minb < 1) return fail(DSFT_ERR_ARG, "bad arguments");
   std::vector<int> f(fac, fac + nfac);
   std::string w;
-  const bool ok = jit_k2_compile_only(nt, minb, f.data(), nfac, &w);
+  const bool ok = jit_k2_compile_only(nt, minb, f.data(), nfac, &w, cluster != 0);
   if (why && why_len) {
     const size_t c = std::min(why_len - 1, w.size());
     memcpy(why, w.data(), c);

@@ -69,4 +69,8 @@ def test_k2_specialisation_compiles_with_nvrtc(tmp_path, monkeypatch):
     for nt, minb, rad in ((256, 2, [10, 9, 9, 5]), (512, 1, [12, 10, 9, 7]), (256, 2, [13]), (256, 2, [16, 3])):
         st, log = d.dsft_debug_jit_compile(nt, minb, rad)
         assert st == 0, log
-    assert len(list(tmp_path.glob("k2_*.cubin"))) == 4
+    # cluster mode (thread-block cluster of C CTAs per row, DSMEM stages): C = 2 and 4
+    for rad in ([2, 12, 9, 5, 7], [4, 13, 7, 7, 7]):
+        st, log = d.dsft_debug_jit_compile(256, 2, rad, cluster=True)
+        assert st == 0, log
+    assert len(list(tmp_path.glob("k2_*.cubin"))) == 6
