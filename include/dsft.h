@@ -141,10 +141,24 @@ dsft_status dsft_execute(dsft_plan* plan, const dsft_c128* f_dev, int64_t* freqs
 dsft_status dsft_execute_batched(dsft_plan* plan, const dsft_c128* f_dev, int64_t batch, int64_t ld,
                                  int64_t* freqs_out_dev, dsft_c128* coeffs_out_dev, void* stream);
 
-/* End-to-end variant with HOST buffers: copies f_host (pinned or pageable) to
- * the device, executes, copies the result back, and synchronises `stream`. */
+/* End-to-end variant with HOST buffers; synchronises `stream` before returning.
+ * If f_host is page-locked and mapped into the device address space
+ * (cudaHostAlloc / cudaHostRegister; e.g. torch pin_memory) and K1's windows
+ * cover at most half of f, K1 gathers the windows straight from host memory
+ * (zero copy: only the sampled bytes cross the host link -- the sublinear
+ * sampling of Algorithm 1).  Otherwise (pageable memory, or
+ * dense sampling) f is copied to a device buffer first.  Results are identical
+ * either way.  DSFT_HOST_ZERO_COPY=0 in the environment forces the copy, =1
+ * reads any mapped f_host in place.  The outputs are copied back. */
 dsft_status dsft_execute_host(dsft_plan* plan, const dsft_c128* f_host, int64_t* freqs_out_host,
                               dsft_c128* coeffs_out_host, void* stream);
+
+/* 1 if dsft_execute_host(plan, f_host, ...) reads f_host in place (zero copy),
+ * 0 if it copies f to the device, -1 for a NULL argument.  If h2d_bytes is not
+ * NULL it receives the bytes of f that cross the host link per execute: the
+ * window bytes sum_t S_t P_t (2 kappa + 1) 16 (an upper bound on the distinct
+ * entries read) in zero-copy mode, N * 16 otherwise. */
+int32_t dsft_plan_host_zero_copy(const dsft_plan* plan, const dsft_c128* f_host, int64_t* h2d_bytes);
 
 /* K2 specialisation (DESIGN.md §6 K2): dsft_plan_create compiles, with NVRTC
  * (loaded with dlopen), the length-P_t DFT kernel of each bucket prime with its

@@ -64,6 +64,7 @@ _SIGS = {
     "dsft_execute": (C.c_int, [_P, _P, _P, _P, _P]),
     "dsft_execute_batched": (C.c_int, [_P, _P, C.c_int64, C.c_int64, _P, _P, _P]),
     "dsft_execute_host": (C.c_int, [_P, _P, _P, _P, _P]),
+    "dsft_plan_host_zero_copy": (C.c_int32, [_P, _P, C.POINTER(C.c_int64)]),
     "dsft_plan_launches_per_execute": (C.c_int64, [_P]),
     "dsft_plan_k2_specialized": (C.c_int32, [_P, C.c_char_p, C.c_size_t]),
     "dsft_plan_set_timing": (C.c_int, [_P, C.c_int32]),
@@ -223,6 +224,15 @@ class Plan:
     def dsft_execute_host(self, f_host, freqs_host, coeffs_host, stream=None):
         _check(lib().dsft_execute_host(self._h, f_host.data_ptr(), freqs_host.data_ptr(),
                                        coeffs_host.data_ptr(), _stream_ptr(stream)))
+
+    def dsft_plan_host_zero_copy(self, f_host):
+        """(zero_copy, h2d_bytes): whether dsft_execute_host reads f_host in place, and
+        the bytes of f that cross the host link per execute (include/dsft.h)."""
+        nb = C.c_int64(0)
+        r = lib().dsft_plan_host_zero_copy(self._h, f_host.data_ptr(), C.byref(nb))
+        if r < 0:
+            raise DsftError("dsft_plan_host_zero_copy: NULL argument")
+        return bool(r), int(nb.value)
 
     def dsft_execute_sharded(self, comm, f, freqs_out, coeffs_out, stream=None):
         _check(lib().dsft_execute_sharded(self._h, comm.handle, f.data_ptr(), freqs_out.data_ptr(),

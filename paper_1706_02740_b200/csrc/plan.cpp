@@ -1061,6 +1061,37 @@ dsft_status dsft_execute_batched(dsft_plan* pl, const dsft_c128* f_dev, int64_t 
   return execute_impl(pl, f_dev, batch, ld, freqs, coeffs, stream);
 }
 
+// Bytes of f under K1's windows: one window of 2 kappa + 1 taps per node, S_t P_t
+// nodes per bucket prime (band-independent).  An upper bound on the distinct bytes.
+static int64_t window_bytes(const Plan& p) {
+  int64_t nodes = 0;
+  for (int t = 0; t < p.T; ++t) nodes += (int64_t)p.bk[t].S * p.bk[t].P;
+  return nodes * (2 * p.kappa + 1) * 16;
+}
+
+// Device alias of f_host when K1 should read it in place over the host link
+// (page-locked, mapped; the windows cover at most half of f), else nullptr.
+static const void* host_alias(const Plan& p, const void* f_host) {
+  const char* env = getenv("DSFT_HOST_ZERO_COPY");  // "0" never, "1" whenever mapped
+  if (env && strcmp(env, "0") == 0) return nullptr;
+  cudaPointerAttributes pa{};
+  if (cudaPointerGetAttributes(&pa, f_host) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  if (pa.type != cudaMemoryTypeHost || !pa.devicePointer) return nullptr;
+  const bool sparse = 2 * window_bytes(p) <= p.N * 16;
+  return (sparse || (env && strcmp(env, "1") == 0)) ? pa.devicePointer : nullptr;
+}
+
+int32_t dsft_plan_host_zero_copy(const dsft_plan* pl, const dsft_c128* f_host, int64_t* h2d_bytes) {
+  if (!pl || !f_host) return -1;
+  const Plan& p = pl->p;
+  const bool zc = host_alias(p, f_host) != nullptr;
+  if (h2d_bytes) *h2d_bytes = zc ? std::min<int64_t>(window_bytes(p), p.N * 16) : p.N * 16;
+  return zc ? 1 : 0;
+}
+
 dsft_status dsft_execute_host(dsft_plan* pl, const dsft_c128* f_host, int64_t* freqs_host, dsft_c128* coeffs_host,
                               void* stream) {
   if (!pl || !f_host || !freqs_host || !coeffs_host) return fail(DSFT_ERR_ARG, "NULL argument");
@@ -1072,8 +1103,14 @@ dsft_status dsft_execute_host(dsft_plan* pl, const dsft_c128* f_host, int64_t* f
   }
   char* base = (char*)p.io_dev;
   cudaStream_t st = (cudaStream_t)stream;
-  CU(cudaMemcpyAsync(base, f_host, (size_t)p.N * 16, cudaMemcpyHostToDevice, st), "H2D f");
-  dsft_status r = dsft_execute(pl, (const dsft_c128*)base, (int64_t*)(base + fb), (dsft_c128*)(base + fb + wb), stream);
+  // zero copy: K1 gathers its windows straight from the page-locked host vector
+  // (only the sampled bytes cross the link); otherwise f is copied first
+  const void* f_dev = host_alias(p, f_host);
+  if (!f_dev) {
+    CU(cudaMemcpyAsync(base, f_host, (size_t)p.N * 16, cudaMemcpyHostToDevice, st), "H2D f");
+    f_dev = base;
+  }
+  dsft_status r = dsft_execute(pl, (const dsft_c128*)f_dev, (int64_t*)(base + fb), (dsft_c128*)(base + fb + wb), stream);
   if (r != DSFT_OK) return r;
   CU(cudaMemcpyAsync(freqs_host, base + fb, (size_t)p.s * 8, cudaMemcpyDeviceToHost, st), "D2H freqs");
   CU(cudaMemcpyAsync(coeffs_host, base + fb + wb, (size_t)p.s * 16, cudaMemcpyDeviceToHost, st), "D2H coeffs");

@@ -199,6 +199,29 @@ def test_host_path_equals_device_path():
     assert np.array_equal(frh.numpy(), f1) and np.array_equal(coh.numpy(), c1)
 
 
+@pytest.mark.parametrize("mode", ["zero_copy", "copy_pinned", "copy_pageable"])
+def test_host_path_modes_equal_device_path(mode, monkeypatch):
+    """dsft_execute_host reads a sparse-sampled pinned f in place (zero copy), copies
+    pageable memory, and gives bitwise the device path's result in every mode."""
+    N, s = 2**22, 50  # BASELINE config 1: windows cover ~2 % of f
+    pl = planted(N, s, cfg=36, trial=0)
+    plan = d.Plan(N, s)
+    f1, c1 = run_gpu(plan, pl.f)
+    if mode == "copy_pinned":
+        monkeypatch.setenv("DSFT_HOST_ZERO_COPY", "0")
+    fh = torch.from_numpy(pl.f.copy())
+    if mode != "copy_pageable":
+        fh = fh.pin_memory()
+    frh = torch.full((s,), 7, dtype=torch.int64)
+    coh = torch.zeros(s, dtype=torch.complex128)
+    zc, nb = plan.dsft_plan_host_zero_copy(fh)
+    assert zc == (mode == "zero_copy")
+    win = plan.info.nodes * (2 * plan.info.kappa + 1) * 16
+    assert nb == (win if zc else N * 16) and (not zc or 2 * win <= N * 16)
+    plan.dsft_execute_host(fh, frh, coh)
+    assert np.array_equal(frh.numpy(), f1) and np.array_equal(coh.numpy(), c1)
+
+
 def test_k2_specialised_equals_runtime_radix(monkeypatch):
     """The plan-time NVRTC specialisation of K2 and the runtime-radix kernel run the
     same passes in the same arithmetic order: outputs bitwise identical."""
