@@ -222,12 +222,19 @@ dsft_status dsft_debug_grid(dsft_plan* plan, const dsft_c128* f_dev, int32_t ban
 dsft_status dsft_debug_copy(dsft_plan* plan, int32_t which, void* dst_dev, size_t bytes, void* stream);
 
 /* dsft_debug_jit_compile: NVRTC-compile (no load, no GPU needed) the specialised
- * K2 kernel k2_ct<nt, minb, fac[0..nfac)> (cluster != 0: the cluster-mode kernel
- * k2_cl<nt, minb, fac[0] = CTAs per cluster, fac[1..nfac) = sub-FFT radices>) to an
- * sm_100a cubin; DSFT_OK or DSFT_ERR_CUDA with the compiler log in `why`
- * (truncated to why_len). */
+ * K2 kernel k2_ct<nt, minb, twf, fac[0..nfac)> (twf: bit i set = stage i ends its
+ * Good-Thomas dimension and has no twiddles; cluster != 0: the cluster-mode kernel
+ * k2_cl<nt, minb, fac[0] = CTAs per cluster, fac[1..nfac) = sub-FFT radices>, twf
+ * ignored) to an sm_100a cubin; DSFT_OK or DSFT_ERR_CUDA with the compiler log in
+ * `why` (truncated to why_len). */
 dsft_status dsft_debug_jit_compile(int32_t nt, int32_t minb, const int32_t* fac, int32_t nfac, int32_t cluster,
-                                   char* why, size_t why_len);
+                                   uint32_t twf, char* why, size_t why_len);
+
+/* K2 stage layout of bucket prime t (plan order, 0 <= t < T): writes the radices
+ * (<= 24) to radices, the twiddle-free stage mask (bit i: stage i ends its
+ * Good-Thomas dimension) to *twf and the number of dimensions to *ndim; returns
+ * the number of stages, or -1 for a bad argument. */
+int32_t dsft_plan_k2_stages(const dsft_plan* plan, int32_t t, int32_t* radices, uint32_t* twf, int32_t* ndim);
 
 #ifdef __cplusplus
 }

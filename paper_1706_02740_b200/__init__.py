@@ -78,7 +78,9 @@ _SIGS = {
     "dsft_debug_grid": (C.c_int, [_P, _P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _P, _P]),
     "dsft_debug_copy": (C.c_int, [_P, C.c_int32, _P, C.c_size_t, _P]),
     "dsft_debug_jit_compile": (C.c_int, [C.c_int32, C.c_int32, C.POINTER(C.c_int32), C.c_int32, C.c_int32,
-                                         C.c_char_p, C.c_size_t]),
+                                         C.c_uint32, C.c_char_p, C.c_size_t]),
+    "dsft_plan_k2_stages": (C.c_int32, [_P, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_uint32),
+                                        C.POINTER(C.c_int32)]),
 }
 
 _lib = None
@@ -147,12 +149,14 @@ def _stream_ptr(stream) -> int | None:
     return stream if isinstance(stream, int) else stream.cuda_stream
 
 
-def dsft_debug_jit_compile(nt: int, minb: int, radices: list[int], cluster: bool = False) -> tuple[int, str]:
+def dsft_debug_jit_compile(nt: int, minb: int, radices: list[int], cluster: bool = False,
+                           twf: int = 0) -> tuple[int, str]:
     """NVRTC-compile the specialised K2 kernel for a radix tuple (no GPU needed): (status, log).
-    cluster: the cluster-mode kernel, radices[0] = CTAs per cluster, the rest the sub-FFT."""
+    cluster: the cluster-mode kernel, radices[0] = CTAs per cluster, the rest the sub-FFT;
+    twf: twiddle-free stage mask (bit i: stage i ends its Good-Thomas dimension)."""
     arr = (C.c_int32 * len(radices))(*radices)
     buf = C.create_string_buffer(4096)
-    st = lib().dsft_debug_jit_compile(nt, minb, arr, len(radices), 1 if cluster else 0, buf, 4096)
+    st = lib().dsft_debug_jit_compile(nt, minb, arr, len(radices), 1 if cluster else 0, twf, buf, 4096)
     return int(st), buf.value.decode(errors="replace")
 
 
@@ -224,6 +228,15 @@ class Plan:
     def dsft_execute_host(self, f_host, freqs_host, coeffs_host, stream=None):
         _check(lib().dsft_execute_host(self._h, f_host.data_ptr(), freqs_host.data_ptr(),
                                        coeffs_host.data_ptr(), _stream_ptr(stream)))
+
+    def dsft_plan_k2_stages(self, t: int):
+        """(radices, twf, ndim) of bucket prime t's K2 stage layout (include/dsft.h)."""
+        rad = (C.c_int32 * 24)()
+        twf, nd = C.c_uint32(0), C.c_int32(0)
+        n = lib().dsft_plan_k2_stages(self._h, t, rad, C.byref(twf), C.byref(nd))
+        if n < 0:
+            raise DsftError("dsft_plan_k2_stages: bad argument")
+        return list(rad[:n]), int(twf.value), int(nd.value)
 
     def dsft_plan_host_zero_copy(self, f_host):
         """(zero_copy, h2d_bytes): whether dsft_execute_host reads f_host in place, and

@@ -67,15 +67,27 @@ struct Bucket {
                                  // mode with R0 = fac[0] = split output blocks of M/R0 elements
   int toff[kMaxFac] = {};       // offset of stage s's twiddle base table in tw
   int ntw = 0;                  // entries in tw: sum over DIF stages of n_s / R_s
+  // Good-Thomas dimensions of the length-M FFT (plan.cpp choose_k2_dims): the radix
+  // list is grouped into ndim coprime dimensions of lengths dim_m[d] (stages
+  // dim_s0[d] .. dim_s0[d+1]-1); twiddles only inside a dimension, so the last
+  // stage of each is twiddle-free (bit i of twf).  ndim = 1: plain mixed radix.
+  int ndim = 1;
+  int dim_m[kMaxFac] = {};
+  int dim_s0[kMaxFac + 1] = {};
+  unsigned twf = 0;
   // device pointers
-  uint16_t* dlog = nullptr;     // [P] discrete log base g (dlog[0] unused; parity hooks)
-  uint16_t* gpow = nullptr;     // [M] g^q mod P: node / bin of Rader position q
+  uint16_t* posn = nullptr;     // [P] array position of node n (posn[0] unused; parity hooks)
+  uint16_t* posb = nullptr;     // [P] array position of bin a (posb[0] unused; parity hooks)
+  uint16_t* gpow = nullptr;     // [M] node at array position x: g^q with pos(q) = x (K1)
+  uint16_t* binat = nullptr;    // [M] bin at array position x: g^-p with pos(p) = x (K3)
   int* shift_r_dev = nullptr;   // [S] K1 shift tables (copies of shift_r, shift_n2, 2 pi / (N P r))
   int* shift_n2_dev = nullptr;
   double* shift_scale_dev = nullptr;
   double2* bhat = nullptr;      // [R_last][M/R_last] FFT_M(b)/M, DIF output position blk*R_last + c stored
                                 // at c*(M/R_last) + blk; b_m = exp(-2 pi i g^-m / P)
-  double2* tw = nullptr;        // [ntw] per DIF stage s (span n_s, m_s = n_s/R_s): exp(-2 pi i k / n_s), k < m_s;
+  double2* tw = nullptr;        // [ntw] per DIF stage s (span n_s, m_s = n_s/R_s): exp(-2 pi i floor(k/in_s) / d_s),
+                                // k < m_s, d_s = the stage's span inside its dimension, in_s = the
+                                // length of the later dimensions (one dimension: exp(-2 pi i k / n_s));
                                 // split mode: stage 0 holds exp(-2 pi i e / M) for all e < M
 };
 
@@ -161,8 +173,10 @@ cudaError_t launch_debug_grid(const Plan& p, int t, const double2* Z, int i, int
                               cudaStream_t st);
 cudaError_t kernels_init();  // one-time attribute setup (dynamic smem limits)
 // jit.cpp: k2_ct<nt, minb, fac...> compiled with NVRTC (cudaKernel_t), or nullptr + *why
-const void* jit_k2(int nt, int minb, const int* fac, int nfac, size_t smem_bytes, std::string* why, bool cluster = false);
-bool jit_k2_compile_only(int nt, int minb, const int* fac, int nfac, std::string* why, bool cluster = false);
+const void* jit_k2(int nt, int minb, const int* fac, int nfac, size_t smem_bytes, std::string* why, bool cluster = false,
+                   unsigned twf = 0);
+bool jit_k2_compile_only(int nt, int minb, const int* fac, int nfac, std::string* why, bool cluster = false,
+                         unsigned twf = 0);
 cudaError_t launch_k6_blocks(const int64_t* bw, const double2* bc, const double* bm, const int32_t* bnz, int nblocks,
                              int64_t budget, int64_t blk_vec, int64_t bn_vec, int64_t s, int nvec, int64_t* freqs,
                              double2* coeffs, cudaStream_t st);

@@ -28,7 +28,8 @@ __device__ __forceinline__ int k2_row(const K2Params& p, int b) {
   return (p.band0 + bl) * p.S + p.sig0 + (b - bl * p.nsig);
 }
 
-template <int NT, int M, int N, int R, bool GSRC>
+// TW = false: a stage that ends its Good-Thomas dimension (twiddles all 1, skipped)
+template <int NT, int M, int N, int R, bool GSRC, bool TW = true>
 __device__ __forceinline__ void dif_ct(const double2* __restrict__ src, double2* s, const double2* __restrict__ tw) {
   constexpr int m = N / R, nbf = M / R, iters = (nbf + NT - 1) / NT;
 #pragma unroll
@@ -38,11 +39,16 @@ __device__ __forceinline__ void dif_ct(const double2* __restrict__ src, double2*
       const int blk = beta / m;
       const int k = beta - blk * m;
       const int base = blk * N + k;
-      const double2 w1 = ldg2(tw + k);
       double2 v[R];
 #pragma unroll
       for (int r = 0; r < R; ++r) v[r] = GSRC ? ldcg2(src + base + r * m) : s[base + r * m];
       dft<R>(v);
+      if constexpr (!TW) {
+#pragma unroll
+        for (int c = 0; c < R; ++c) s[base + c * m] = v[c];
+        continue;
+      }
+      const double2 w1 = ldg2(tw + k);
       const double2 w2 = cmul(w1, w1);
       double2 wa = w1, wb = w2;
       s[base] = v[0];
@@ -60,7 +66,7 @@ __device__ __forceinline__ void dif_ct(const double2* __restrict__ src, double2*
   }
 }
 
-template <int NT, int M, int N, int R, bool GDST>
+template <int NT, int M, int N, int R, bool GDST, bool TW = true>
 __device__ __forceinline__ void dit_ct(double2* s, double2* __restrict__ dst, const double2* __restrict__ tw, double2 x0) {
   constexpr int m = N / R, nbf = M / R, iters = (nbf + NT - 1) / NT;
   const uint64_t pol = l2_evict_last();
@@ -71,14 +77,14 @@ __device__ __forceinline__ void dit_ct(double2* s, double2* __restrict__ dst, co
       const int blk = beta / m;
       const int k = beta - blk * m;
       const int base = blk * N + k;
-      const double2 w1 = ldg2(tw + k);
       double2 v[R];
 #pragma unroll
       for (int r = 0; r < R; ++r) v[r] = s[base + r * m];
+      const double2 w1 = TW ? ldg2(tw + k) : make_double2(1.0, 0.0);
       const double2 w2 = cmul(w1, w1);
       double2 wa = w1, wb = w2;
 #pragma unroll
-      for (int r = 1; r < R; ++r) {
+      for (int r = 1; r < R && TW; ++r) {
         if (r & 1) {
           v[r] = cmul(v[r], wa);
           if (r + 2 < R) wa = cmul(wa, w2);
@@ -156,26 +162,28 @@ struct RadixList {
   }
 };
 
-template <int NT, class L, int S>
+// TWF: bit S set = stage S ends its Good-Thomas dimension (no twiddles)
+template <int NT, class L, int S, unsigned TWF = 0u>
 __device__ __forceinline__ void dif_mid(double2* sm, const K2Params& p) {
   if constexpr (S <= L::F - 2) {
-    dif_ct<NT, L::M, L::span(S), L::R[S], false>(sm, sm, p.tw + p.toff[S]);
+    dif_ct<NT, L::M, L::span(S), L::R[S], false, !((TWF >> S) & 1u)>(sm, sm, p.tw + p.toff[S]);
     __syncthreads();
-    dif_mid<NT, L, S + 1>(sm, p);
+    dif_mid<NT, L, S + 1, TWF>(sm, p);
   }
 }
 
-template <int NT, class L, int S>
+template <int NT, class L, int S, unsigned TWF = 0u>
 __device__ __forceinline__ void dit_mid(double2* sm, const K2Params& p, double2 x0) {
   if constexpr (S >= 1) {
-    dit_ct<NT, L::M, L::span(S), L::R[S], false>(sm, sm, p.tw + p.toff[S], x0);
+    dit_ct<NT, L::M, L::span(S), L::R[S], false, !((TWF >> S) & 1u)>(sm, sm, p.tw + p.toff[S], x0);
     __syncthreads();
-    dit_mid<NT, L, S - 1>(sm, p, x0);
+    dit_mid<NT, L, S - 1, TWF>(sm, p, x0);
   }
 }
 
-// NT threads, MINB CTAs per SM (register cap 65536 / (NT MINB)), radices Rs...
-template <int NT, int MINB, int... Rs>
+// NT threads, MINB CTAs per SM (register cap 65536 / (NT MINB)), radices Rs...;
+// TWF: twiddle-free stages (bit i: stage i ends its Good-Thomas dimension)
+template <int NT, int MINB, unsigned TWF, int... Rs>
 __global__ void __launch_bounds__(NT) __maxnreg__(((65536 / (NT * MINB)) & ~7) > 255 ? 255 : ((65536 / (NT * MINB)) & ~7))
     k2_ct(const __grid_constant__ K2Params p) {
   using L = RadixList<Rs...>;
@@ -192,13 +200,14 @@ __global__ void __launch_bounds__(NT) __maxnreg__(((65536 / (NT * MINB)) & ~7) >
     const uint64_t pol = l2_evict_last();
     for (int i = threadIdx.x; i < M; i += NT) st_keep(row + i, cadd(x0, cconj(sm[i])), pol);
   } else {
-    dif_ct<NT, M, M, L::R[0], true>(row, sm, p.tw + p.toff[0]);
+    constexpr bool tw0 = !(TWF & 1u);
+    dif_ct<NT, M, M, L::R[0], true, tw0>(row, sm, p.tw + p.toff[0]);
     __syncthreads();
-    dif_mid<NT, L, 1>(sm, p);
+    dif_mid<NT, L, 1, TWF>(sm, p);
     turn_ct<NT, M, L::R[F - 1]>(sm, p.bhat, &sX0);
     __syncthreads();
-    dit_mid<NT, L, F - 2>(sm, p, x0);
-    dit_ct<NT, M, M, L::R[0], true>(sm, row, p.tw + p.toff[0], x0);
+    dit_mid<NT, L, F - 2, TWF>(sm, p, x0);
+    dit_ct<NT, M, M, L::R[0], true, tw0>(sm, row, p.tw + p.toff[0], x0);
   }
   if (threadIdx.x == 0) row[M] = cadd(x0, sX0);  // X[0] = x0 + sum_q a_q
 }

@@ -38,7 +38,7 @@ struct K1Prime {
   double2* Z;
   int64_t z_vec_stride;  // elements per vector in Z
   int P, S;
-  const uint16_t* gpow;  // [P-1] node n1 = g^q of Rader position q (position P-1: node 0)
+  const uint16_t* gpow;  // [P-1] node at array position x: g^q with pos(q) = x (position P-1: node 0)
   int keep_l2;           // Z stores with the L2 evict_last policy (consumed next) or evict_first
   int node0, nnode;      // this launch covers nodes [node0, node0 + nnode) of the prime (node = sigma P + q)
   const int* shift_r;    // [S] residue prime of shift sigma (1 for the P-subgrid)   (device tables)
@@ -669,7 +669,7 @@ struct K3Params {
   int64_t crtM;
   int64_t crtE[DSFT_MAX_K + 1];
   int64_t qfirst, qstep, halfN_up, halfN_dn, w, B_lo, B_hi;
-  const uint16_t* gpow;   // [P-1] g^q mod P (K2 left bin g^-p at Rader position p)
+  const uint16_t* binat;  // [P-1] bin at array position x (K2 left bin g^-p at pos(p), plan.cpp upload_tables)
   int64_t* cand_w;
   double2* cand_v;
   int64_t cw_vec_stride;  // elements per vector in cand_w (nb * sumP)
@@ -713,10 +713,10 @@ __global__ void __launch_bounds__(256) k3_identify(const __grid_constant__ K3Par
   if (gid >= (int64_t)p.nb * p.P) return;
   const int v = blockIdx.y;
   const int jl = (int)(gid / p.P);
-  const int64_t pos = gid - (int64_t)jl * p.P;  // Rader position: bucket a = g^-pos (pos < P-1), 0 (pos = P-1)
+  const int64_t pos = gid - (int64_t)jl * p.P;  // array position: bucket a = binat[pos] (pos < P-1), 0 (pos = P-1)
   const int j = p.j0 + jl;
   const int64_t Mr = p.P - 1;
-  const int64_t a = pos == Mr ? 0 : (int64_t)__ldg(p.gpow + (pos == 0 ? 0 : Mr - pos));
+  const int64_t a = pos == Mr ? 0 : (int64_t)__ldg(p.binat + pos);
   const double2* col = p.Z + (int64_t)v * p.z_vec_stride + (int64_t)j * p.S * p.P + pos;
   int64_t R = a * p.crtE[0];
   double2 yv[DSFT_MAX_K];
@@ -1251,7 +1251,8 @@ __global__ void __launch_bounds__(kK5Threads) k5b_select(const __grid_constant__
 // ================================================================ debug grid
 struct DbgParams {
   const double2* Z;
-  const uint16_t* dlog;  // Rader position of node / bin n: dlog[n] (samples), -dlog[n] mod (P-1) (bins)
+  const uint16_t* posn;  // array position of node n (samples)
+  const uint16_t* posb;  // array position of bin a (K2 output)
   int64_t P, r, L;
   int64_t rinvP, PinvR;  // r^-1 mod P, P^-1 mod r
   int S, sb, what, band;
@@ -1267,11 +1268,11 @@ __global__ void k_debug_grid(const __grid_constant__ DbgParams p) {
   if (p.what == 0) {
     const int64_t n1 = ((k % p.P) * p.rinvP) % p.P;
     const int64_t n2 = ((k % p.r) * p.PinvR) % p.r;
-    const int64_t q = n1 == 0 ? Mr : (int64_t)p.dlog[n1];
+    const int64_t q = n1 == 0 ? Mr : (int64_t)p.posn[n1];
     p.out[k] = zb[sig(n2) * p.P + q];
   } else {
     const int64_t a = k % p.P, c = k % p.r;
-    const int64_t pos = a == 0 ? Mr : (Mr - (int64_t)p.dlog[a]) % Mr;
+    const int64_t pos = a == 0 ? Mr : (int64_t)p.posb[a];
     double2 acc = make_double2(0.0, 0.0);
     for (int64_t n2 = 0; n2 < p.r; ++n2) {
       double sn, cs;
@@ -1467,7 +1468,7 @@ cudaError_t launch_k3(const Plan& p, int t, const double2* Z, int64_t zstride, i
   k.w = p.w;
   k.B_lo = p.B_lo;
   k.B_hi = p.B_hi;
-  k.gpow = b.gpow;
+  k.binat = b.binat;
   k.t = t;
   if (nb_launch <= 0) j0 = 0, nb_launch = nbands;
   k.j0 = j0;
@@ -1605,7 +1606,8 @@ cudaError_t launch_debug_grid(const Plan& p, int t, const double2* Z, int i, int
   const WsLayout L = ws_layout(p, p.ws_batch);
   DbgParams k{};
   k.Z = Z;
-  k.dlog = b.dlog;
+  k.posn = b.posn;
+  k.posb = b.posb;
   k.P = b.P;
   k.r = b.r[i];
   k.L = b.P * b.r[i];

@@ -184,6 +184,80 @@ bool choose_radices(int M, std::vector<int>& out) {
   return true;
 }
 
+// Good-Thomas dimensions of the length-M FFT (DESIGN.md §6 K2).  The prime-power
+// components of M are grouped into coprime dimensions m_1 .. m_D; each dimension
+// gets the radices of choose_radices(m_d), and the radix list is their
+// concatenation.  Index maps (Good / CRT) turn the length-M DFT into the
+// D-dimensional DFT over the m_1 x .. x m_D array, so twiddles are needed only
+// inside a dimension: the last stage of every dimension is twiddle-free.  The
+// maps cost nothing at run time -- K1 writes each node at its array position, K3
+// reads each bin from its own, and bhat is stored in the DIF output layout.
+// Chosen: fewest passes, then fewest twiddled stages (= passes - D), then an odd
+// last (turn) radix, then choose_radices' order within ties.
+static void choose_k2_dims(Bucket& b, std::vector<int>& rad) {
+  const int M = b.M;
+  b.ndim = 1;
+  b.dim_m[0] = M;
+  b.dim_s0[0] = 0;
+  b.dim_s0[1] = (int)rad.size();
+  b.twf = 0;
+  const char* env = getenv("DSFT_K2_PFA");  // "0": one dimension (experiments)
+  if (env && strcmp(env, "0") == 0) return;
+  std::vector<int> comp;  // prime-power components
+  for (int m = M, p = 2; m > 1; ++p)
+    if (m % p == 0) {
+      int q = 1;
+      while (m % p == 0) m /= p, q *= p;
+      comp.push_back(q);
+    }
+  const int nc = (int)comp.size();
+  if (nc < 2) return;
+  auto key_of = [](const std::vector<std::vector<int>>& dims) {
+    int passes = 0, mn = 1 << 30, mx = 0;
+    for (const auto& d : dims)
+      for (int r : d) ++passes, mn = std::min(mn, r), mx = std::max(mx, r);
+    const int last = dims.back().back();
+    return std::make_tuple(passes, passes - (int)dims.size(), (last & 1) ? 0 : 1, -mn, mx);
+  };
+  std::vector<std::vector<int>> best;
+  std::vector<int> lab(nc, 0);  // restricted growth string: component -> group
+  std::function<void(int, int)> rec = [&](int i, int ng) {
+    if (i == nc) {
+      std::vector<std::vector<int>> dims(ng);
+      std::vector<int> mg(ng, 1);
+      for (int c = 0; c < nc; ++c) mg[lab[c]] *= comp[c];
+      for (int g = 0; g < ng; ++g)
+        if (!choose_radices(mg[g], dims[g])) return;
+      // order: dimensions with an odd last radix go last (the turn radix), larger first
+      std::stable_sort(dims.begin(), dims.end(), [](const std::vector<int>& x, const std::vector<int>& y) {
+        const bool ox = x.back() & 1, oy = y.back() & 1;
+        if (ox != oy) return !ox;
+        return x.size() > y.size();
+      });
+      if (best.empty() || key_of(dims) < key_of(best)) best = dims;
+      return;
+    }
+    for (int g = 0; g <= ng; ++g) {
+      lab[i] = g;
+      rec(i + 1, std::max(ng, g + 1));
+    }
+  };
+  rec(0, 0);
+  std::vector<std::vector<int>> one(1, rad);
+  if (best.empty() || !(key_of(best) < key_of(one))) return;
+  rad.clear();
+  b.ndim = (int)best.size();
+  for (int d = 0; d < b.ndim; ++d) {
+    b.dim_s0[d] = (int)rad.size();
+    int m = 1;
+    for (int r : best[d]) rad.push_back(r), m *= r;
+    b.dim_m[d] = m;
+    b.twf |= 1u << (rad.size() - 1);
+  }
+  b.dim_s0[b.ndim] = (int)rad.size();
+  b.twf &= ~(1u << (rad.size() - 1));  // the turn stage has no twiddle table
+}
+
 // K2 layout (DESIGN.md §6 K2): radices of choose_radices, CTA-wide stages.
 // Instantiation by shared-memory fit: <64,8> small rows, <256,2> two rows per
 // SM (8 warps, 128 registers: 4 warps per SM sub-partition), <512,1> one row per
@@ -193,6 +267,8 @@ bool choose_k2_layout(Bucket& b, std::vector<int>& rad) {
   const int M = b.M;
   b.split = 0;
   b.cl = 0;
+  b.ndim = 1;  // cluster / split rows: one dimension (their stage 0 spans the whole row)
+  b.twf = 0;
   // cluster mode (k2_cl): rows too long for one CTA's shared memory are held by a
   // cluster of C <= 8 CTAs (smallest C | M whose blocks of M/C fit two per SM and
   // leave a sub-FFT of at least two passes); split mode with R0 = C is the fallback.
@@ -236,6 +312,8 @@ bool choose_k2_layout(Bucket& b, std::vector<int>& rad) {
     return false;
   }
   if (!choose_radices(M, rad)) return false;
+  choose_k2_dims(b, rad);
+  if ((int)rad.size() > kMaxFac) return false;
   if (M <= 1200) b.fft_variant = 0, b.fft_threads = 64;
   else if ((size_t)2 * ((size_t)M * 16 + 2048) <= 228 * 1024) b.fft_variant = 1, b.fft_threads = 256;
   else b.fft_variant = 2, b.fft_threads = 512;
@@ -462,6 +540,11 @@ static dsft_status derive(int64_t N, int64_t s, const dsft_params& prm, Plan& P)
     if (!choose_k2_layout(b, rad)) return fail(DSFT_ERR_INTERNAL, "P-1 not 13-smooth or too many FFT stages");
     b.nfac = (int)rad.size();
     for (int i = 0; i < b.nfac; ++i) b.fac[i] = rad[i];
+    if (b.ndim == 1) {
+      b.dim_m[0] = b.M;
+      b.dim_s0[0] = 0;
+      b.dim_s0[1] = b.nfac;
+    }
     // twiddle base tables of the DIF/DIT stages 0..F-2 (the last stage has span R, no twiddle)
     int span = b.M, ntw = 0;
     for (int i = 0; i + 1 < b.nfac; ++i) {
@@ -518,7 +601,7 @@ static dsft_status derive(int64_t N, int64_t s, const dsft_params& prm, Plan& P)
 }
 
 static dsft_status upload_tables(Plan& P) {
-  // one allocation; per t: dlog [P] uint16 | gpow [M] uint16 | bhat [M] | tw [ntw] (double2);
+  // one allocation; per t: posn [P] | posb [P] | gpow [M] | binat [M] (uint16) | bhat [M] | tw [ntw] (double2);
   // then the K1 tables k1tab [J][kappa][2], ctab [kappa+1]
   size_t bytes = 0;
   std::vector<size_t> offs(P.T), goff(P.T), cpx(P.T), soff(P.T);
@@ -527,8 +610,8 @@ static dsft_status upload_tables(Plan& P) {
     soff[t] = bytes;  // K1 shift tables: scale [S] double | r [S] int | n2 [S] int
     bytes = align256(bytes + (size_t)b.S * 16);
     offs[t] = bytes;
-    goff[t] = align256(bytes + (size_t)b.P * 2);
-    cpx[t] = align256(goff[t] + (size_t)b.M * 2);
+    goff[t] = align256(bytes + (size_t)b.P * 4);
+    cpx[t] = align256(goff[t] + (size_t)b.M * 4);
     bytes = align256(cpx[t] + (size_t)(b.M + b.ntw) * 16);
   }
   const size_t k1off = bytes;
@@ -547,16 +630,34 @@ static dsft_status upload_tables(Plan& P) {
         sn[sg] = b.shift_n2[sg];
       }
     }
-    uint16_t* dlog = (uint16_t*)(host.data() + offs[t]);
+    uint16_t* posn = (uint16_t*)(host.data() + offs[t]);
+    uint16_t* posb = posn + b.P;
     uint16_t* gpow = (uint16_t*)(host.data() + goff[t]);
+    uint16_t* binat = gpow + M;
     double* bhat = (double*)(host.data() + cpx[t]);
     double* tw = bhat + 2 * (size_t)M;
+    // Good-Thomas dimensions (choose_k2_dims): inner[d] = product of the later
+    // dimensions; time-domain index q sits at pos(q) = sum_d ((q u_d) mod m_d) inner[d]
+    // with u_d = (M/m_d)^-1 mod m_d (Good's map), frequency c at the DIF output
+    // position sum_d rev_d(c mod m_d) inner[d] (CRT map, digits reversed inside d).
+    int64_t inner[kMaxFac + 1], u[kMaxFac];
+    inner[b.ndim] = 1;
+    for (int d = b.ndim - 1; d >= 0; --d) inner[d] = inner[d + 1] * b.dim_m[d];
+    for (int d = 0; d < b.ndim; ++d) u[d] = b.dim_m[d] == M ? 1 : invmod((M / b.dim_m[d]) % b.dim_m[d], b.dim_m[d]);
+    auto pos_time = [&](int64_t q) {
+      int64_t x = 0;
+      for (int d = 0; d < b.ndim; ++d) x += ((q * u[d]) % b.dim_m[d]) * inner[d + 1];
+      return x;
+    };
     const int64_t ginv = invmod(b.g, b.P);
     int64_t gp = 1, gn = 1;
     std::vector<cld> bseq(M), bf(M);
     for (int q = 0; q < M; ++q) {
-      dlog[gp] = (uint16_t)q;        // g^q = gp
-      gpow[q] = (uint16_t)gp;
+      const int64_t x = pos_time(q);
+      posn[gp] = (uint16_t)x;        // node g^q = gp: K1 input of Rader index q
+      gpow[x] = (uint16_t)gp;
+      posb[gn] = (uint16_t)x;        // bin g^-q = gn: K2 output of Rader index q
+      binat[x] = (uint16_t)gn;
       bseq[q] = unit_root(gn, b.P);  // b_m = W_P^{g^-m}
       gp = gp * b.g % b.P;
       gn = gn * ginv % b.P;
@@ -564,28 +665,39 @@ static dsft_status upload_tables(Plan& P) {
     fft_rec(bseq.data(), bf.data(), M, 1);
     const int RL = b.fac[b.nfac - 1], nblk = M / RL;
     for (int c = 0; c < M; ++c) {
-      // DIF output position of frequency c: pos = sum_s d_s M/(R_1..R_s), c = d_1 + R_1(d_2 + ...)
-      int64_t cc = c, pos = 0, span = M;
-      for (int i = 0; i < b.nfac; ++i) {
-        const int64_t d = cc % b.fac[i];
-        cc /= b.fac[i];
-        span /= b.fac[i];
-        pos += d * span;
+      // DIF output position of frequency c: per dimension d, c_d = c mod m_d =
+      // e_1 + R_1(e_2 + ...) over d's radices lands at sum_s e_s m_d/(R_1..R_s)
+      int64_t pos = 0;
+      for (int d = 0; d < b.ndim; ++d) {
+        int64_t cc = c % b.dim_m[d], pd = 0, span = b.dim_m[d];
+        for (int i = b.dim_s0[d]; i < b.dim_s0[d + 1]; ++i) {
+          const int64_t e = cc % b.fac[i];
+          cc /= b.fac[i];
+          span /= b.fac[i];
+          pd += e * span;
+        }
+        pos += pd * inner[d + 1];
       }
       const int64_t at = (pos % RL) * nblk + pos / RL;  // turn-stage layout [c][blk]
       bhat[2 * at] = (double)(bf[c].real() / (long double)M);
       bhat[2 * at + 1] = (double)(bf[c].imag() / (long double)M);
     }
     int span = M;
-    for (int i = 0; i + 1 < b.nfac; ++i) {
-      const int m = span / b.fac[i];
-      const int entries = (i == 0 && b.split) ? span : m;
-      for (int k = 0; k < entries; ++k) {
-        const cld wv = unit_root(k, span);
-        tw[2 * (b.toff[i] + k)] = (double)wv.real();
-        tw[2 * (b.toff[i] + k) + 1] = (double)wv.imag();
+    for (int d = 0, i = 0; d < b.ndim; ++d) {
+      int64_t dspan = b.dim_m[d];  // the stage's span inside its dimension
+      for (; i < b.dim_s0[d + 1]; ++i) {
+        const int m = span / b.fac[i];
+        if (i + 1 < b.nfac) {
+          const int entries = (i == 0 && b.split) ? span : m;
+          for (int k = 0; k < entries; ++k) {
+            const cld wv = unit_root(k / inner[d + 1], dspan);
+            tw[2 * (b.toff[i] + k)] = (double)wv.real();
+            tw[2 * (b.toff[i] + k) + 1] = (double)wv.imag();
+          }
+        }
+        span = m;
+        dspan /= b.fac[i];
       }
-      span = m;
     }
   }
   memcpy(host.data() + k1off, P.k1tab.data(), P.k1tab.size() * 8);
@@ -598,8 +710,10 @@ static dsft_status upload_tables(Plan& P) {
     b.shift_scale_dev = (double*)(base + soff[t]);
     b.shift_r_dev = (int*)(b.shift_scale_dev + b.S);
     b.shift_n2_dev = b.shift_r_dev + b.S;
-    b.dlog = (uint16_t*)(base + offs[t]);
+    b.posn = (uint16_t*)(base + offs[t]);
+    b.posb = b.posn + b.P;
     b.gpow = (uint16_t*)(base + goff[t]);
+    b.binat = b.gpow + b.M;
     b.bhat = (double2*)(base + cpx[t]);
     b.tw = b.bhat + b.M;
   }
@@ -641,7 +755,7 @@ static void specialise_k2(Plan& P) {
           nt = a, minb = c;
       }
       bb.jit_threads = nt;
-      bb.k2_jit = jit_k2(nt, minb, bb.fac, bb.nfac, (size_t)bb.M * 16, &why[t]);
+      bb.k2_jit = jit_k2(nt, minb, bb.fac, bb.nfac, (size_t)bb.M * 16, &why[t], false, bb.twf);
     });
   }
   for (auto& x : th) x.join();
@@ -780,17 +894,26 @@ dsft_status dsft_plan_create(int64_t N, int64_t s, const dsft_params* params, ds
 }
 
 dsft_status dsft_debug_jit_compile(int32_t nt, int32_t minb, const int32_t* fac, int32_t nfac, int32_t cluster,
-                                   char* why, size_t why_len) {
+                                   uint32_t twf, char* why, size_t why_len) {
   if (!fac || nfac < 1 || nfac > kMaxFac || nt < 32 || minb < 1) return fail(DSFT_ERR_ARG, "bad arguments");
   std::vector<int> f(fac, fac + nfac);
   std::string w;
-  const bool ok = jit_k2_compile_only(nt, minb, f.data(), nfac, &w, cluster != 0);
+  const bool ok = jit_k2_compile_only(nt, minb, f.data(), nfac, &w, cluster != 0, cluster ? 0u : twf);
   if (why && why_len) {
     const size_t c = std::min(why_len - 1, w.size());
     memcpy(why, w.data(), c);
     why[c] = '\0';
   }
   return ok ? DSFT_OK : fail(DSFT_ERR_CUDA, "NVRTC compile failed: " + w.substr(0, 200));
+}
+
+int32_t dsft_plan_k2_stages(const dsft_plan* pl, int32_t t, int32_t* radices, uint32_t* twf, int32_t* ndim) {
+  if (!pl || !radices || !twf || !ndim || t < 0 || t >= pl->p.T) return -1;
+  const Bucket& b = pl->p.bk[t];
+  for (int i = 0; i < b.nfac; ++i) radices[i] = b.fac[i];
+  *twf = b.twf;
+  *ndim = b.ndim;
+  return b.nfac;
 }
 
 int32_t dsft_plan_k2_specialized(const dsft_plan* pl, char* why, size_t why_len) {

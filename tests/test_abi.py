@@ -73,4 +73,8 @@ def test_k2_specialisation_compiles_with_nvrtc(tmp_path, monkeypatch):
     for rad in ([2, 12, 9, 5, 7], [4, 13, 7, 7, 7]):
         st, log = d.dsft_debug_jit_compile(256, 2, rad, cluster=True)
         assert st == 0, log
-    assert len(list(tmp_path.glob("k2_*.cubin"))) == 6
+    # Good-Thomas dimensions: twiddle-free stages (M = 8 * 3 * 13^2, 9 * 11 * 50)
+    for rad, twf in (([8, 3, 13, 13], 0b011), ([9, 11, 10, 5], 0b011)):
+        st, log = d.dsft_debug_jit_compile(256, 2, rad, twf=twf)
+        assert st == 0, log
+    assert len(list(tmp_path.glob("k2_*.cubin"))) == 8
