@@ -1298,6 +1298,15 @@ cudaError_t kernels_init() {
   if ((e = cudaFuncSetAttribute(k2_prime_dft<256, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm))) return e;
   if ((e = cudaFuncSetAttribute(k2_prime_dft<512, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm))) return e;
   if ((e = cudaFuncSetAttribute(k2a_split<512, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm))) return e;
+  if (const char* co = getenv("DSFT_CARVEOUT")) {  // experiment: one shared-memory carveout for all kernels
+    const int pct = atoi(co);
+    const void* fs[] = {(const void*)k1_gather_mix_fast<6>, (const void*)k1_gather_mix_fast<4>,
+                        (const void*)k3_identify<7>, (const void*)k3_identify<13>, (const void*)k3_identify<17>,
+                        (const void*)k3_identify<31>, (const void*)k5s_scan, (const void*)k5a_medians,
+                        (const void*)k5b_select, (const void*)k6_merge};
+    for (const void* f : fs)
+      if ((e = cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, pct))) return e;
+  }
   done = true;
   return cudaSuccess;
 }
