@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define DSFT_MAX_T 16   /* bucket primes per plan                        */
+#define DSFT_MAX_T 64   /* bucket primes per plan                        */
 #define DSFT_MAX_K 10   /* residue primes per bucket prime               */
 #define DSFT_MAX_J 128  /* passbands (Algorithm 1 line 3: ceil(c2))      */
 
@@ -70,7 +70,9 @@ enum { DSFT_ALPHA_CORRECTED = 0, DSFT_ALPHA_LITERAL = 1 };
  *  tau           passband floor, 0 < tau < 1/sqrt(2 pi) (Lemma 3)
  *  alpha_rule    CORRECTED (reading R2) or LITERAL (PAPER.md:597 as printed)
  *  bucket_factor c_b: bucket primes drawn from [ceil(c_b s), 2 ceil(c_b s))
- *  n_bucket_primes T (<= DSFT_MAX_T); vote_min v_min in [1, T]
+ *  n_bucket_primes T (<= DSFT_MAX_T); 0 = the deterministic variant (reading
+ *                R13): every prime of the pool, no draw
+ *  vote_min      v_min in [1, T]; 0 = "more than half": floor(T/2) + 1
  *  band_budget   entries kept per band after line 9 (0 = s; reading R11)
  *  seed          SplitMix64 seed of the bucket-prime draw (reading R7)   */
 typedef struct {

@@ -43,8 +43,8 @@ class OracleParams:
     tau: float = 1.0 / 3.0
     alpha_rule: str = "corrected"  # reading R2; "literal" = PAPER.md:597 as printed
     bucket_factor: float = 4.0     # c_b (reading R6)
-    n_bucket_primes: int = 5       # T   (reading R6)
-    vote_min: int = 3              # v_min (reading R9: > T/2)
+    n_bucket_primes: int = 5       # T   (reading R6); 0 = deterministic variant (reading R13)
+    vote_min: int = 3              # v_min (reading R9: > T/2); 0 = floor(T/2) + 1
     band_budget: int = 0           # 0 = s (reading R11)
     seed: int = 0
 
@@ -178,18 +178,29 @@ def derive_plan(N: int, s: int, params: OracleParams | None = None) -> Plan:
     B_hi = N // 2
 
     # Inner SFT (reading R6-R8): bucket primes and residue primes.
-    T = int(p.n_bucket_primes)
+    pool = bucket_pool(s, p.bucket_factor)
+    if int(p.n_bucket_primes) == 0:
+        # Reading R13, the deterministic variant (the
+        # measurements "always succeed"; the randomized variant reads a random subset
+        # of them): every prime of the pool, no draw.
+        T = len(pool)
+        primes = list(pool)
+    else:
+        T = int(p.n_bucket_primes)
+        if T < 1:
+            raise ConfigError("need at least one bucket prime")
+        if len(pool) < T:
+            raise ConfigError(f"bucket-prime pool has {len(pool)} < T={T} primes")
+        primes = draw_distinct(pool, T, p.seed)
     if T < 1:
         raise ConfigError("need at least one bucket prime")
-    pool = bucket_pool(s, p.bucket_factor)
-    if len(pool) < T:
-        raise ConfigError(f"bucket-prime pool has {len(pool)} < T={T} primes")
-    primes = draw_distinct(pool, T, p.seed)
     residues = [residue_moduli(P, N) for P in primes]
-    if not (1 <= p.vote_min <= T):
+    # vote_min 0: "more than half" of the T primes
+    vote_min = T // 2 + 1 if int(p.vote_min) == 0 else int(p.vote_min)
+    if not (1 <= vote_min <= T):
         raise ConfigError("vote_min must lie in [1, T]")
     budget = int(p.band_budget) if p.band_budget > 0 else s
 
     return Plan(N=N, s=s, preset=p.preset, kappa=kappa, beta=beta, c1=c1, tau=p.tau,
                 alpha=alpha, w=w, J=J, q=q, B_lo=B_lo, B_hi=B_hi, pool=pool, primes=primes,
-                residues=residues, vote_min=int(p.vote_min), band_budget=budget, seed=int(p.seed))
+                residues=residues, vote_min=vote_min, band_budget=budget, seed=int(p.seed))

@@ -19,7 +19,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libdsft.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "dsft.h")
 
-DSFT_MAX_T, DSFT_MAX_K, DSFT_MAX_J = 16, 10, 128
+DSFT_MAX_T, DSFT_MAX_K, DSFT_MAX_J = 64, 10, 128
 DSFT_OK, DSFT_ERR_CONFIG, DSFT_ERR_ARG, DSFT_ERR_CUDA = 0, 2, 3, 4
 DSFT_ERR_NCCL, DSFT_ERR_NOMEM, DSFT_ERR_INTERNAL, DSFT_ERR_UNSUPPORTED = 5, 6, 7, 8
 PRESETS = {"dmsft6": 0, "dmsft4": 1, "thm4": 2}

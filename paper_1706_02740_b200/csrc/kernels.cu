@@ -63,6 +63,7 @@ struct K1Params {
   double tab[kK1TabMax];     // [nb][kappa][2] cos/sin(q_j u 2 pi / N) (fast path)
   K1Prime pr[DSFT_MAX_T];
 };
+static_assert(sizeof(K1Params) <= 32764, "K1Params exceeds the kernel parameter limit");
 
 // prime of this CTA and the CTA's index within that prime's range
 __device__ __forceinline__ int k1_prime(const K1Params& p, int& lb) {
@@ -679,7 +680,7 @@ struct K3Params {
   int nprev;              // bucket primes processed before this one (plan order) ...
   int prev[DSFT_MAX_T];   // ... in processing order
   int64_t Pt[DSFT_MAX_T], offt[DSFT_MAX_T];  // all bucket primes and their slot offsets
-  int32_t* vmask;         // [vec][band][sum_t P_t] vote mask per candidate slot (reading R9)
+  uint64_t* vmask;        // [vec][band][sum_t P_t] vote mask per candidate slot (reading R9)
 };
 
 template <int R>
@@ -746,7 +747,7 @@ __global__ void __launch_bounds__(256) k3_identify(const __grid_constant__ K3Par
   const bool ok = (om <= q + p.halfN_dn) && (om >= q - p.w) && (om < q + p.w) && (om >= p.B_lo) && (om <= p.B_hi);
   const int64_t slot = (int64_t)v * p.cw_vec_stride + (int64_t)j * p.sumP + p.off + a;
   p.cand_w[slot] = ok ? om : kSentinel;
-  int32_t mk = 0;
+  uint64_t mk = 0;
   if (ok) {
     double2* cv = p.cand_v + slot * p.Kmax;
     for (int i = 0; i < p.K; ++i) cv[i] = yv[i];
@@ -764,8 +765,8 @@ __global__ void __launch_bounds__(256) k3_identify(const __grid_constant__ K3Par
         break;
       }
     }
-    if (t0 == p.t) mk = 1 << p.t;
-    else atomicOr(p.vmask + bb + p.offt[t0] + pmod(om, p.Pt[t0]), 1 << p.t);
+    if (t0 == p.t) mk = 1ull << p.t;
+    else atomicOr((unsigned long long*)(p.vmask + bb + p.offt[t0] + pmod(om, p.Pt[t0])), 1ull << p.t);
   }
   p.vmask[slot] = mk;  // this prime's slots: written only here, OR-ed only by later K3s
 }
@@ -782,23 +783,12 @@ struct K5aParams {
   int64_t off[DSFT_MAX_T];
   int K[DSFT_MAX_T];
   const int64_t* acc_w;
-  const int32_t* acc_mask;
+  const uint64_t* acc_mask;
   double2* acc_z;
 };
 
 constexpr int kMaxVals = DSFT_MAX_T * DSFT_MAX_K;
 
-__device__ void sort_small(double* a, int n) {
-  for (int i = 1; i < n; ++i) {
-    const double x = a[i];
-    int j = i - 1;
-    while (j >= 0 && a[j] > x) {
-      a[j + 1] = a[j];
-      --j;
-    }
-    a[j + 1] = x;
-  }
-}
 
 // Median of up to 32 values held one per lane (pad +inf): bitonic sort by
 // shuffles, then the middle order statistic(s) (mean of the two middle ones for
@@ -819,17 +809,82 @@ __device__ __forceinline__ double warp_median(double v, int cnt, int lane) {
   return (cnt & 1) ? b : 0.5 * (a + b);
 }
 
+// Median of cnt > 32 values (up to kMaxVals; T * K grids of the deterministic
+// variant), value k = lane + 32 m held by lane k mod 32 in slot m: every value is
+// broadcast once; the k-th order statistic is the value x with
+// #{< x} <= k < #{<= x} (ties share it).  O(cnt^2 / 32) compares per lane.
+constexpr int kMedSlots = (kMaxVals + 31) / 32;
+
+__device__ __forceinline__ double warp_kth(const double (&v)[kMedSlots], int cnt, int k, int lane) {
+  int lt[kMedSlots], le[kMedSlots];
+#pragma unroll
+  for (int m = 0; m < kMedSlots; ++m) lt[m] = le[m] = 0;
+#pragma unroll
+  for (int m2 = 0; m2 < kMedSlots; ++m2) {
+    if (32 * m2 >= cnt) break;
+    for (int sl = 0; sl < 32 && 32 * m2 + sl < cnt; ++sl) {
+      const double x = __shfl_sync(0xffffffffu, v[m2], sl);
+#pragma unroll
+      for (int m = 0; m < kMedSlots; ++m) {
+        lt[m] += x < v[m];
+        le[m] += x <= v[m];
+      }
+    }
+  }
+  double found = 0.0;
+  bool hit = false;
+#pragma unroll
+  for (int m = 0; m < kMedSlots; ++m)
+    if (lane + 32 * m < cnt && lt[m] <= k && k < le[m]) {
+      found = v[m];
+      hit = true;
+    }
+  const unsigned b = __ballot_sync(0xffffffffu, hit);
+  return __shfl_sync(0xffffffffu, found, __ffs(b) - 1);
+}
+
+__device__ __noinline__ double2 median_warp_big(const K5aParams& p, int64_t base, int64_t om, uint64_t mask,
+                                                double sgn, int cnt, int lane) {
+  double re[kMedSlots], im[kMedSlots];
+#pragma unroll
+  for (int m = 0; m < kMedSlots; ++m) re[m] = im[m] = INFINITY;
+  int c = 0;
+  for (int t = 0; t < p.T; ++t) {
+    if (!(mask & (1ull << t))) continue;
+    const int64_t slot = p.off[t] + pmod(om, p.P[t]);
+#pragma unroll
+    for (int m = 0; m < kMedSlots; ++m) {
+      const int i = lane + 32 * m - c;
+      if (i >= 0 && i < p.K[t]) {
+        const double2 y = p.cand_v[(base + slot) * p.Kmax + i];
+        re[m] = sgn * y.x;
+        im[m] = sgn * y.y;
+      }
+    }
+    c += p.K[t];
+  }
+  const int k1 = (cnt - 1) >> 1, k2 = cnt >> 1;
+  double2 z;
+  z.x = warp_kth(re, cnt, k2, lane);
+  z.y = warp_kth(im, cnt, k2, lane);
+  if (!(cnt & 1)) {
+    z.x = 0.5 * (warp_kth(re, cnt, k1, lane) + z.x);
+    z.y = 0.5 * (warp_kth(im, cnt, k1, lane) + z.y);
+  }
+  return z;
+}
+
 // accepted entry `pos` of band j of vector v, one warp
 __device__ __forceinline__ void median_warp(const K5aParams& p, int v, int j, int pos, int lane) {
   {
     const int64_t base = (int64_t)v * p.cw_vec_stride + (int64_t)j * p.sumP;
     const int64_t om = __ldcg(p.acc_w + base + pos);
-    const int32_t mask = __ldcg(p.acc_mask + base + pos);
+    const uint64_t mask = __ldcg((const unsigned long long*)(p.acc_mask + base + pos));
     const double sgn = (om & 1) ? -1.0 : 1.0;
     // lane -> (t, i) over the voting primes in ascending t
     int cnt = 0, my_t = -1, my_i = 0;
     for (int t = 0; t < p.T; ++t) {
-      if (mask & (1 << t)) {
+      if (mask & (1ull << t)) {
         if (lane >= cnt && lane < cnt + p.K[t]) {
           my_t = t;
           my_i = lane - cnt;
@@ -848,23 +903,8 @@ __device__ __forceinline__ void median_warp(const K5aParams& p, int v, int j, in
       }
       z.x = warp_median(re, cnt, lane);
       z.y = warp_median(im, cnt, lane);
-    } else if (lane == 0) {  // more than 32 voting grids (T*K > 32): serial fallback
-      double rv[kMaxVals], iv[kMaxVals];
-      int c = 0;
-      for (int t = 0; t < p.T; ++t)
-        if (mask & (1 << t)) {
-          const int64_t slot = p.off[t] + pmod(om, p.P[t]);
-          for (int i = 0; i < p.K[t]; ++i) {
-            const double2 y = p.cand_v[(base + slot) * p.Kmax + i];
-            rv[c] = sgn * y.x;
-            iv[c] = sgn * y.y;
-            ++c;
-          }
-        }
-      sort_small(rv, c);
-      sort_small(iv, c);
-      z = (c & 1) ? make_double2(rv[c / 2], iv[c / 2])
-                  : make_double2(0.5 * (rv[c / 2 - 1] + rv[c / 2]), 0.5 * (iv[c / 2 - 1] + iv[c / 2]));
+    } else {  // more than 32 voting grids (deterministic variant): rank selection
+      z = median_warp_big(p, base, om, mask, sgn, cnt, lane);
     }
     if (lane == 0) p.acc_z[base + pos] = z;
   }
@@ -1178,10 +1218,10 @@ __global__ void __launch_bounds__(kK6Threads) k6_merge(const __grid_constant__ K
 struct K5Params {
   K5aParams a;
   K5bParams b;
-  const int32_t* vmask;
+  const uint64_t* vmask;
   const int64_t* cand_w;
   int64_t* acc_w;
-  int32_t* acc_mask;
+  uint64_t* acc_mask;
   int32_t* acc_n;    // [vec][band]
   int64_t* work;     // [vec][band * sumP] packed (band << 32 | pos)
   int32_t* work_n;   // [vec]
@@ -1195,8 +1235,8 @@ __global__ void __launch_bounds__(256) k5s_scan(const __grid_constant__ K5Params
   const int v = blockIdx.y;
   const int j = (int)(gid / p.b.sumP);
   const int64_t base = (int64_t)v * p.b.cw_vec_stride + (int64_t)j * p.b.sumP;
-  const int32_t mk = __ldcg(p.vmask + (int64_t)v * p.b.cw_vec_stride + gid);
-  if (__popc(mk) < p.vote_min) return;
+  const uint64_t mk = __ldcg((const unsigned long long*)(p.vmask + (int64_t)v * p.b.cw_vec_stride + gid));
+  if (__popcll(mk) < p.vote_min) return;
   const int pos = atomicAdd(p.acc_n + (int64_t)v * p.b.bn_vec + j, 1);
   p.acc_w[base + pos] = __ldcg(p.cand_w + (int64_t)v * p.b.cw_vec_stride + gid);
   p.acc_mask[base + pos] = mk;
@@ -1487,7 +1527,7 @@ cudaError_t launch_k3(const Plan& p, int t, const double2* Z, int64_t zstride, i
     k.Pt[t2] = p.bk[t2].P;
     k.offt[t2] = p.bk[t2].off;
   }
-  k.vmask = (int32_t*)((char*)ws + L.vmask);
+  k.vmask = (uint64_t*)((char*)ws + L.vmask);
   k.cand_w = (int64_t*)((char*)ws + L.cand_w);
   k.cand_v = (double2*)((char*)ws + L.cand_v);
   k.cw_vec_stride = L.cw_vec;
@@ -1523,10 +1563,10 @@ cudaError_t launch_k45(const Plan& p, int nvec, void* ws, const int* bands, int 
                        int64_t* freqs, double2* coeffs) {
   const WsLayout L = ws_layout(p, p.ws_batch);
   K5Params f{};
-  f.vmask = (const int32_t*)((char*)ws + L.vmask);
+  f.vmask = (const uint64_t*)((char*)ws + L.vmask);
   f.cand_w = (const int64_t*)((char*)ws + L.cand_w);
   f.acc_w = (int64_t*)((char*)ws + L.acc_w);
-  f.acc_mask = (int32_t*)((char*)ws + L.acc_mask);
+  f.acc_mask = (uint64_t*)((char*)ws + L.acc_mask);
   f.acc_n = (int32_t*)((char*)ws + L.acc_n);
   f.work = (int64_t*)((char*)ws + L.work);
   f.work_n = (int32_t*)((char*)ws + L.work_n);

@@ -347,11 +347,11 @@ WsLayout ws_layout(const Plan& p, int64_t nvec) {
   L.zs = take(p.any_split ? (size_t)L.z_buf * 16 : 0);
   L.cand_w = take((size_t)nvec * L.cw_vec * 8);
   L.cand_v = take((size_t)nvec * L.cw_vec * p.Kmax * 16);
-  L.vmask = take((size_t)nvec * L.cw_vec * 4);
+  L.vmask = take((size_t)nvec * L.cw_vec * 8);
   L.acc_w = take((size_t)nvec * L.cw_vec * 8);
   L.acc_z = take((size_t)nvec * L.cw_vec * 16);
   L.acc_r = take((size_t)nvec * L.cw_vec * 4);
-  L.acc_mask = take((size_t)nvec * L.cw_vec * 4);
+  L.acc_mask = take((size_t)nvec * L.cw_vec * 8);
   // counters acc_n, work_n, ticket: contiguous, zeroed at allocation, re-zeroed by
   // the last K5b CTA of each vector after use
   L.acc_n = take((size_t)nvec * L.bn_vec * 4);
@@ -405,16 +405,18 @@ static dsft_status derive(int64_t N, int64_t s, const dsft_params& prm, Plan& P)
   const int64_t J = (int64_t)ceil(alpha * sqrt(lnN) / 2.0);          // ceil(c2)
   if (J > DSFT_MAX_J) return fail(DSFT_ERR_UNSUPPORTED, "more than DSFT_MAX_J passbands");
   const int64_t halfN_up = (N + 1) / 2;
-  const int T = prm.n_bucket_primes;
-  if (T < 1) return fail(DSFT_ERR_CONFIG, "need at least one bucket prime");
-  if (T > DSFT_MAX_T) return fail(DSFT_ERR_UNSUPPORTED, "T > DSFT_MAX_T");
+  if (prm.n_bucket_primes < 0) return fail(DSFT_ERR_CONFIG, "need at least one bucket prime");
   // bucket-prime pool (reading R6)
   const int64_t lo = (int64_t)ceil(prm.bucket_factor * (double)s);
   const int64_t hi = 2 * lo;
   std::vector<int64_t> pool;
   for (int64_t pr : primes_below(hi))
     if (pr >= lo && largest_prime_factor(pr - 1) <= 13) pool.push_back(pr);
+  // T = 0: the deterministic variant (reading R13) -- every prime of the pool
+  const int T = prm.n_bucket_primes == 0 ? (int)pool.size() : prm.n_bucket_primes;
+  if (T < 1) return fail(DSFT_ERR_CONFIG, "need at least one bucket prime");
   if ((int64_t)pool.size() < T) return fail(DSFT_ERR_CONFIG, "bucket-prime pool smaller than T");
+  if (T > DSFT_MAX_T) return fail(DSFT_ERR_UNSUPPORTED, "T > DSFT_MAX_T");
   // draw T distinct by partial Fisher-Yates with SplitMix64 (reading R7)
   SplitMix64 rng{prm.seed};
   std::vector<int64_t> work = pool;
@@ -425,13 +427,17 @@ static dsft_status derive(int64_t N, int64_t s, const dsft_params& prm, Plan& P)
   }
   std::vector<int64_t> primes(work.begin(), work.begin() + T);
   std::sort(primes.begin(), primes.end());
-  if (prm.vote_min < 1 || prm.vote_min > T) return fail(DSFT_ERR_CONFIG, "vote_min must lie in [1, T]");
+  // vote_min = 0: "more than half" of the T primes, floor(T/2) + 1
+  const int vote_min = prm.vote_min == 0 ? T / 2 + 1 : prm.vote_min;
+  if (vote_min < 1 || vote_min > T) return fail(DSFT_ERR_CONFIG, "vote_min must lie in [1, T]");
 
   std::vector<int64_t> odd;
   for (int64_t pr : primes_below(512))
     if (pr > 2) odd.push_back(pr);
 
   P.params = prm;
+  P.params.n_bucket_primes = T;  // resolved (0 = every pool prime)
+  P.params.vote_min = vote_min;  // resolved (0 = majority)
   P.N = N;
   P.s = s;
   P.kappa = kappa;
@@ -589,7 +595,7 @@ static dsft_status derive(int64_t N, int64_t s, const dsft_params& prm, Plan& P)
   I.alpha = alpha;
   I.tau = prm.tau;
   I.q1 = P.q1;
-  I.vote_min = prm.vote_min;
+  I.vote_min = vote_min;
   I.band_budget = prm.band_budget > 0 ? prm.band_budget : s;
   for (int t = 0; t < T; ++t) {
     I.primes[t] = P.bk[t].P;

@@ -170,6 +170,30 @@ def c3(quick):
     return {"N": N, "s": s, "snr_sweep": out, "ms_per_transform": ms}
 
 
+def det(quick):
+    """SURVEY 8(f) next row 1, the deterministic variant (reading R13): every pool prime
+    (n_bucket_primes = 0), majority vote; throughput and exact support at c1 / c2 sizes,
+    oracle parity where the oracle finishes in seconds (c1)."""
+    out = []
+    prm = dict(n_bucket_primes=0, vote_min=0)
+    for N, s, cfg in ((2 ** 22, 50, 1), (2 ** 26, 200, 2), (2 ** 26, 1000, 2)):
+        pl = planted(N, s, cfg=cfg, trial=0)
+        f = torch.from_numpy(pl.f).to(DEV)
+        plan = d.Plan(N, s, d.make_params(**prm))
+        g = run(plan, f)
+        fr = torch.empty(s, dtype=torch.int64, device=DEV)
+        co = torch.empty(s, dtype=torch.complex128, device=DEV)
+        ms = timed(lambda: plan.dsft_execute(f, fr, co), 5 if quick else 20)
+        row = {"N": N, "s": s, "T": plan.info.T, "vote_min": plan.info.vote_min, "ms_per_transform": ms,
+               "transforms_per_s": 1e3 / ms, **accuracy(g, pl.freqs, pl.fhat, s)}
+        if N == 2 ** 22:
+            row["oracle"] = parity(g, dsft(pl.f, s, OracleParams(**prm)))
+        out.append(row)
+        print("  det", row, flush=True)
+        del f
+    return {"rows": out}
+
+
 def synth_device(N, s, cfg, trial, vector, snr_db, out_row):
     """dsft_synth.planted's draws (same generator, same order), inverse DFT on the device."""
     rng = rng_for(cfg, trial, vector)
@@ -216,7 +240,7 @@ def c4(quick):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--only", default="c0,c1,c2,c3,c4")
+    ap.add_argument("--only", default="c0,c1,c2,c3,c4,det")
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "configs.json"))
     ap.add_argument("--quick", action="store_true")
     a = ap.parse_args()

@@ -36,10 +36,16 @@ def test_plan_matches_oracle(N, s, seed, preset):
 
 
 def test_literal_alpha_and_kappa_override_match():
-    for kw in (dict(alpha_rule="literal"), dict(kappa=5), dict(tau=0.1), dict(bucket_factor=5.0, n_bucket_primes=7, vote_min=4)):
+    for kw in (dict(alpha_rule="literal"), dict(kappa=5), dict(tau=0.1), dict(bucket_factor=5.0, n_bucket_primes=7, vote_min=4),
+               dict(n_bucket_primes=0, vote_min=0), dict(n_bucket_primes=0, vote_min=5), dict(vote_min=0)):
         info = d.dsft_plan_derive_info(2**20, 100, d.make_params(**kw))
         p = derive_plan(2**20, 100, OracleParams(**kw))
         assert (info.w, info.J, info.kappa, list(info.primes[:info.T])) == (p.w, p.J, p.kappa, p.primes)
+        assert (info.T, info.vote_min) == (len(p.primes), p.vote_min)
+    # the deterministic variant at the headline s: T = 37 bucket primes (<= DSFT_MAX_T)
+    info = d.dsft_plan_derive_info(2**26, 1000, d.make_params(n_bucket_primes=0, vote_min=0))
+    p = derive_plan(2**26, 1000, OracleParams(n_bucket_primes=0, vote_min=0))
+    assert info.T == len(p.primes) == 37 and list(info.primes[:info.T]) == p.primes and info.vote_min == 19
 
 
 @pytest.mark.parametrize("N,s,kw", [(30, 4, {}), (4096, 1, {}), (4096, 4097, {}), (4096, 8, dict(tau=0.5)),

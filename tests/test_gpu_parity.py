@@ -275,3 +275,30 @@ def test_headline_config_full_size(s):
     gpu = run_gpu(plan, pl.f)
     assert_parity(gpu, ref, s)
     assert sorted(ref.freqs.tolist()) == pl.freqs.tolist()
+
+
+@pytest.mark.parametrize("N,s", [(2**22, 50), (2**20, 300)])
+def test_deterministic_variant_parity(N, s):
+    """Reading R13 (every pool prime, majority vote): T = 12 and 28 bucket primes --
+    64-bit vote masks, T K > 32 median values per frequency (warp rank selection)."""
+    pl = planted(N, s, cfg=41, trial=0)
+    plan = d.Plan(N, s, d.make_params(n_bucket_primes=0, vote_min=0))
+    ref = dsft(pl.f, s, OracleParams(n_bucket_primes=0, vote_min=0))
+    dp = derive_plan(N, s, OracleParams(n_bucket_primes=0, vote_min=0))
+    assert plan.info.T == len(dp.primes) > 5 and plan.primes() == dp.primes
+    assert_parity(run_gpu(plan, pl.f), ref, s)
+
+
+def test_deterministic_variant_headline_size():
+    """BASELINE config 2 (N = 2^26, s = 1000) with all 37 pool primes: exact support
+    and the planted coefficients (the oracle takes minutes here; parity at the sizes
+    above)."""
+    N, s = 2**26, 1000
+    pl = planted(N, s, cfg=2, trial=0)
+    plan = d.Plan(N, s, d.make_params(n_bucket_primes=0, vote_min=0))
+    assert plan.info.T == 37 and plan.info.vote_min == 19
+    fr, co = run_gpu(plan, pl.f)
+    assert sorted(fr.tolist()) == pl.freqs.tolist()
+    got = dict(zip(fr.tolist(), co))
+    err = max(abs(got[int(w)] - c) for w, c in zip(pl.freqs, pl.fhat))
+    assert err < 1e-3

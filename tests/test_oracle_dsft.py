@@ -246,3 +246,21 @@ def test_zero_input_and_determinism_and_scaling():
     assert np.array_equal(a.freqs, b.freqs) and np.array_equal(a.coeffs, b.coeffs)
     c = dsft(2.0 * pl.f, s, plan=plan)  # exact power-of-two scaling is exact in every stage
     assert np.array_equal(c.freqs, a.freqs) and np.array_equal(c.coeffs, 2.0 * a.coeffs)
+
+
+@pytest.mark.parametrize("N,s", [(1024, 12), (4096, 16), (4096, 30)])
+def test_deterministic_variant_vs_bruteforce_dft(N, s):
+    """Reading R13, the deterministic variant (n_bucket_primes = 0: every pool prime,
+    PAPER.md:40-44, 604-610; vote_min = 0: more than half): exactly
+    s-sparse input, the output set is R_s^opt of the O(N^2) brute-force DFT."""
+    prm = OracleParams(n_bucket_primes=0, vote_min=0)
+    plan = derive_plan(N, s, prm)
+    assert len(plan.primes) > 5 and plan.vote_min == len(plan.primes) // 2 + 1
+    for trial in range(2):
+        pl = planted(N, s, cfg=19, trial=trial)
+        B, fh = centered_dft_bruteforce(pl.f)
+        order = sorted(range(N), key=lambda k: (-abs(fh[k]), B[k]))[:s]
+        res = dsft(pl.f, s, plan=plan)
+        assert sorted(res.freqs.tolist()) == sorted(B[k] for k in order)
+        d = dict(zip(res.freqs.tolist(), res.coeffs))
+        assert max(abs(d[int(B[k])] - fh[k]) for k in order) < 1e-4

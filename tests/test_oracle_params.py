@@ -166,3 +166,15 @@ def test_residue_rule_headline_values():
 def test_config_errors(bad):
     with pytest.raises(ConfigError):
         derive_plan(bad["N"], bad["s"], bad.get("params"))
+
+
+@pytest.mark.parametrize("s", [8, 50, 300, 1000])
+def test_deterministic_variant_plan(s):
+    """Reading R13: n_bucket_primes = 0 takes every prime of the pool (brute-force pool
+    rule, no draw, independent of the seed); vote_min = 0 is floor(T/2) + 1."""
+    ref = [p for p in range(4 * s, 8 * s) if _is_prime_naive(p)
+           and max(d for d in range(2, p) if (p - 1) % d == 0 and _is_prime_naive(d)) <= 13]
+    for seed in (0, 7):
+        p = derive_plan(2**20, s, OracleParams(n_bucket_primes=0, vote_min=0, seed=seed))
+        assert p.primes == ref and p.vote_min == len(ref) // 2 + 1
+    assert derive_plan(2**20, s, OracleParams(n_bucket_primes=0, vote_min=2)).vote_min == 2
