@@ -194,6 +194,57 @@ def det(quick):
     return {"rows": out}
 
 
+def thm4(quick):
+    """the THM4 preset (kappa = O(log N) windows, larger J) at
+    the headline sizes: throughput, exact support, error against the planted spectrum;
+    oracle parity at N = 2^16 (the oracle needs minutes at N = 2^26 here)."""
+    out = []
+    for N, s in ((2 ** 16, 50), (2 ** 22, 50), (2 ** 26, 1000)):
+        pl = planted(N, s, cfg=2, trial=0)
+        f = torch.from_numpy(pl.f).to(DEV)
+        plan = d.Plan(N, s, d.make_params(preset="thm4"))
+        g = run(plan, f)
+        fr = torch.empty(s, dtype=torch.int64, device=DEV)
+        co = torch.empty(s, dtype=torch.complex128, device=DEV)
+        ms = timed(lambda: plan.dsft_execute(f, fr, co), 5 if quick else 20)
+        row = {"N": N, "s": s, "kappa": plan.info.kappa, "J": plan.info.J, "nodes": plan.info.nodes,
+               "ms_per_transform": ms, "transforms_per_s": 1e3 / ms, **accuracy(g, pl.freqs, pl.fhat, s)}
+        if N == 2 ** 16:
+            row["oracle"] = parity(g, dsft(pl.f, s, OracleParams(preset="thm4")))
+        out.append(row)
+        print("  thm4", row, flush=True)
+        del f
+    return {"rows": out}
+
+
+def nsweep(quick):
+    """SURVEY 8(f) next row 3 (PAPER.md:663-673 protocol): runtime vs N at s = 50,
+    N = 2^16 .. 2^30 (2^30 complex128 = 16 GiB, synthesised on the device)."""
+    out = []
+    s = 50
+    for e in range(16, 31, 2):
+        N = 2 ** e
+        plan = d.Plan(N, s, d.make_params(seed=0))
+        f = torch.empty(N, dtype=torch.complex128, device=DEV)
+        try:
+            freqs, fhat = synth_device(N, s, 5, 0, 0, None, f)
+        except RuntimeError as e:  # device synthesis out of memory: record and stop
+            out.append({"N": N, "s": s, "error": str(e)[:200]})
+            break
+        g = run(plan, f)
+        fr = torch.empty(s, dtype=torch.int64, device=DEV)
+        co = torch.empty(s, dtype=torch.complex128, device=DEV)
+        ms = timed(lambda: plan.dsft_execute(f, fr, co), 5 if quick else 20)
+        row = {"N": N, "s": s, "ms_per_transform": ms, "transforms_per_s": 1e3 / ms,
+               "window_MB": plan.info.nodes * (2 * plan.info.kappa + 1) * 16 / 1e6,
+               **accuracy(g, freqs, fhat, s)}
+        out.append(row)
+        print("  nsweep", row, flush=True)
+        del f
+        torch.cuda.empty_cache()
+    return {"rows": out}
+
+
 def synth_device(N, s, cfg, trial, vector, snr_db, out_row):
     """dsft_synth.planted's draws (same generator, same order), inverse DFT on the device."""
     rng = rng_for(cfg, trial, vector)
@@ -205,9 +256,14 @@ def synth_device(N, s, cfg, trial, vector, snr_db, out_row):
     chat = torch.zeros(N, dtype=torch.complex128, device=DEV)
     chat[torch.from_numpy(freqs % N).to(DEV)] = torch.from_numpy(c).to(DEV)
     f = N * torch.fft.ifft(chat)
-    n = torch.complex(torch.from_numpy(rng.standard_normal(N)).to(DEV), torch.from_numpy(rng.standard_normal(N)).to(DEV))
-    n *= torch.linalg.vector_norm(f) / (torch.linalg.vector_norm(n) * 10.0 ** (snr_db / 20.0))
-    out_row.copy_(f + n)
+    del chat
+    if snr_db is None:  # noiseless
+        out_row.copy_(f)
+    else:
+        n = torch.complex(torch.from_numpy(rng.standard_normal(N)).to(DEV),
+                          torch.from_numpy(rng.standard_normal(N)).to(DEV))
+        n *= torch.linalg.vector_norm(f) / (torch.linalg.vector_norm(n) * 10.0 ** (snr_db / 20.0))
+        out_row.copy_(f + n)
     order = np.argsort(freqs)
     sign = np.where(freqs % 2 == 0, 1.0, -1.0)
     return freqs[order], (sign * c)[order]
@@ -240,7 +296,7 @@ def c4(quick):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--only", default="c0,c1,c2,c3,c4,det")
+    ap.add_argument("--only", default="c0,c1,c2,c3,c4,det,thm4,nsweep")
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "configs.json"))
     ap.add_argument("--quick", action="store_true")
     a = ap.parse_args()
