@@ -131,7 +131,7 @@ struct Plan {
   // K1 of bucket prime t+1 runs on `aux` into the other Z buffer and K3 of prime
   // t-1 on `aux3` while K2 of prime t runs on the caller's stream (pipe_ev:
   // fork/join events, no timing)
-  cudaStream_t aux = nullptr, aux3 = nullptr;
+  cudaStream_t aux = nullptr, aux3 = nullptr, aux2 = nullptr;  // aux2: every other K2 launch
   std::string jit_why;         // why some bucket runs the runtime-radix K2 ("" if none)
   std::vector<cudaEvent_t> pipe_ev;
 };

@@ -943,6 +943,7 @@ void dsft_plan_destroy(dsft_plan* pl) {
   for (cudaEvent_t e : pl->p.pipe_ev) cudaEventDestroy(e);
   if (pl->p.aux) cudaStreamDestroy(pl->p.aux);
   if (pl->p.aux3) cudaStreamDestroy(pl->p.aux3);
+  if (pl->p.aux2) cudaStreamDestroy(pl->p.aux2);
   if (pl->p.dev_tables) cudaFree(pl->p.dev_tables);
   if (pl->p.ws_owned && pl->p.ws) cudaFree(pl->p.ws);
   if (pl->p.io_dev) cudaFree(pl->p.io_dev);
@@ -1079,7 +1080,8 @@ static dsft_status ensure_pipe(Plan& p) {
   CU(cudaDeviceGetStreamPriorityRange(&lo, &hi), "stream priority range");
   if (!p.aux) CU(cudaStreamCreateWithPriority(&p.aux, cudaStreamNonBlocking, hi), "create aux stream");
   if (!p.aux3) CU(cudaStreamCreateWithPriority(&p.aux3, cudaStreamNonBlocking, hi), "create aux3 stream");
-  const size_t need = 3 * (size_t)p.T + 3;
+  if (!p.aux2) CU(cudaStreamCreateWithPriority(&p.aux2, cudaStreamNonBlocking, lo), "create aux2 stream");
+  const size_t need = 3 * (size_t)p.T + 4;
   while (p.pipe_ev.size() < need) {
     cudaEvent_t e;
     CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "create pipeline event");
@@ -1099,9 +1101,17 @@ static dsft_status run_bands(Plan& p, const double2* f, int64_t ld, int nv, cons
   cudaEvent_t* evK2 = p.pipe_ev.data() + p.T;      // [T] K2(t) done (st)
   cudaEvent_t* evK3 = p.pipe_ev.data() + 2 * p.T;  // [T] K3(t) done (aux3)
   cudaEvent_t evFork = p.pipe_ev[3 * p.T], evJoin1 = p.pipe_ev[3 * p.T + 1], evJoin3 = p.pipe_ev[3 * p.T + 2];
+  cudaEvent_t evJoin2 = p.pipe_ev[3 * p.T + 3];
+  // K2 launches alternate between the caller's stream and aux2 (DSFT_K2_STREAMS=1:
+  // all on the caller's stream): K2(k+1) depends only on K1(k+1), so its CTAs fill
+  // the SMs K2(k)'s last wave leaves idle
+  const char* k2s = getenv("DSFT_K2_STREAMS");
+  const bool k2alt = !serial && !(k2s && strcmp(k2s, "1") == 0);
+  cudaStream_t a2 = k2alt ? p.aux2 : st;
   CU(cudaEventRecord(evFork, st), "pipeline fork");
   CU(cudaStreamWaitEvent(a1, evFork, 0), "pipeline fork wait");
   CU(cudaStreamWaitEvent(a3, evFork, 0), "pipeline fork wait");
+  if (k2alt) CU(cudaStreamWaitEvent(a2, evFork, 0), "pipeline fork wait");
   // k: processing position; t = p.order[k]: bucket prime.  Two-buffer pipeline (one
   // K1 launch per prime): Z buffer k % kZBufs, K1(k) waits for K3(k - kZBufs).
   // Grouped K1 (every prime its own Z region): one launch per group, no K3 wait.
@@ -1145,9 +1155,10 @@ static dsft_status run_bands(Plan& p, const double2* f, int64_t ld, int nv, cons
     double2* Z;
     int64_t zs;
     zfor(k, t, Z, zs);
-    CU(cudaStreamWaitEvent(st, evK1[gof[k]], 0), "K2 waits K1");
-    CU(timed(p, 1, st, [&] { return launch_k2(p, t, Z, zs, nv, p.ws, bands, nb, st); }), "K2 prime_dft launch");
-    CU(cudaEventRecord(evK2[k], st), "K2 event");
+    cudaStream_t sk = (k & 1) ? a2 : st;
+    CU(cudaStreamWaitEvent(sk, evK1[gof[k]], 0), "K2 waits K1");
+    CU(timed(p, 1, sk, [&] { return launch_k2(p, t, Z, zs, nv, p.ws, bands, nb, sk); }), "K2 prime_dft launch");
+    CU(cudaEventRecord(evK2[k], sk), "K2 event");
     CU(cudaStreamWaitEvent(a3, evK2[k], 0), "K3 waits K2");
     CU(timed(p, 2, a3, [&] { return launch_k3(p, t, Z, zs, nv, p.ws, bands, nb, a3, p.order, k); }),
        "K3 identify launch");
@@ -1157,6 +1168,10 @@ static dsft_status run_bands(Plan& p, const double2* f, int64_t ld, int nv, cons
   CU(cudaEventRecord(evJoin3, a3), "pipeline join");
   CU(cudaStreamWaitEvent(st, evJoin1, 0), "pipeline join wait");
   CU(cudaStreamWaitEvent(st, evJoin3, 0), "pipeline join wait");
+  if (k2alt) {
+    CU(cudaEventRecord(evJoin2, a2), "pipeline join");
+    CU(cudaStreamWaitEvent(st, evJoin2, 0), "pipeline join wait");
+  }
   CU(timed(p, 3, st, [&] { return launch_k45(p, nv, p.ws, bands, nb, st, freqs, coeffs); }),
      "K456 vote/estimate/merge launch");
   return DSFT_OK;
