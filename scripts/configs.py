@@ -245,6 +245,40 @@ def nsweep(quick):
     return {"rows": out}
 
 
+def noise22(quick):
+    """noise robustness at N = 2^22, s = 50 (PAPER.md:685-702
+    protocol), avg-l1 against the planted spectrum per SNR."""
+    N, s = 2 ** 22, 50
+    trials = 3 if quick else 10
+    plan = d.Plan(N, s, d.make_params(seed=0))
+    out = []
+    for snr in (0.0, 10.0, 20.0, 40.0, 60.0, 80.0):
+        l1, exact = [], 0
+        for t in range(trials):
+            pl = planted(N, s, cfg=6, trial=t, snr_db=snr)
+            a = accuracy(run(plan, torch.from_numpy(pl.f).to(DEV)), pl.freqs, pl.fhat, s)
+            l1.append(a["avg_l1"])
+            exact += a["support_exact"]
+        out.append({"snr_db": snr, "avg_l1_mean": float(np.mean(l1)), "avg_l1_max": float(np.max(l1)),
+                    "support_exact": exact, "trials": trials})
+        print("  noise22", out[-1], flush=True)
+    return {"N": N, "s": s, "snr_sweep": out}
+
+
+def dense(quick):
+    """Context only (the FFTW analogue): a dense complex128 cuFFT of
+    the whole vector (torch.fft.fft, a library call) at N = 2^22 and 2^26."""
+    out = []
+    for e in (22, 26):
+        N = 2 ** e
+        x = torch.randn(N, dtype=torch.complex128, device=DEV)
+        ms = timed(lambda: torch.fft.fft(x), 5 if quick else 20)
+        out.append({"N": N, "ms": ms, "transforms_per_s": 1e3 / ms})
+        print("  dense", out[-1], flush=True)
+        del x
+    return {"rows": out}
+
+
 def synth_device(N, s, cfg, trial, vector, snr_db, out_row):
     """dsft_synth.planted's draws (same generator, same order), inverse DFT on the device."""
     rng = rng_for(cfg, trial, vector)
@@ -296,7 +330,7 @@ def c4(quick):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--only", default="c0,c1,c2,c3,c4,det,thm4,nsweep")
+    ap.add_argument("--only", default="c0,c1,c2,c3,c4,det,thm4,nsweep,noise22,dense")
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "configs.json"))
     ap.add_argument("--quick", action="store_true")
     a = ap.parse_args()
