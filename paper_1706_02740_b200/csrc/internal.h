@@ -60,6 +60,7 @@ struct Bucket {
   int fft_variant = 0;           // K2 instantiation: 0 <64,8>, 1 <288,2>, 2 <512,1>
   int fft_group = 1;             // reserved (warp-group sub-FFT layout, not used)
   const void* k2_jit = nullptr;  // plan-time NVRTC specialisation of K2 (cudaKernel_t), or null
+  const void* k3_jit = nullptr;  // K3 with this prime's residue tuple as constants (NVRTC), or null
   int jit_threads = 0;           // its CTA size (default fft_threads)
   int cl = 0;                    // > 1: cluster mode (k2_cl, C = fac[0] CTAs per row, DSMEM); falls back
                                  // to the split mode below if the specialised kernel is unavailable
@@ -177,6 +178,8 @@ const void* jit_k2(int nt, int minb, const int* fac, int nfac, size_t smem_bytes
                    unsigned twf = 0);
 bool jit_k2_compile_only(int nt, int minb, const int* fac, int nfac, std::string* why, bool cluster = false,
                          unsigned twf = 0);
+// jit.cpp: k3_identify<rmax, rs...> (residue primes as constants), or nullptr + *why
+const void* jit_k3(int rmax, const int* rs, int K, std::string* why);
 cudaError_t launch_k6_blocks(const int64_t* bw, const double2* bc, const double* bm, const int32_t* bnz, int nblocks,
                              int64_t budget, int64_t blk_vec, int64_t bn_vec, int64_t s, int nvec, int64_t* freqs,
                              double2* coeffs, cudaStream_t st);

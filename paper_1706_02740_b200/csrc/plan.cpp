@@ -743,6 +743,15 @@ static void specialise_k2(Plan& P) {
   cudaGetDevice(&dev);
   std::vector<std::thread> th;
   std::vector<std::string> why(P.T);
+  std::vector<std::string> why3(P.T);
+  const char* k3e = getenv("DSFT_K3_JIT");  // "0": runtime-residue K3 (experiments)
+  const bool k3jit = !(k3e && strcmp(k3e, "0") == 0);
+  for (int t = 0; t < P.T && k3jit; ++t)
+    th.emplace_back([&, t, dev] {
+      cudaSetDevice(dev);
+      Bucket& bb = P.bk[t];
+      bb.k3_jit = jit_k3(bb.r[bb.K - 1], bb.r, bb.K, &why3[t]);
+    });
   for (int t = 0; t < P.T; ++t) {
     Bucket& b = P.bk[t];
     if ((b.split && !b.cl) || b.fft_variant == 0) continue;
@@ -770,8 +779,8 @@ static void specialise_k2(Plan& P) {
   for (auto& x : th) x.join();
   P.jit_why.clear();
   for (int t = 0; t < P.T; ++t)
-    if (!why[t].empty()) {
-      P.jit_why = "P=" + std::to_string(P.bk[t].P) + ": " + why[t];
+    if (!why[t].empty() || !why3[t].empty()) {
+      P.jit_why = "P=" + std::to_string(P.bk[t].P) + ": " + (why[t].empty() ? "K3: " + why3[t] : why[t]);
       break;
     }
 }
