@@ -179,7 +179,7 @@ const void* jit_k2(int nt, int minb, const int* fac, int nfac, size_t smem_bytes
 bool jit_k2_compile_only(int nt, int minb, const int* fac, int nfac, std::string* why, bool cluster = false,
                          unsigned twf = 0);
 // jit.cpp: k3_identify<rmax, rs...> (residue primes as constants), or nullptr + *why
-const void* jit_k3(int rmax, const int* rs, int K, std::string* why);
+const void* jit_k3(int rmax, int P, const int* rs, int K, std::string* why);
 cudaError_t launch_k6_blocks(const int64_t* bw, const double2* bc, const double* bm, const int32_t* bnz, int nblocks,
                              int64_t budget, int64_t blk_vec, int64_t bn_vec, int64_t s, int nvec, int64_t* freqs,
                              double2* coeffs, cudaStream_t st);

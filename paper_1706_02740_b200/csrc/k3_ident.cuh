@@ -66,32 +66,35 @@ __device__ __forceinline__ void residue_argmax(const double2* __restrict__ col, 
 }
 
 template <int R>
-__device__ __forceinline__ void k3_res(const K3Params& p, const double2* col, int i, int64_t& Rc, double2* yv) {
+__device__ __forceinline__ void k3_res(const K3Params& p, int64_t P, const double2* col, int i, int64_t& Rc,
+                                       double2* yv) {
   int b = 0;
   double2 y = make_double2(0.0, 0.0);
-  residue_argmax<R>(col, p.P, p.shift_base[i], p.invL[i], b, y);
+  residue_argmax<R>(col, P, p.shift_base[i], p.invL[i], b, y);
   Rc += (int64_t)b * p.crtE[i + 1];
   yv[i] = y;
 }
 
 // RMAX: largest residue prime of the runtime-residue path; Rs...: the residue
 // primes as compile-time constants (plan-common tuples; empty = runtime path)
-template <int RMAX, int... Rs>
+// PC > 0: the bucket prime as a constant (plan-time kernels), 0: p.P
+template <int RMAX, int PC, int... Rs>
 __global__ void __launch_bounds__(256, sizeof...(Rs) > 0 ? 2 : 1) k3_identify(const __grid_constant__ K3Params p) {
+  const int64_t P = PC > 0 ? (int64_t)PC : p.P;
   const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (gid >= (int64_t)p.nb * p.P) return;
+  if (gid >= (int64_t)p.nb * P) return;
   const int v = blockIdx.y;
-  const int jl = (int)(gid / p.P);
-  const int64_t pos = gid - (int64_t)jl * p.P;  // array position: bucket a = binat[pos] (pos < P-1), 0 (pos = P-1)
+  const int jl = (int)(gid / P);
+  const int64_t pos = gid - (int64_t)jl * P;  // array position: bucket a = binat[pos] (pos < P-1), 0 (pos = P-1)
   const int j = p.j0 + jl;
-  const int64_t Mr = p.P - 1;
+  const int64_t Mr = P - 1;
   const int64_t a = pos == Mr ? 0 : (int64_t)__ldg(p.binat + pos);
-  const double2* col = p.Z + (int64_t)v * p.z_vec_stride + (int64_t)j * p.S * p.P + pos;
+  const double2* col = p.Z + (int64_t)v * p.z_vec_stride + (int64_t)j * p.S * P + pos;
   int64_t R = a * p.crtE[0];
   double2 yv[kK3MaxK];
   if constexpr (sizeof...(Rs) > 0) {
     int i = 0;
-    ((k3_res<Rs>(p, col, i, R, yv), ++i), ...);
+    ((k3_res<Rs>(p, P, col, i, R, yv), ++i), ...);
   } else
   for (int i = 0; i < p.K; ++i) {
     int b = 0;
@@ -100,7 +103,7 @@ __global__ void __launch_bounds__(256, sizeof...(Rs) > 0 ? 2 : 1) k3_identify(co
     switch (p.r[i]) {
 #define DSFT_RES(RR) \
   case RR:           \
-    if constexpr (RR <= RMAX) residue_argmax<RR>(col, p.P, sb, p.invL[i], b, y); \
+    if constexpr (RR <= RMAX) residue_argmax<RR>(col, P, sb, p.invL[i], b, y); \
     break;
       DSFT_RES(3) DSFT_RES(5) DSFT_RES(7) DSFT_RES(11) DSFT_RES(13) DSFT_RES(17) DSFT_RES(19) DSFT_RES(23)
       DSFT_RES(29) DSFT_RES(31)

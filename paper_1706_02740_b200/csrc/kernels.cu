@@ -1229,8 +1229,8 @@ cudaError_t kernels_init() {
   if (const char* co = getenv("DSFT_CARVEOUT")) {  // experiment: one shared-memory carveout for all kernels
     const int pct = atoi(co);
     const void* fs[] = {(const void*)k1_gather_mix_fast<6>, (const void*)k1_gather_mix_fast<4>,
-                        (const void*)k3_identify<7>, (const void*)k3_identify<13>, (const void*)k3_identify<17>,
-                        (const void*)k3_identify<31>, (const void*)k5s_scan, (const void*)k5a_medians,
+                        (const void*)k3_identify<7, 0>, (const void*)k3_identify<13, 0>, (const void*)k3_identify<17, 0>,
+                        (const void*)k3_identify<31, 0>, (const void*)k5s_scan, (const void*)k5a_medians,
                         (const void*)k5b_select, (const void*)k6_merge};
     for (const void* f : fs)
       if ((e = cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, pct))) return e;
@@ -1428,10 +1428,10 @@ cudaError_t launch_k3(const Plan& p, int t, const double2* Z, int64_t zstride, i
     void* args[] = {(void*)&k};
     return cudaLaunchKernel(b.k3_jit, grid, dim3(256), args, 0, st);
   }
-  if (p.Rmax <= 7) k3_identify<7><<<grid, 256, 0, st>>>(k);
-  else if (p.Rmax <= 13) k3_identify<13><<<grid, 256, 0, st>>>(k);
-  else if (p.Rmax <= 17) k3_identify<17><<<grid, 256, 0, st>>>(k);
-  else k3_identify<31><<<grid, 256, 0, st>>>(k);
+  if (p.Rmax <= 7) k3_identify<7, 0><<<grid, 256, 0, st>>>(k);
+  else if (p.Rmax <= 13) k3_identify<13, 0><<<grid, 256, 0, st>>>(k);
+  else if (p.Rmax <= 17) k3_identify<17, 0><<<grid, 256, 0, st>>>(k);
+  else k3_identify<31, 0><<<grid, 256, 0, st>>>(k);
   return cudaGetLastError();
 }
 

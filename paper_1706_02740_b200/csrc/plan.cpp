@@ -750,7 +750,7 @@ static void specialise_k2(Plan& P) {
     th.emplace_back([&, t, dev] {
       cudaSetDevice(dev);
       Bucket& bb = P.bk[t];
-      bb.k3_jit = jit_k3(bb.r[bb.K - 1], bb.r, bb.K, &why3[t]);
+      bb.k3_jit = jit_k3(bb.r[bb.K - 1], (int)bb.P, bb.r, bb.K, &why3[t]);
     });
   for (int t = 0; t < P.T; ++t) {
     Bucket& b = P.bk[t];
