@@ -173,9 +173,10 @@ class Plan:
         _check(lib().dsft_plan_get_info(self._h, C.byref(self.info)))
 
     def close(self):
-        if getattr(self, "_h", None):
-            lib().dsft_plan_destroy(self._h)
-            self._h = None
+        h = getattr(self, "_h", None)
+        self._h = None
+        if h and _lib is not None and callable(lib):  # (at interpreter exit the module may be torn down)
+            _lib.dsft_plan_destroy(h)
 
     __del__ = close
 

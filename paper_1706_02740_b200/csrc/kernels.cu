@@ -1086,7 +1086,10 @@ __device__ void merge_range(const K6Params& p, int v, int64_t e_lo, int64_t e_hi
   }
 }
 
+__device__ __forceinline__ void pdl_wait6() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 __global__ void __launch_bounds__(kK6Threads) k6_merge(const __grid_constant__ K6Params p) {
+  pdl_wait6();
   extern __shared__ unsigned char k6_smem[];
   __shared__ int32_t pre[kK6MaxBlocks + 1];
   double* sm_m = (double*)k6_smem;
@@ -1117,7 +1120,14 @@ struct K5Params {
   int vote_min, nb;
 };
 
+// Programmatic dependent launch inside the tail (K5s -> K5a -> K5b -> K6): each
+// kernel lets its successor launch as soon as all its CTAs are resident, and the
+// successor waits for the predecessor's completion (and memory) before reading it.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 __global__ void __launch_bounds__(256) k5s_scan(const __grid_constant__ K5Params p) {
+  pdl_trigger();
   const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (gid >= (int64_t)p.nb * p.b.sumP) return;
   const int v = blockIdx.y;
@@ -1133,6 +1143,8 @@ __global__ void __launch_bounds__(256) k5s_scan(const __grid_constant__ K5Params
 }
 
 __global__ void __launch_bounds__(256) k5a_medians(const __grid_constant__ K5Params p) {
+  pdl_trigger();
+  pdl_wait();
   const int v = blockIdx.y;
   const int lane = threadIdx.x & 31;
   const int nwarps = gridDim.x * (blockDim.x >> 5);
@@ -1156,6 +1168,8 @@ __device__ unsigned long long g_k5trace[64][4];
 #endif
 
 __global__ void __launch_bounds__(kK5Threads) k5b_select(const __grid_constant__ K5Params p) {
+  pdl_trigger();
+  pdl_wait();
   K5T(0);
   extern __shared__ unsigned char k5_smem[];
   __shared__ int s_nz, s_last;
@@ -1453,6 +1467,26 @@ static K6Params k6_params(const int64_t* bw, const double2* bc, const double* bm
   return k;
 }
 
+// launch with programmatic stream serialization (DSFT_PDL=0: plain stream order)
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 g, dim3 b, size_t smem, cudaStream_t st, Args... args) {
+  static const bool off = [] {
+    const char* e = getenv("DSFT_PDL");
+    return e && strcmp(e, "0") == 0;
+  }();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = g;
+  cfg.blockDim = b;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = off ? 0 : 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 cudaError_t launch_k45(const Plan& p, int nvec, void* ws, const int* bands, int nbands, cudaStream_t st,
                        int64_t* freqs, double2* coeffs) {
   const WsLayout L = ws_layout(p, p.ws_batch);
@@ -1508,10 +1542,10 @@ cudaError_t launch_k45(const Plan& p, int nvec, void* ws, const int* bands, int 
   cudaError_t e;
   k5s_scan<<<dim3(cdiv((int64_t)nbands * p.sumP, 256), nvec), 256, 0, st>>>(f);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  k5a_medians<<<dim3(2 * 148, nvec), 256, 0, st>>>(f);
-  if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  k5b_select<<<dim3(nbands, nvec), kK5Threads, kRankTile * 2 * 8 + kRankTile * 8, st>>>(f);
-  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  if ((e = launch_pdl(k5a_medians, dim3(2 * 148, nvec), dim3(256), 0, st, f)) != cudaSuccess) return e;
+  if ((e = launch_pdl(k5b_select, dim3(nbands, nvec), dim3(kK5Threads), kRankTile * 2 * 8 + kRankTile * 8, st, f)) !=
+      cudaSuccess)
+    return e;
   if (!freqs) return cudaSuccess;  // sharded: merged after the allgather
   if (nbands != p.J) return cudaErrorInvalidValue;
   return launch_k6_blocks(k.band_w, k.band_c, k.band_m, k.band_nz, p.J, p.info.band_budget, L.band_vec, L.bn_vec, p.s,
@@ -1524,8 +1558,7 @@ cudaError_t launch_k6_blocks(const int64_t* bw, const double2* bc, const double*
   if (nblocks > kK6MaxBlocks) return cudaErrorInvalidValue;
   const K6Params k = k6_params(bw, bc, bm, bnz, nblocks, budget, blk_vec, bn_vec, s, freqs, coeffs);
   const int64_t cap = std::max<int64_t>((int64_t)nblocks * budget, s);
-  k6_merge<<<dim3(cdiv(cap, kK6Threads), nvec), kK6Threads, kK6Stage * 16, st>>>(k);
-  return cudaGetLastError();
+  return launch_pdl(k6_merge, dim3(cdiv(cap, kK6Threads), nvec), dim3(kK6Threads), kK6Stage * 16, st, k);
 }
 
 cudaError_t launch_k6(const Plan& p, int nvec, void* ws, int64_t* freqs, double2* coeffs, cudaStream_t st) {
