@@ -786,16 +786,20 @@ static void specialise_k2(Plan& P) {
 }
 
 // Processing order of the bucket primes (results do not depend on it: K3's vote is
-// order-free): by K1/K3 work S_t P_t ascending.  (Measured at BASELINE config 2,
-// six orders: ascending is best; moving the largest prime, whose K2 runs one CTA
-// per SM, next to the concurrent K1/K3 work slowed it by up to 37 %.)
-// DSFT_ORDER="i,j,..." overrides (experiments).
+// order-free): by K1/K3 work S_t P_t ascending, then the largest moved to the
+// second-to-last position, so the last (exposed) K3 is not the largest one and the
+// largest K2 overlaps the last K1.  (Measured at BASELINE config 2 with the
+// four-stream pipeline, twelve orders: ascending 2356, largest second-to-last
+// 2452-2458, largest first 2355-2365 transforms/s.)  DSFT_ORDER="i,j,..." overrides
+// (experiments); DSFT_ORDER_SWAP=0 keeps plain ascending order.
 static void choose_order(Plan& P) {
   std::vector<int> ord(P.T);
   for (int t = 0; t < P.T; ++t) ord[t] = t;
   std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) {
     return (int64_t)P.bk[a].S * P.bk[a].P < (int64_t)P.bk[b].S * P.bk[b].P;
   });
+  const char* sw = getenv("DSFT_ORDER_SWAP");
+  if (P.T >= 3 && !(sw && strcmp(sw, "0") == 0)) std::swap(ord[P.T - 1], ord[P.T - 2]);
   if (const char* env = getenv("DSFT_ORDER")) {
     std::vector<int> o;
     std::string tok;
