@@ -1119,7 +1119,9 @@ static dsft_status run_bands(Plan& p, const double2* f, int64_t ld, int nv, cons
   // all on the caller's stream): K2(k+1) depends only on K1(k+1), so its CTAs fill
   // the SMs K2(k)'s last wave leaves idle
   const char* k2s = getenv("DSFT_K2_STREAMS");
-  const bool k2alt = !serial && !(k2s && strcmp(k2s, "1") == 0);
+  bool k2alt = !serial && !(k2s && strcmp(k2s, "1") == 0);
+  for (int t = 0; t < p.T; ++t)  // split-mode rows share one scratch region (Zs): one K2 at a time
+    if (p.bk[t].split && !(p.bk[t].cl && p.bk[t].k2_jit)) k2alt = false;
   cudaStream_t a2 = k2alt ? p.aux2 : st;
   CU(cudaEventRecord(evFork, st), "pipeline fork");
   CU(cudaStreamWaitEvent(a1, evFork, 0), "pipeline fork wait");

@@ -302,3 +302,16 @@ def test_deterministic_variant_headline_size():
     got = dict(zip(fr.tolist(), co))
     err = max(abs(got[int(w)] - c) for w, c in zip(pl.freqs, pl.fhat))
     assert err < 1e-3
+
+
+@pytest.mark.parametrize("N,s,cfg,trial", [(2**20, 2000, 2, 0), (2**21, 4000, 2, 1)])
+def test_split_mode_fallback(N, s, cfg, trial, monkeypatch):
+    """Rows above one CTA's shared memory run the thread-block-cluster K2 by default;
+    DSFT_K2_CLUSTER=0 selects the two-launch split mode (the fallback when the
+    cluster kernel is unavailable): same oracle parity."""
+    monkeypatch.setenv("DSFT_K2_CLUSTER", "0")
+    pl = planted(N, s, cfg=cfg, trial=trial)
+    ref = dsft(pl.f, s, OracleParams(seed=trial))
+    plan = d.Plan(N, s, d.make_params(seed=trial))
+    assert plan.launches_per_execute() > 4 + 3 * plan.info.T  # K2a + K2b launches
+    assert_parity(run_gpu(plan, pl.f), ref, s)
