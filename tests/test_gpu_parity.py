@@ -187,6 +187,27 @@ def test_large_batch_equals_single():
         assert np.array_equal(frn[v], f1) and np.array_equal(con[v], c1)
 
 
+def test_config4_vector_size_batched_parity():
+    """BASELINE config 4 at its per-vector size in the batched launch configuration
+    (N = 2^24, s = 256, 20 dB noise, one seed per vector; 6 vectors = 1.5 GiB): oracle
+    parity on three of them, and the batched results equal single executes."""
+    N, s, B = 2**24, 256, 6
+    fs = [planted(N, s, cfg=4, trial=v, vector=v, snr_db=20.0).f for v in range(B)]
+    plan = d.Plan(N, s)
+    fdev = torch.empty(B * N, dtype=torch.complex128, device=DEV)
+    for v in range(B):
+        fdev[v * N:(v + 1) * N].copy_(torch.from_numpy(fs[v]))
+    fr = torch.empty(B * s, dtype=torch.int64, device=DEV)
+    co = torch.empty(B * s, dtype=torch.complex128, device=DEV)
+    plan.dsft_execute_batched(fdev, B, N, fr, co)
+    torch.cuda.synchronize()
+    frn, con = fr.cpu().numpy().reshape(B, s), co.cpu().numpy().reshape(B, s)
+    for v in (0, 2, B - 1):
+        assert_parity((frn[v], con[v]), dsft(fs[v], s, OracleParams()), s)
+    f1, c1 = run_gpu(plan, fs[1])
+    assert np.array_equal(frn[1], f1) and np.array_equal(con[1], c1)
+
+
 def test_host_path_equals_device_path():
     N, s = 2**16, 50
     pl = planted(N, s, cfg=35, trial=0)
