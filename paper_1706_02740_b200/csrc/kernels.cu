@@ -854,11 +854,21 @@ __device__ void select_band(const K5bParams& p, int v, int j, double* sm_m, int6
       }
     }
     __syncthreads();
-    for (int e = tid; e < n; e += kK5Threads) {  // rank 1: (|z|^2 desc, omega asc); keep rank < budget
-      const double my_m = sm_m[e];
-      const int64_t my_w = sm_w[e];
+    // kSub lanes per entry, each counting a strided quarter of the list (a band holds
+    // only ~70 entries: one lane per entry left most warps idle and each working warp
+    // issuing ~5 k dependent instructions, ~10 us per CTA)
+    constexpr int kSub = 4;
+    const int sub = tid & (kSub - 1);
+    for (int e0 = 0; e0 < n; e0 += kK5Threads / kSub) {  // rank 1: (|z|^2 desc, omega asc); keep rank < budget
+      const int e = e0 + tid / kSub;
+      const double my_m = e < n ? sm_m[e] : 0.0;
+      const int64_t my_w = e < n ? sm_w[e] : 0;
       int rank = 0;
-      for (int i = 0; i < n; ++i) rank += (sm_m[i] > my_m || (sm_m[i] == my_m && sm_w[i] < my_w)) ? 1 : 0;
+      if (e < n)
+        for (int i = sub; i < n; i += kSub) rank += (sm_m[i] > my_m || (sm_m[i] == my_m && sm_w[i] < my_w)) ? 1 : 0;
+      rank += __shfl_xor_sync(0xffffffffu, rank, 1);
+      rank += __shfl_xor_sync(0xffffffffu, rank, 2);
+      if (e >= n || sub != 0) continue;
       double m2 = -2.0;  // not kept: never ranks ahead
       if (rank < p.budget) {
         const double2 z = ldcg2(accz + e);
@@ -869,12 +879,16 @@ __device__ void select_band(const K5bParams& p, int v, int j, double* sm_m, int6
       sm_m2[e] = m2;
     }
     __syncthreads();
-    for (int e = tid; e < n; e += kK5Threads) {  // rank 2 among kept -> output slot
-      const double my_m = sm_m2[e];
-      if (my_m < -1.5) continue;
-      const int64_t my_w = sm_w[e];
+    for (int e0 = 0; e0 < n; e0 += kK5Threads / kSub) {  // rank 2 among kept -> output slot
+      const int e = e0 + tid / kSub;
+      const double my_m = e < n ? sm_m2[e] : -2.0;
+      const int64_t my_w = e < n ? sm_w[e] : 0;
       int rank = 0;
-      for (int i = 0; i < n; ++i) rank += (sm_m2[i] > my_m || (sm_m2[i] == my_m && sm_w[i] < my_w)) ? 1 : 0;
+      if (my_m >= -1.5)
+        for (int i = sub; i < n; i += kSub) rank += (sm_m2[i] > my_m || (sm_m2[i] == my_m && sm_w[i] < my_w)) ? 1 : 0;
+      rank += __shfl_xor_sync(0xffffffffu, rank, 1);
+      rank += __shfl_xor_sync(0xffffffffu, rank, 2);
+      if (my_m < -1.5 || sub != 0) continue;
       const double2 z = ldcg2(accz + e);
       const double gh = ghat_dev(p.c1, my_w - q);
       const int64_t o = (int64_t)v * p.band_vec + (int64_t)j * p.budget + rank;
@@ -988,6 +1002,7 @@ struct K6Params {
 };
 
 constexpr int kK6Threads = 256;
+constexpr int kK6Ranks = 64;  // output ranks per CTA (4 lanes per rank)
 constexpr int kK6MaxBlocks = 512;
 constexpr int kK6Stage = 4096;  // entries staged in shared memory (48 KB dynamic)
 
@@ -1033,8 +1048,15 @@ __device__ void merge_range(const K6Params& p, int v, int64_t e_lo, int64_t e_hi
     }
     __syncthreads();
   }
-  for (int64_t e = e_lo + threadIdx.x; e < hi; e += kK6Threads) {
-    if (e < n) {
+  // kSub6 lanes per output rank, each searching a strided subset of the other blocks
+  // (one lane per rank serialised all ~15 searches in one thread: ~17 us per CTA)
+  constexpr int kSub6 = 4;
+  const int sub = threadIdx.x & (kSub6 - 1);
+  for (int64_t e0 = e_lo; e0 < hi; e0 += kK6Threads / kSub6) {  // CTA-uniform trip count
+    const int64_t e = e0 + threadIdx.x / kSub6;
+    const bool live = e < hi && e < n;
+    int64_t i = 0, sl = 0, rank = 0, w = 0;
+    if (live) {
       int lo = 0, hb = p.nb;
       while (hb - lo > 1) {
         const int mid = (lo + hb) >> 1;
@@ -1042,13 +1064,12 @@ __device__ void merge_range(const K6Params& p, int v, int64_t e_lo, int64_t e_hi
         else hb = mid;
       }
       const int b = lo;
-      const int64_t i = e - pre[b];
-      const int64_t sl = (int64_t)b * p.budget + i;
-      int64_t rank = i;
+      i = e - pre[b];
+      sl = (int64_t)b * p.budget + i;
       if (staged) {  // (separate loops: a select between an smem and a global load issues both)
         const double m = sm_m[e];
-        const int64_t w = sm_w[e];
-        for (int b2 = 0; b2 < p.nb; ++b2) {
+        w = sm_w[e];
+        for (int b2 = sub; b2 < p.nb; b2 += kSub6) {
           if (b2 == b) continue;
           int l2 = 0, h2 = pre[b2 + 1] - pre[b2];  // first entry of b2 not ahead of (m, w)
           const int f2 = pre[b2];
@@ -1061,8 +1082,8 @@ __device__ void merge_range(const K6Params& p, int v, int64_t e_lo, int64_t e_hi
         }
       } else {
         const double m = __ldcg(bm + sl);
-        const int64_t w = __ldcg(bw + sl);
-        for (int b2 = 0; b2 < p.nb; ++b2) {
+        w = __ldcg(bw + sl);
+        for (int b2 = sub; b2 < p.nb; b2 += kSub6) {
           if (b2 == b) continue;
           int l2 = 0, h2 = pre[b2 + 1] - pre[b2];
           const int64_t o2 = (int64_t)b2 * p.budget;
@@ -1074,7 +1095,12 @@ __device__ void merge_range(const K6Params& p, int v, int64_t e_lo, int64_t e_hi
           rank += l2;
         }
       }
-      const int64_t w = staged ? sm_w[e] : __ldcg(bw + sl);
+    }
+    rank += __shfl_xor_sync(0xffffffffu, rank, 1);
+    rank += __shfl_xor_sync(0xffffffffu, rank, 2);
+    if (sub != 0 || e >= hi) continue;
+    if (e < n) {
+      rank += i;
       if (rank < p.s) {
         ow[rank] = w;
         oc[rank] = ldcg2(bc + sl);
@@ -1093,7 +1119,7 @@ __global__ void __launch_bounds__(kK6Threads) k6_merge(const __grid_constant__ K
   extern __shared__ unsigned char k6_smem[];
   __shared__ int32_t pre[kK6MaxBlocks + 1];
   double* sm_m = (double*)k6_smem;
-  merge_range(p, blockIdx.y, (int64_t)blockIdx.x * kK6Threads, (int64_t)(blockIdx.x + 1) * kK6Threads, sm_m,
+  merge_range(p, blockIdx.y, (int64_t)blockIdx.x * kK6Ranks, (int64_t)(blockIdx.x + 1) * kK6Ranks, sm_m,
               (int64_t*)(sm_m + kK6Stage), pre);
 }
 
@@ -1558,7 +1584,7 @@ cudaError_t launch_k6_blocks(const int64_t* bw, const double2* bc, const double*
   if (nblocks > kK6MaxBlocks) return cudaErrorInvalidValue;
   const K6Params k = k6_params(bw, bc, bm, bnz, nblocks, budget, blk_vec, bn_vec, s, freqs, coeffs);
   const int64_t cap = std::max<int64_t>((int64_t)nblocks * budget, s);
-  return launch_pdl(k6_merge, dim3(cdiv(cap, kK6Threads), nvec), dim3(kK6Threads), kK6Stage * 16, st, k);
+  return launch_pdl(k6_merge, dim3(cdiv(cap, kK6Ranks), nvec), dim3(kK6Threads), kK6Stage * 16, st, k);
 }
 
 cudaError_t launch_k6(const Plan& p, int nvec, void* ws, int64_t* freqs, double2* coeffs, cudaStream_t st) {
