@@ -836,6 +836,17 @@ __device__ __forceinline__ double ghat_dev(double c1, int64_t dq) {
   return exp(-(c1 * c1) * d * d / 2.0) / 2.5066282746310002;  // Lemma 2
 }
 
+#ifdef DSFT_K2_TRACE
+__device__ unsigned long long g_k5trace[64][8];
+#define K5T(i)                                                                      \
+  do {                                                                              \
+    if (threadIdx.x == 0 && blockIdx.x < 64) g_k5trace[blockIdx.x][(i)] = globaltimer_ns(); \
+  } while (0)
+#else
+#define K5T(i) \
+  do {         \
+  } while (0)
+#endif
 // one band of one vector per CTA (kK5Threads threads); sm_m / sm_w: kRankTile each
 __device__ void select_band(const K5bParams& p, int v, int j, double* sm_m, int64_t* sm_w, int* s_nzp) {
   const int tid = threadIdx.x;
@@ -851,15 +862,29 @@ __device__ void select_band(const K5bParams& p, int v, int j, double* sm_m, int6
   if (n <= kRankTile) {
     // staged: keys in shared memory, one global read per entry
     double* sm_m2 = sm_m + kRankTile;  // rank-2 keys (the buffer holds kK6Stage >= 2 kRankTile)
+    // every entry's z, unbiased c = z / ghat and merge key |c|^2 computed here, all
+    // entries in parallel (the exp and divisions inside the rank passes ran once per
+    // pass iteration on one lane per entry: ~3 us per pass, DSFT_K2_TRACE)
+    double2* sm_z = (double2*)(sm_w + kRankTile);
+    double2* sm_c = sm_z + kRankTile;
+    double* sm_mc = (double*)(sm_c + kRankTile);
 #pragma unroll
     for (int it = 0; it < kRankTile / kK5Threads; ++it) {  // fixed trip: loads in flight together
       const int i = tid + it * kK5Threads;
       if (i < n) {
-        sm_m[i] = cabs2_rn(ldcg2(accz + i));
-        sm_w[i] = __ldcg(accw + i);
+        const double2 z = ldcg2(accz + i);
+        const int64_t w = __ldcg(accw + i);
+        sm_z[i] = z;
+        sm_m[i] = cabs2_rn(z);
+        sm_w[i] = w;
+        const double gh = ghat_dev(p.c1, w - q);
+        const double2 c = make_double2(z.x / gh, z.y / gh);
+        sm_c[i] = c;
+        sm_mc[i] = (c.x == 0.0 && c.y == 0.0) ? -1.0 : cabs2_rn(c);
       }
     }
     __syncthreads();
+    K5T(2);
     // kSub lanes per entry, each counting a strided quarter of the list (a band holds
     // only ~70 entries: one lane per entry left most warps idle and each working warp
     // issuing ~5 k dependent instructions, ~10 us per CTA)
@@ -875,16 +900,10 @@ __device__ void select_band(const K5bParams& p, int v, int j, double* sm_m, int6
 #pragma unroll
       for (int o = 1; o < kSub; o <<= 1) rank += __shfl_xor_sync(0xffffffffu, rank, o);
       if (e >= n || sub != 0) continue;
-      double m2 = -2.0;  // not kept: never ranks ahead
-      if (rank < p.budget) {
-        const double2 z = ldcg2(accz + e);
-        const double gh = ghat_dev(p.c1, my_w - q);
-        const double2 c = make_double2(z.x / gh, z.y / gh);
-        m2 = (c.x == 0.0 && c.y == 0.0) ? -1.0 : cabs2_rn(c);
-      }
-      sm_m2[e] = m2;
+      sm_m2[e] = rank < p.budget ? sm_mc[e] : -2.0;  // not kept: never ranks ahead
     }
     __syncthreads();
+    K5T(3);
     for (int e0 = 0; e0 < n; e0 += kK5Threads / kSub) {  // rank 2 among kept -> output slot
       const int e = e0 + tid / kSub;
       const double my_m = e < n ? sm_m2[e] : -2.0;
@@ -895,16 +914,15 @@ __device__ void select_band(const K5bParams& p, int v, int j, double* sm_m, int6
 #pragma unroll
       for (int o = 1; o < kSub; o <<= 1) rank += __shfl_xor_sync(0xffffffffu, rank, o);
       if (my_m < -1.5 || sub != 0) continue;
-      const double2 z = ldcg2(accz + e);
-      const double gh = ghat_dev(p.c1, my_w - q);
       const int64_t o = (int64_t)v * p.band_vec + (int64_t)j * p.budget + rank;
       p.band_w[o] = my_w;
-      p.band_z[o] = z;
-      p.band_c[o] = make_double2(z.x / gh, z.y / gh);
+      p.band_z[o] = sm_z[e];
+      p.band_c[o] = sm_c[e];
       p.band_m[o] = my_m;
       if (my_m >= 0.0) atomicAdd(&s_nz, 1);
     }
     __syncthreads();
+    K5T(4);
     if (tid == 0) {
       p.band_n[(int64_t)v * p.bn_vec + j] = (int32_t)(n < p.budget ? n : p.budget);
       p.band_nz[(int64_t)v * p.bn_vec + j] = s_nz;
@@ -1187,17 +1205,6 @@ __global__ void __launch_bounds__(256) k5a_medians(const __grid_constant__ K5Par
   }
 }
 
-#ifdef DSFT_K2_TRACE
-__device__ unsigned long long g_k5trace[64][4];
-#define K5T(i)                                                                      \
-  do {                                                                              \
-    if (threadIdx.x == 0 && blockIdx.x < 64) g_k5trace[blockIdx.x][(i)] = globaltimer_ns(); \
-  } while (0)
-#else
-#define K5T(i) \
-  do {         \
-  } while (0)
-#endif
 
 __global__ void __launch_bounds__(kK5Threads) k5b_select(const __grid_constant__ K5Params p) {
   pdl_trigger();
@@ -1214,6 +1221,7 @@ __global__ void __launch_bounds__(kK5Threads) k5b_select(const __grid_constant__
   __syncthreads();
   if (tid == 0) s_last = atomicAdd(p.ticket + v, 1) == p.nb - 1;
   __syncthreads();
+  K5T(5);
   if (!s_last) return;
   for (int b = tid; b < p.nb; b += kK5Threads) p.acc_n[(int64_t)v * p.b.bn_vec + b] = 0;
   if (tid == 0) {
@@ -1267,7 +1275,7 @@ cudaError_t kernels_init() {
   const int maxsm = 227 * 1024 - 1024;  // leave room for the static reduction buffer
   if ((e = cudaFuncSetAttribute(k2_prime_dft<64, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm))) return e;
   if ((e = cudaFuncSetAttribute(k6_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, kK6Stage * 16))) return e;
-  if ((e = cudaFuncSetAttribute(k5b_select, cudaFuncAttributeMaxDynamicSharedMemorySize, kRankTile * 24))) return e;
+  if ((e = cudaFuncSetAttribute(k5b_select, cudaFuncAttributeMaxDynamicSharedMemorySize, kRankTile * 64))) return e;
 
   if ((e = cudaFuncSetAttribute(k2_prime_dft<256, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm))) return e;
   if ((e = cudaFuncSetAttribute(k2_prime_dft<512, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm))) return e;
@@ -1575,7 +1583,7 @@ cudaError_t launch_k45(const Plan& p, int nvec, void* ws, const int* bands, int 
   k5s_scan<<<dim3(cdiv((int64_t)nbands * p.sumP, 256), nvec), 256, 0, st>>>(f);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   if ((e = launch_pdl(k5a_medians, dim3(2 * 148, nvec), dim3(256), 0, st, f)) != cudaSuccess) return e;
-  if ((e = launch_pdl(k5b_select, dim3(nbands, nvec), dim3(kK5Threads), kRankTile * 2 * 8 + kRankTile * 8, st, f)) !=
+  if ((e = launch_pdl(k5b_select, dim3(nbands, nvec), dim3(kK5Threads), kRankTile * 64, st, f)) !=
       cudaSuccess)
     return e;
   if (!freqs) return cudaSuccess;  // sharded: merged after the allgather

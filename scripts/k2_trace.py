@@ -48,11 +48,12 @@ for t in range(info.T):
           "| start spread us", round((start.max() - start.min()) / 1e3, 1))
 
 
-t5 = np.zeros((64, 4), dtype=np.uint64)
+t5 = np.zeros((64, 8), dtype=np.uint64)
 if hasattr(L, "dsft_debug_k5_trace") and L.dsft_debug_k5_trace(t5.ctypes.data_as(C.c_void_p)) == 0:
     t5 = t5.astype(np.int64)[:info.J]
     t0 = t5[:, 0].min()
     for j in range(info.J):
         r = t5[j]
-        print(f"K5b band {j}: start {(r[0]-t0)/1e3:7.2f} select {(r[1]-r[0])/1e3:7.2f} us" +
-              "")
+        print(f"K5b band {j}: start {(r[0]-t0)/1e3:7.2f} select {(r[1]-r[0])/1e3:7.2f} us "
+              f"(stage {(r[2]-r[0])/1e3:6.2f}, rank1 {(r[3]-r[2])/1e3:6.2f}, rank2 {(r[4]-r[3])/1e3:6.2f}) "
+              f"ticket {(r[5]-r[1])/1e3:6.2f}")
