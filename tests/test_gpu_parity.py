@@ -3,6 +3,7 @@ seeded inputs.  Frequency sets bit-exact; coefficients within relative l2 1e-10
 (north_star); intermediate stages element by element."""
 
 import math
+import os
 
 import numpy as np
 import pytest
@@ -246,6 +247,8 @@ def test_host_path_modes_equal_device_path(mode, monkeypatch):
 def test_k2_specialised_equals_runtime_radix(monkeypatch):
     """The plan-time NVRTC specialisation of K2 and the runtime-radix kernel run the
     same passes in the same arithmetic order: outputs bitwise identical."""
+    if os.environ.get("DSFT_JIT") == "0":
+        pytest.skip("NVRTC specialisation disabled by DSFT_JIT=0 in the environment")
     N, s = 2**20, 300  # bucket primes in [1200, 2400): runtime-radix <256,2> rows -> specialised
     pl = planted(N, s, cfg=38, trial=0)
     plan = d.Plan(N, s)
