@@ -12,6 +12,10 @@ constexpr int64_t kK3Sentinel = (int64_t)(-9223372036854775807LL - 1);  // INT64
 
 // ============================================================== K3 identify
 __device__ __forceinline__ int64_t pmod(int64_t x, int64_t m) {
+  if (x == (int64_t)(int)x && m == (int64_t)(int)m) {  // 32-bit remainder (far fewer instructions)
+    const int r = (int)x % (int)m;
+    return r < 0 ? (int64_t)r + m : (int64_t)r;
+  }
   int64_t r = x % m;
   return r < 0 ? r + m : r;
 }
