@@ -66,3 +66,16 @@ def planted_with_tail(N: int, s: int, tail: int, tail_mag: float, cfg: int = 0,
     rng = rng_for(cfg, trial, 1)
     mags = mags[rng.permutation(s + tail)]
     return planted(N, s + tail, cfg=cfg, trial=trial, magnitudes=mags)
+
+
+def planted_at(N: int, freqs, coeffs) -> Planted:
+    """f_j = sum_omega c_omega exp(2 pi i omega j / N) for GIVEN frequencies on B and
+    coefficients c (test fixtures with tones placed on band edges etc.)."""
+    freqs = np.asarray(freqs, dtype=np.int64)
+    c = np.asarray(coeffs, dtype=np.complex128)
+    chat = np.zeros(N, dtype=np.complex128)
+    chat[freqs % N] = c
+    f = N * np.fft.ifft(chat)
+    sign = np.where(freqs % 2 == 0, 1.0, -1.0)
+    order = np.argsort(freqs)
+    return Planted(f=f, freqs=freqs[order], fhat=(sign * c)[order])

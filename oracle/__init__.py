@@ -20,11 +20,20 @@ Parity status per function (DESIGN.md §4 lists the pin for each):
   filt.ghat / filt.g       pinned (Lemma 2 vs quadrature of eq. (4))
   params.derive_plan       pinned (worked values, Lemma 3 exhaustive, coverage)
   numtheory.*              pinned (brute-force CRT / sieve / SplitMix64 vectors)
-  dsft.filtered_samples    pinned (closed form within Theorem 4 bound)
+  dsft.nearest_grid_index  pinned (brute-force argmin over exact rationals, Lemma 10)
+  dsft.filtered_samples    pinned (closed form within Theorem 4 bound; impulse-response
+                           support = the brute-force windows)
   dsft.alias_dft           pinned (brute-force DFT, aliasing identity)
-  dsft.identify / vote     pinned (brute-force CRT, planted isolated tones)
-  dsft.estimate / merge    pinned (planted exact inversion, brute-force sort)
-  dsft.dsft (end to end)   pinned (brute-force DFT on tiny N; Theorem 5 bound)
+  dsft.window_representative pinned (brute-force scan of q + B, both edges)
+  dsft.identify            pinned (brute-force CRT + window + passband)
+  dsft.vote                pinned (hand-built vote sets at v_min - 1 / v_min votes)
+  dsft.estimate            pinned (hand-built measurements with a closed-form median;
+                           non-identifying grids in the majority; line-9 budget cut)
+  dsft.merge               pinned (brute-force sort, zero drop)
+  dsft.dsft (end to end)   pinned (brute-force DFT on tiny N; Theorem 5 bound;
+                           passband-edge and B-extreme tones)
+  scripts/mutation_check.py applies 18 plausible mistakes to the oracle; every one
+  fails at least one `-m "not gpu"` test.
   inner-SFT design constants (c_b, T, v_min, pool rule, residue rule):
                            parity unpinned -- the paper prints no values for
                            them; only invariants pin them.

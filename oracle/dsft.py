@@ -29,6 +29,15 @@ from .params import OracleParams, Plan, derive_plan
 
 
 # --------------------------------------------------------------------------- O2
+def nearest_grid_index(k, N: int, L: int):
+    """j' = argmin_j |x_k - y_j| (Lemma 10) for the nodes
+    x_k = -pi + 2 pi k / L and the grid y_j = -pi + 2 pi j / N:
+    |x_k - y_j| = 2 pi |kN - jL| / (NL), minimised by j = round(kN / L), computed
+    exactly in integers as floor((2kN + L) / (2L)).  L odd: no ties (reading R3)."""
+    k = np.asarray(k, dtype=np.int64)
+    return (2 * k * N + L) // (2 * L)
+
+
 def filtered_samples(f: np.ndarray, plan: Plan, q: int, L: int) -> np.ndarray:
     """h_q(x_k) for the L nodes x_k = -pi + 2 pi k / L, k = 0..L-1.
 
@@ -43,7 +52,7 @@ def filtered_samples(f: np.ndarray, plan: Plan, q: int, L: int) -> np.ndarray:
     c1 = plan.c1
     NL = N * L
     k = np.arange(L, dtype=np.int64)
-    jp = (2 * k * N + L) // (2 * L)
+    jp = nearest_grid_index(k, N, L)
     acc = np.zeros(L, dtype=np.complex128)
     for u in range(-plan.kappa, plan.kappa + 1):
         j = jp + u
@@ -129,12 +138,23 @@ def identify(plan: Plan, j: int, t: int, Yt: list[np.ndarray]) -> Identification
     R = np.zeros(P, dtype=np.int64)
     for rr, em in zip(res, e):
         R = (R + rr * em) % M
-    lo = q - (N + 1) // 2 + 1
-    om = lo + (R - lo) % M
-    ok = om <= q + N // 2
+    om = window_representative(R, M, q, N)
+    ok = om != SENTINEL
     ok &= (om >= q - plan.w) & (om < q + plan.w) & (om >= plan.B_lo) & (om <= plan.B_hi)
     cand = np.where(ok, om, SENTINEL)
     return Identification(cand=cand, gap=gap)
+
+
+def window_representative(R, M: int, q: int, N: int):
+    """The unique integer omega' = R (mod M) in the window
+    q + B = (q - ceil(N/2), q + floor(N/2)] (B of PAPER.md:84 shifted to the band
+    centre; reading R7 / G4), or SENTINEL if the window holds none.  M >= N
+    (reading R8), so the window of N consecutive integers holds at most one."""
+    R = np.asarray(R, dtype=np.int64)
+    lo = q - (N + 1) // 2 + 1          # smallest element of q + B
+    hi = q + N // 2                    # largest element of q + B
+    om = lo + (R - lo) % M             # smallest integer >= lo congruent to R
+    return np.where(om <= hi, om, SENTINEL)
 
 
 # --------------------------------------------------------------------------- O5

@@ -1,0 +1,82 @@
+#!/usr/bin/env python3
+"""Mutation check of the oracle's pins ("What's weak" 1).
+
+Copies the repository to a scratch directory, applies one plausible mistake at a
+time to oracle/*.py, runs the CPU suite (`-m "not gpu"`) there and reports which
+mutants survive.  A surviving mutant means a part of the oracle no pin checks.
+
+    python scripts/mutation_check.py [-k NAME]
+"""
+
+from __future__ import annotations
+
+import argparse
+import os
+import shutil
+import subprocess
+import sys
+import tempfile
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+# (name, file, old, new) -- each `old` must occur exactly once
+MUTANTS = [
+    ("vote >= 1", "oracle/dsft.py", "len(voters(plan, ids, om)) >= plan.vote_min)",
+     "len(voters(plan, ids, om)) >= 1)"),
+    ("vote >= v_min + 1", "oracle/dsft.py", "len(voters(plan, ids, om)) >= plan.vote_min)",
+     "len(voters(plan, ids, om)) >= plan.vote_min + 1)"),
+    ("majority floor(T/2)", "oracle/params.py", "vote_min = T // 2 + 1 if", "vote_min = max(1, T // 2) if"),
+    ("no band-budget cut", "oracle/dsft.py", "keep = order[:plan.band_budget]", "keep = order"),
+    ("j' = floor(kN/L)", "oracle/dsft.py", "return (2 * k * N + L) // (2 * L)", "return (k * N) // L"),
+    ("j' = ceil(kN/L)", "oracle/dsft.py", "return (2 * k * N + L) // (2 * L)", "return (k * N + L - 1) // L"),
+    ("q+B right edge open", "oracle/dsft.py", "return np.where(om <= hi, om, SENTINEL)",
+     "return np.where(om < hi, om, SENTINEL)"),
+    ("q+B left edge shifted", "oracle/dsft.py", "lo = q - (N + 1) // 2 + 1          #",
+     "lo = q - (N + 1) // 2          #"),
+    ("estimate over all T", "oracle/dsft.py", "for t in voters(plan, ids, om):\n            for i, L",
+     "for t in range(plan.T):\n            for i, L"),
+    ("passband upper closed", "oracle/dsft.py", "(om < q + plan.w)", "(om <= q + plan.w)"),
+    ("passband lower open", "oracle/dsft.py", "(om >= q - plan.w)", "(om > q - plan.w)"),
+    ("B upper open", "oracle/dsft.py", "(om <= plan.B_hi)", "(om < plan.B_hi)"),
+    ("no (-1)^omega", "oracle/dsft.py", "sgn = -1.0 if om % 2 else 1.0", "sgn = 1.0"),
+    ("median -> mean", "oracle/dsft.py", "zs.append(complex(np.median(v.real), np.median(v.imag)))",
+     "zs.append(complex(np.mean(v.real), np.mean(v.imag)))"),
+    ("unbias ghat_{omega+q}", "oracle/dsft.py", "float(ghat(om - q, plan.c1))", "float(ghat(om + q, plan.c1))"),
+    ("modulation sign", "oracle/dsft.py", "phase = np.exp(2j * math.pi * rho / NL)",
+     "phase = np.exp(-2j * math.pi * rho / NL)"),
+    ("merge keeps zeros", "oracle/dsft.py", "if not (c.real == 0.0 and c.imag == 0.0)]", "]"),
+    ("window kappa - 1", "oracle/dsft.py", "for u in range(-plan.kappa, plan.kappa + 1):",
+     "for u in range(-plan.kappa + 1, plan.kappa):"),
+]
+
+
+def main() -> int:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("-k", default=None, help="only mutants whose name contains this")
+    a = ap.parse_args()
+    survivors = []
+    with tempfile.TemporaryDirectory() as tmp:
+        dst = os.path.join(tmp, "repo")
+        shutil.copytree(ROOT, dst, ignore=shutil.ignore_patterns(".git", "gpurun_out", "profiles", "*.so", "build*"))
+        for name, rel, old, new in MUTANTS:
+            if a.k and a.k not in name:
+                continue
+            path = os.path.join(dst, rel)
+            orig = open(os.path.join(ROOT, rel)).read()
+            assert orig.count(old) == 1, (name, orig.count(old))
+            open(path, "w").write(orig.replace(old, new))
+            r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "not gpu", "tests",
+                                "--ignore=tests/test_abi.py", "--ignore=tests/test_dist_gloo.py"],
+                               cwd=dst, capture_output=True, text=True)
+            killed = r.returncode != 0
+            tail = [ln for ln in r.stdout.splitlines() if ln.startswith("FAILED")][:1]
+            print(f"{'killed ' if killed else 'SURVIVED'}  {name:24s} {tail[0] if tail else ''}", flush=True)
+            if not killed:
+                survivors.append(name)
+            open(path, "w").write(orig)
+    print(f"{len(survivors)} surviving mutant(s): {survivors}")
+    return 1 if survivors else 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

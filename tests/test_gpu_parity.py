@@ -16,7 +16,7 @@ if not torch.cuda.is_available():  # pragma: no cover - CPU container
     pytest.skip("needs a CUDA device", allow_module_level=True)
 
 import paper_1706_02740_b200 as d  # noqa: E402
-from dsft_synth import planted  # noqa: E402
+from dsft_synth import planted, planted_at  # noqa: E402
 from oracle.dsft import SENTINEL, alias_dft, band_measurements, dsft, filtered_samples, identify  # noqa: E402
 from oracle.params import OracleParams, derive_plan  # noqa: E402
 
@@ -339,3 +339,22 @@ def test_split_mode_fallback(N, s, cfg, trial, monkeypatch):
     plan = d.Plan(N, s, d.make_params(seed=trial))
     assert plan.launches_per_execute() > 4 + 3 * plan.info.T  # K2a + K2b launches
     assert_parity(run_gpu(plan, pl.f), ref, s)
+
+
+def test_band_budget_and_edge_tones_parity():
+    """The oracle pins of tests/test_oracle_pins.py on the GPU path: a band budget of 1
+    with two tones in one passband (line 9), tones on the passband edges q_j - w and
+    q_j + w and at both extremes of B (line 10)."""
+    for N in (4096, 4095):
+        op = derive_plan(N, 8, OracleParams(seed=3))
+        w, q = op.w, op.q
+        freqs = sorted({q[2] - w, q[2] + w, q[5] + w - 1, op.B_lo, op.B_hi, q[9], q[9] + 30})
+        pl = planted_at(N, freqs, np.exp(1j * np.arange(len(freqs))) * np.linspace(1, 2, len(freqs)))
+        for kw in ({}, {"band_budget": 1}):
+            ref = dsft(pl.f, 8, OracleParams(seed=3, **kw))
+            plan = d.Plan(N, 8, d.make_params(seed=3, **kw))
+            assert_parity(run_gpu(plan, pl.f), ref, 8)
+            if not kw:
+                assert sorted(ref.freqs.tolist()) == freqs
+            else:
+                assert q[9] not in ref.freqs.tolist() and q[9] + 30 in ref.freqs.tolist()

@@ -200,31 +200,6 @@ def test_theorem5_bound_with_tails():
         assert lhs <= rhs
 
 
-def test_estimate_median_and_unbias():
-    """O6: z is the separate Re/Im median (even count -> mean of the middle two)
-    of (-1)^omega E[omega mod L] over the voting primes; c = z / ghat_{omega-q}."""
-    N = 4096
-    plan = derive_plan(N, 8, OracleParams(seed=6))
-    pl = planted(N, 6, cfg=19, trial=0)
-    om0 = int(pl.freqs[0])
-    j = [jj for jj in range(plan.J) if plan.q[jj] - plan.w <= om0 < plan.q[jj] + plan.w][0]
-    br = process_band(pl.f, plan, j)
-    assert om0 in br.omegas
-    from oracle.dsft import band_measurements, voters
-    Y = band_measurements(pl.f, plan, j)
-    for om, c in zip(br.omegas, br.coeffs):
-        vals = []
-        for t in voters(plan, br.ids, om):
-            for i, L in enumerate(plan.grid_lengths(t)):
-                vals.append((-1) ** (om % 2) * Y[t][i][om % L])
-        re = sorted(v.real for v in vals)
-        im = sorted(v.imag for v in vals)
-        n = len(vals)
-        med = (lambda a: a[n // 2] if n % 2 else 0.5 * (a[n // 2 - 1] + a[n // 2]))
-        z = complex(med(re), med(im))
-        assert abs(c - z / (math.exp(-plan.c1 ** 2 * (om - plan.q[j]) ** 2 / 2) / math.sqrt(2 * math.pi))) < 1e-15
-
-
 def test_merge_bruteforce():
     plan = derive_plan(4096, 6, OracleParams())
     rng = np.random.default_rng(3)
