@@ -61,6 +61,30 @@ typedef enum {
 
 enum { DSFT_PRESET_DMSFT6 = 0, DSFT_PRESET_DMSFT4 = 1, DSFT_PRESET_THM4 = 2 };
 enum { DSFT_ALPHA_CORRECTED = 0, DSFT_ALPHA_LITERAL = 1 };
+/* Bucket-prime pool (reading R6): FULL = every prime in [ceil(c_b s), 2 ceil(c_b s))
+ * (the Monte Carlo variant reads a random subset of the
+ * deterministic measurements); SMOOTH = only the primes P whose P - 1 has no prime
+ * factor above 13 (every length-P DFT is then a Rader convolution over a 13-smooth
+ * FFT; the general primes of FULL use a Bluestein chirp-z convolution). */
+enum { DSFT_POOL_FULL = 0, DSFT_POOL_SMOOTH = 1 };
+/* dsft_params.flags (execution options; results are bitwise identical either way):
+ *  NO_JIT       no plan-time NVRTC specialisation (runtime-parameter K2/K3 kernels)
+ *  NO_CLUSTER   rows above one CTA's shared memory use the two-launch split K2
+ *               instead of the thread-block-cluster kernel
+ *  HOST_COPY    dsft_execute_host always copies f to the device (no zero copy)
+ *  HOST_MAPPED  dsft_execute_host reads any mapped f_host in place (zero copy even
+ *               for dense sampling)
+ *  SERIAL       every launch on the caller's stream (no pipeline streams; debugging,
+ *               compute-sanitizer)
+ *  NO_GRAPH     no CUDA-graph replay of the execute sequence */
+enum {
+  DSFT_FLAG_NO_JIT = 1u,
+  DSFT_FLAG_NO_CLUSTER = 2u,
+  DSFT_FLAG_HOST_COPY = 4u,
+  DSFT_FLAG_HOST_MAPPED = 8u,
+  DSFT_FLAG_SERIAL = 16u,
+  DSFT_FLAG_NO_GRAPH = 32u
+};
 
 /* Parameters of Algorithm 1 and of the inner SFT.
  *  preset        DMSFT6 (kappa = 6), DMSFT4 (kappa = 4)  -- PAPER.md:653;
@@ -74,7 +98,9 @@ enum { DSFT_ALPHA_CORRECTED = 0, DSFT_ALPHA_LITERAL = 1 };
  *                R13): every prime of the pool, no draw
  *  vote_min      v_min in [1, T]; 0 = "more than half": floor(T/2) + 1
  *  band_budget   entries kept per band after line 9 (0 = s; reading R11)
- *  seed          SplitMix64 seed of the bucket-prime draw (reading R7)   */
+ *  seed          SplitMix64 seed of the bucket-prime draw (reading R7)
+ *  pool_rule     DSFT_POOL_FULL or DSFT_POOL_SMOOTH (reading R6)
+ *  flags         DSFT_FLAG_* execution options (above)                     */
 typedef struct {
   int32_t preset;
   double r;
@@ -86,6 +112,8 @@ typedef struct {
   int32_t vote_min;
   int64_t band_budget;
   uint64_t seed;
+  int32_t pool_rule;
+  uint32_t flags;
 } dsft_params;
 
 /* Derived plan quantities, for oracle cross-checks (read-only copy). */
@@ -150,8 +178,8 @@ dsft_status dsft_execute_batched(dsft_plan* plan, const dsft_c128* f_dev, int64_
  * (zero copy: only the sampled bytes cross the host link -- the sublinear
  * sampling of Algorithm 1).  Otherwise (pageable memory, or
  * dense sampling) f is copied to a device buffer first.  Results are identical
- * either way.  DSFT_HOST_ZERO_COPY=0 in the environment forces the copy, =1
- * reads any mapped f_host in place.  The outputs are copied back. */
+ * either way.  dsft_params.flags DSFT_FLAG_HOST_COPY forces the copy,
+ * DSFT_FLAG_HOST_MAPPED reads any mapped f_host in place.  The outputs are copied back. */
 dsft_status dsft_execute_host(dsft_plan* plan, const dsft_c128* f_host, int64_t* freqs_out_host,
                               dsft_c128* coeffs_out_host, void* stream);
 
@@ -166,7 +194,7 @@ int32_t dsft_plan_host_zero_copy(const dsft_plan* plan, const dsft_c128* f_host,
  * (loaded with dlopen), the length-P_t DFT kernel of each bucket prime with its
  * radix tuple, spans and trip counts as compile-time constants, for sm_100a;
  * compiled cubins are cached in-process and in $DSFT_JIT_CACHE (default
- * ~/.cache/dsft_jit).  Setting DSFT_JIT=0 in the environment disables it.  Any
+ * ~/.cache/dsft_jit).  dsft_params.flags DSFT_FLAG_NO_JIT disables it.  Any
  * failure keeps that bucket on the runtime-radix kernel (same arithmetic,
  * bitwise-identical results).  Returns the number of bucket primes running the
  * specialised kernel; if why != NULL, copies (NUL-terminated, truncated to
@@ -191,22 +219,59 @@ dsft_status dsft_plan_collect_times(dsft_plan* plan, double* ms_out, int64_t* la
  * recorded (may exceed n), or -1 on error.  Clears the record like collect. */
 int64_t dsft_plan_collect_timeline(dsft_plan* plan, double* rows_out, int64_t n);
 
-/* ---- multi-GPU (NCCL loaded with dlopen; one process per GPU) ----------
- * dsft_comm_get_unique_id writes NCCL's 128-byte unique id on rank 0; the
- * caller broadcasts it (e.g. torch.distributed) and every rank calls
- * dsft_comm_create.  dsft_execute_sharded: f_dev replicated on every rank;
- * rank rho computes the bands j = rho (mod world), then one ncclAllGather of
- * the fixed-capacity per-band result blocks and the merge run on every rank,
- * so all ranks end with the identical result.  dsft_execute_batched_sharded:
- * each rank passes its own slice of vectors (no exchange needed; outputs are
- * per-rank). */
+/* ---- multi-GPU (NCCL loaded with dlopen; one process per GPU) --
+ * The method partitions naturally: the passbands of Algorithm 1's
+ * line-3 loop are independent until line 13's merge, and so are
+ * separate input vectors.
+ *
+ * dsft_comm_get_unique_id writes NCCL's 128-byte unique id on rank 0; the caller
+ * broadcasts it (e.g. torch.distributed) and every rank calls dsft_comm_create
+ * (collective, blocking).  The current CUDA device must be the rank's GPU.  Errors:
+ * DSFT_ERR_NCCL with NCCL's message in dsft_last_error(). */
 dsft_status dsft_comm_get_unique_id(void* out128);
-/* Host-only: the bands j = rank (mod world) a rank computes (bands_out[J]). */
-void dsft_shard_bands(int32_t J, int32_t rank, int32_t world, int32_t* bands_out, int32_t* nbands_out);
 dsft_status dsft_comm_create(int32_t rank, int32_t world, const void* unique_id128, dsft_comm** out);
 void dsft_comm_destroy(dsft_comm* comm);
+/* Bounded wait for `stream` after a sharded execute: polls the stream and NCCL's
+ * asynchronous error every 50 us; on an asynchronous error, or when timeout_ms
+ * (< 0: no limit) passes, the communicator is aborted (pending collectives are
+ * cancelled; destroy it afterwards) and DSFT_ERR_NCCL is returned.  DSFT_OK once
+ * the stream is idle. */
+dsft_status dsft_comm_wait(dsft_comm* comm, void* stream, int64_t timeout_ms);
+/* Host-only: the bands j = rank (mod world) a rank computes (bands_out[J]). */
+void dsft_shard_bands(int32_t J, int32_t rank, int32_t world, int32_t* bands_out, int32_t* nbands_out);
+
+/* Band-sharded single transform.  f_dev: the same vector on every rank.  Rank rho
+ * runs K1..K5 for its bands (line 4's j = rho mod world), one grouped ncclAllGather
+ * moves the fixed-capacity per-band result blocks, and every rank runs the line-13
+ * merge: on return (stream-ordered) every rank holds the identical result, bitwise
+ * equal to dsft_execute's.  Outputs as dsft_execute. */
 dsft_status dsft_execute_sharded(dsft_plan* plan, dsft_comm* comm, const dsft_c128* f_dev,
                                  int64_t* freqs_out_dev, dsft_c128* coeffs_out_dev, void* stream);
+/* The two halves of dsft_execute_sharded, for drivers that move the blocks
+ * themselves (and for single-process tests of the protocol: "virtual ranks").
+ * One rank's block = nbmax = ceil(J / world) band slots of band_budget entries:
+ *   w_out  int64     [nbmax][band_budget]  omegas of each band, sorted by the merge key
+ *   c_out  dsft_c128 [nbmax][band_budget]  unbiased coefficients
+ *   m_out  double    [nbmax][band_budget]  merge key |c|^2 (-1 for exact zeros)
+ *   nz_out int32     [nbmax]               entries with a non-zero key per band
+ * dsft_shard_block_entries returns nbmax * band_budget (0 for bad arguments).
+ * dsft_merge_sharded merges world such blocks laid out [world][...] (rank-major,
+ * exactly what ncclAllGather of each array produces) into freqs/coeffs_out_dev[s]. */
+int64_t dsft_shard_block_entries(const dsft_plan* plan, int32_t world);
+dsft_status dsft_execute_sharded_local(dsft_plan* plan, int32_t rank, int32_t world, const dsft_c128* f_dev,
+                                       int64_t* w_out, dsft_c128* c_out, double* m_out, int32_t* nz_out,
+                                       void* stream);
+dsft_status dsft_merge_sharded(dsft_plan* plan, int32_t world, const int64_t* w_all, const dsft_c128* c_all,
+                               const double* m_all, const int32_t* nz_all, int64_t* freqs_out_dev,
+                               dsft_c128* coeffs_out_dev, void* stream);
+/* Batched and sharded (BASELINE config 4 across ranks): each rank passes ITS OWN
+ * `batch` vectors f_dev + b*ld (the same batch on every rank).  Rank rho writes its
+ * results to rows [rho*batch, (rho+1)*batch) of freqs_out_dev / coeffs_out_dev
+ * ([world*batch][s], allocated on every rank), then one grouped in-place
+ * ncclAllGather leaves all world*batch results on every rank. */
+dsft_status dsft_execute_batched_sharded(dsft_plan* plan, dsft_comm* comm, const dsft_c128* f_dev, int64_t batch,
+                                         int64_t ld, int64_t* freqs_out_dev, dsft_c128* coeffs_out_dev,
+                                         void* stream);
 
 /* ---- parity hooks (tests only; same kernels as execute) ----------------
  * dsft_debug_grid: run K1 (what = 0: filtered samples h_q(x_k), k < L) or

@@ -270,7 +270,8 @@ def dsft(f: np.ndarray, s: int, params: OracleParams | None = None, plan: Plan |
     """Algorithm 1: returns the s-sparse approximation of
     fhat = F f (PAPER.md:82 convention) as (freqs, coeffs), sorted by
     (|c| desc, omega asc)."""
-    f = np.ascontiguousarray(f, dtype=np.complex128)
+    if isinstance(f, np.ndarray):  # (tests may pass an object that evaluates f lazily by index)
+        f = np.ascontiguousarray(f, dtype=np.complex128)
     if plan is None:
         plan = derive_plan(f.shape[0], s, params)
     all_om, all_c, bands = [], [], []

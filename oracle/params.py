@@ -47,6 +47,7 @@ class OracleParams:
     vote_min: int = 3              # v_min (reading R9: > T/2); 0 = floor(T/2) + 1
     band_budget: int = 0           # 0 = s (reading R11)
     seed: int = 0
+    pool_rule: str = "smooth"      # reading R6: "full" = every prime of the range, "smooth" = 13-smooth P-1
 
 
 @dataclass
@@ -84,12 +85,17 @@ def odd_primes(count_hint: int = 64) -> list[int]:
     return [p for p in primes_below(512) if p > 2][:count_hint]
 
 
-def bucket_pool(s: int, bucket_factor: float) -> list[int]:
-    """Reading R6: primes P in [ceil(c_b s), 2 ceil(c_b s)) whose P-1 has no
-    prime factor above 13.  PAPER.md:175-177 / 845-850 fix only that the
-    moduli are primes and that the randomized variant reads a random subset."""
+def bucket_pool(s: int, bucket_factor: float, rule: str = "smooth") -> list[int]:
+    """Reading R6: the primes P in [ceil(c_b s), 2 ceil(c_b s)) ("full"), or only those
+    whose P-1 has no prime factor above 13 ("smooth").  PAPER.md:175-177 / 845-850 fix
+    only that the moduli are primes and that the randomized variant reads a random
+    subset of the deterministic measurements."""
     lo = int(math.ceil(bucket_factor * s))
     hi = 2 * lo
+    if rule == "full":
+        return [p for p in primes_below(hi) if p >= lo]
+    if rule != "smooth":
+        raise ConfigError(f"unknown pool_rule {rule!r}")
     return [p for p in primes_below(hi) if p >= lo and largest_prime_factor(p - 1) <= RADER_SMOOTH]
 
 
@@ -178,7 +184,7 @@ def derive_plan(N: int, s: int, params: OracleParams | None = None) -> Plan:
     B_hi = N // 2
 
     # Inner SFT (reading R6-R8): bucket primes and residue primes.
-    pool = bucket_pool(s, p.bucket_factor)
+    pool = bucket_pool(s, p.bucket_factor, p.pool_rule)
     if int(p.n_bucket_primes) == 0:
         # Reading R13, the deterministic variant (the
         # measurements "always succeed"; the randomized variant reads a random subset

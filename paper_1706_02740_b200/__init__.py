@@ -24,6 +24,8 @@ DSFT_OK, DSFT_ERR_CONFIG, DSFT_ERR_ARG, DSFT_ERR_CUDA = 0, 2, 3, 4
 DSFT_ERR_NCCL, DSFT_ERR_NOMEM, DSFT_ERR_INTERNAL, DSFT_ERR_UNSUPPORTED = 5, 6, 7, 8
 PRESETS = {"dmsft6": 0, "dmsft4": 1, "thm4": 2}
 ALPHA_RULES = {"corrected": 0, "literal": 1}
+POOL_RULES = {"full": 0, "smooth": 1}
+FLAG_NO_JIT, FLAG_NO_CLUSTER, FLAG_HOST_COPY, FLAG_HOST_MAPPED, FLAG_SERIAL, FLAG_NO_GRAPH = 1, 2, 4, 8, 16, 32
 SENTINEL = -(1 << 63)
 
 
@@ -36,7 +38,8 @@ class DsftError(RuntimeError):
 class dsft_params(C.Structure):
     _fields_ = [("preset", C.c_int32), ("r", C.c_double), ("kappa", C.c_int32), ("tau", C.c_double),
                 ("alpha_rule", C.c_int32), ("bucket_factor", C.c_double), ("n_bucket_primes", C.c_int32),
-                ("vote_min", C.c_int32), ("band_budget", C.c_int64), ("seed", C.c_uint64)]
+                ("vote_min", C.c_int32), ("band_budget", C.c_int64), ("seed", C.c_uint64),
+                ("pool_rule", C.c_int32), ("flags", C.c_uint32)]
 
 
 class dsft_plan_info(C.Structure):
@@ -74,7 +77,12 @@ _SIGS = {
     "dsft_shard_bands": (None, [C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
     "dsft_comm_create": (C.c_int, [C.c_int32, C.c_int32, _P, C.POINTER(_P)]),
     "dsft_comm_destroy": (None, [_P]),
+    "dsft_comm_wait": (C.c_int, [_P, _P, C.c_int64]),
     "dsft_execute_sharded": (C.c_int, [_P, _P, _P, _P, _P, _P]),
+    "dsft_shard_block_entries": (C.c_int64, [_P, C.c_int32]),
+    "dsft_execute_sharded_local": (C.c_int, [_P, C.c_int32, C.c_int32, _P, _P, _P, _P, _P, _P]),
+    "dsft_merge_sharded": (C.c_int, [_P, C.c_int32, _P, _P, _P, _P, _P, _P, _P]),
+    "dsft_execute_batched_sharded": (C.c_int, [_P, _P, _P, C.c_int64, C.c_int64, _P, _P, _P]),
     "dsft_debug_grid": (C.c_int, [_P, _P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _P, _P]),
     "dsft_debug_copy": (C.c_int, [_P, C.c_int32, _P, C.c_size_t, _P]),
     "dsft_debug_jit_compile": (C.c_int, [C.c_int32, C.c_int32, C.POINTER(C.c_int32), C.c_int32, C.c_int32,
@@ -118,7 +126,9 @@ def _check(st: int) -> None:
 
 def make_params(preset: str = "dmsft6", r: float = 1.0, kappa: int = 0, tau: float = 1.0 / 3.0,
                 alpha_rule: str = "corrected", bucket_factor: float = 4.0, n_bucket_primes: int = 5,
-                vote_min: int = 3, band_budget: int = 0, seed: int = 0) -> dsft_params:
+                vote_min: int = 3, band_budget: int = 0, seed: int = 0, pool_rule: str | None = None,
+                flags: int = 0) -> dsft_params:
+    """dsft_params from keyword values (pool_rule None = the library default)."""
     p = dsft_params()
     lib().dsft_params_default(C.byref(p))
     p.preset = PRESETS[preset]
@@ -126,7 +136,40 @@ def make_params(preset: str = "dmsft6", r: float = 1.0, kappa: int = 0, tau: flo
     p.alpha_rule = ALPHA_RULES[alpha_rule]
     p.bucket_factor, p.n_bucket_primes, p.vote_min = bucket_factor, n_bucket_primes, vote_min
     p.band_budget, p.seed = band_budget, seed
+    if pool_rule is not None:
+        p.pool_rule = POOL_RULES[pool_rule]
+    p.flags = flags
     return p
+
+
+def default_pool_rule() -> str:
+    p = dsft_params()
+    lib().dsft_params_default(C.byref(p))
+    return {v: k for k, v in POOL_RULES.items()}[p.pool_rule]
+
+
+def _dev(t, dtype: str, numel: int, what: str, device=None):
+    """Argument check before a device pointer crosses the ABI: a torch tensor of the
+    right dtype, contiguous, on a CUDA device (or on `device`), with >= numel elements."""
+    if str(t.dtype) != "torch." + dtype:
+        raise DsftError(DSFT_ERR_ARG, f"{what}: dtype {t.dtype}, need torch.{dtype}")
+    if not t.is_contiguous():
+        raise DsftError(DSFT_ERR_ARG, f"{what}: tensor is not contiguous")
+    if t.device.type != "cuda" or (device is not None and t.device != device):
+        raise DsftError(DSFT_ERR_ARG, f"{what}: tensor on {t.device}, need {device or 'a CUDA device'}")
+    if t.numel() < numel:
+        raise DsftError(DSFT_ERR_ARG, f"{what}: {t.numel()} elements, need >= {numel}")
+    return t.data_ptr()
+
+
+def _host(t, dtype: str, numel: int, what: str):
+    if str(t.dtype) != "torch." + dtype:
+        raise DsftError(DSFT_ERR_ARG, f"{what}: dtype {t.dtype}, need torch.{dtype}")
+    if not t.is_contiguous() or t.device.type != "cpu":
+        raise DsftError(DSFT_ERR_ARG, f"{what}: need a contiguous CPU tensor")
+    if t.numel() < numel:
+        raise DsftError(DSFT_ERR_ARG, f"{what}: {t.numel()} elements, need >= {numel}")
+    return t.data_ptr()
 
 
 def dsft_plan_derive_info(N: int, s: int, params: dsft_params | None = None) -> dsft_plan_info:
@@ -218,17 +261,24 @@ class Plan:
             raise DsftError(-1, "dsft_plan_collect_timeline failed")
         return [(self.KERNEL_CLASSES[int(rows[3 * i])], rows[3 * i + 1], rows[3 * i + 2]) for i in range(min(rec, n))]
 
+    def _io(self, f, freqs_out, coeffs_out, nf: int, nout: int):
+        dv = f.device
+        return (_dev(f, "complex128", nf, "f"), _dev(freqs_out, "int64", nout, "freqs_out", dv),
+                _dev(coeffs_out, "complex128", nout, "coeffs_out", dv))
+
     def dsft_execute(self, f, freqs_out, coeffs_out, stream=None):
-        _check(lib().dsft_execute(self._h, f.data_ptr(), freqs_out.data_ptr(), coeffs_out.data_ptr(),
-                                  _stream_ptr(stream)))
+        pf, pw, pc = self._io(f, freqs_out, coeffs_out, self.N, self.s)
+        _check(lib().dsft_execute(self._h, pf, pw, pc, _stream_ptr(stream)))
 
     def dsft_execute_batched(self, f, batch: int, ld: int, freqs_out, coeffs_out, stream=None):
-        _check(lib().dsft_execute_batched(self._h, f.data_ptr(), batch, ld, freqs_out.data_ptr(),
-                                          coeffs_out.data_ptr(), _stream_ptr(stream)))
+        pf, pw, pc = self._io(f, freqs_out, coeffs_out, (batch - 1) * ld + self.N, batch * self.s)
+        _check(lib().dsft_execute_batched(self._h, pf, batch, ld, pw, pc, _stream_ptr(stream)))
 
     def dsft_execute_host(self, f_host, freqs_host, coeffs_host, stream=None):
-        _check(lib().dsft_execute_host(self._h, f_host.data_ptr(), freqs_host.data_ptr(),
-                                       coeffs_host.data_ptr(), _stream_ptr(stream)))
+        _check(lib().dsft_execute_host(self._h, _host(f_host, "complex128", self.N, "f_host"),
+                                       _host(freqs_host, "int64", self.s, "freqs_host"),
+                                       _host(coeffs_host, "complex128", self.s, "coeffs_host"),
+                                       _stream_ptr(stream)))
 
     def dsft_plan_k2_stages(self, t: int):
         """(radices, twf, ndim) of bucket prime t's K2 stage layout (include/dsft.h)."""
@@ -236,7 +286,7 @@ class Plan:
         twf, nd = C.c_uint32(0), C.c_int32(0)
         n = lib().dsft_plan_k2_stages(self._h, t, rad, C.byref(twf), C.byref(nd))
         if n < 0:
-            raise DsftError("dsft_plan_k2_stages: bad argument")
+            raise DsftError(DSFT_ERR_ARG, "dsft_plan_k2_stages: bad argument")
         return list(rad[:n]), int(twf.value), int(nd.value)
 
     def dsft_plan_host_zero_copy(self, f_host):
@@ -245,12 +295,41 @@ class Plan:
         nb = C.c_int64(0)
         r = lib().dsft_plan_host_zero_copy(self._h, f_host.data_ptr(), C.byref(nb))
         if r < 0:
-            raise DsftError("dsft_plan_host_zero_copy: NULL argument")
+            raise DsftError(DSFT_ERR_ARG, "dsft_plan_host_zero_copy: NULL argument")
         return bool(r), int(nb.value)
 
     def dsft_execute_sharded(self, comm, f, freqs_out, coeffs_out, stream=None):
-        _check(lib().dsft_execute_sharded(self._h, comm.handle, f.data_ptr(), freqs_out.data_ptr(),
-                                          coeffs_out.data_ptr(), _stream_ptr(stream)))
+        pf, pw, pc = self._io(f, freqs_out, coeffs_out, self.N, self.s)
+        _check(lib().dsft_execute_sharded(self._h, comm.handle, pf, pw, pc, _stream_ptr(stream)))
+
+    def dsft_execute_batched_sharded(self, comm, f, batch: int, ld: int, freqs_out, coeffs_out, stream=None):
+        """Each rank passes its own `batch` vectors; outputs [world*batch][s] on every rank."""
+        pf, pw, pc = self._io(f, freqs_out, coeffs_out, (batch - 1) * ld + self.N, comm.world * batch * self.s)
+        _check(lib().dsft_execute_batched_sharded(self._h, comm.handle, pf, batch, ld, pw, pc, _stream_ptr(stream)))
+
+    def dsft_shard_block_entries(self, world: int) -> int:
+        return int(lib().dsft_shard_block_entries(self._h, world))
+
+    def dsft_execute_sharded_local(self, rank: int, world: int, f, w_out, c_out, m_out, nz_out, stream=None):
+        """One rank's half of dsft_execute_sharded: its band blocks into caller buffers."""
+        n = self.dsft_shard_block_entries(world)
+        nb = n // self.info.band_budget
+        dv = f.device
+        _check(lib().dsft_execute_sharded_local(
+            self._h, rank, world, _dev(f, "complex128", self.N, "f"), _dev(w_out, "int64", n, "w_out", dv),
+            _dev(c_out, "complex128", n, "c_out", dv), _dev(m_out, "float64", n, "m_out", dv),
+            _dev(nz_out, "int32", nb, "nz_out", dv), _stream_ptr(stream)))
+
+    def dsft_merge_sharded(self, world: int, w_all, c_all, m_all, nz_all, freqs_out, coeffs_out, stream=None):
+        """The merge half: world gathered blocks ([world][...], rank-major) -> top-s."""
+        n = world * self.dsft_shard_block_entries(world)
+        nb = n // self.info.band_budget
+        dv = w_all.device
+        _check(lib().dsft_merge_sharded(
+            self._h, world, _dev(w_all, "int64", n, "w_all", dv), _dev(c_all, "complex128", n, "c_all", dv),
+            _dev(m_all, "float64", n, "m_all", dv), _dev(nz_all, "int32", nb, "nz_all", dv),
+            _dev(freqs_out, "int64", self.s, "freqs_out", dv), _dev(coeffs_out, "complex128", self.s, "coeffs_out", dv),
+            _stream_ptr(stream)))
 
     def dsft_debug_grid(self, f, band: int, t: int, i: int, what: int, out, stream=None):
         _check(lib().dsft_debug_grid(self._h, f.data_ptr(), band, t, i, what, out.data_ptr(), _stream_ptr(stream)))
@@ -277,6 +356,12 @@ class Comm:
         buf = C.create_string_buffer(bytes(unique_id), 128)
         _check(lib().dsft_comm_create(rank, world, C.cast(buf, _P), C.byref(h)))
         self._h = h
+        self.rank, self.world = rank, world
+
+    def wait(self, stream=None, timeout_ms: int = 120_000):
+        """Bounded wait for the stream carrying this communicator's collectives
+        (aborts the communicator on an NCCL error or timeout; include/dsft.h)."""
+        _check(lib().dsft_comm_wait(self._h, _stream_ptr(stream), timeout_ms))
 
     @staticmethod
     def unique_id() -> bytes:

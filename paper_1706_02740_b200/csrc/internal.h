@@ -31,6 +31,7 @@ namespace dsft {
 
 constexpr int kMaxShifts = 160;  // 1 + sum_i (r_i - 1) for up to 10 residue primes
 constexpr int kK1TabMax = 32 * 6 * 2;  // J <= 32 with kappa <= 6 in kernel params
+constexpr int kK1MaxKappa = 256;       // generic K1: [kappa][32] cos/sin table in shared memory (128 KB)
 constexpr int64_t kSentinel = INT64_MIN;
 constexpr int64_t kMaxWave = 4096;  // vectors processed concurrently by one batched wave
 #ifndef DSFT_ZBUFS
@@ -38,6 +39,7 @@ constexpr int64_t kMaxWave = 4096;  // vectors processed concurrently by one bat
 #endif
 constexpr int kZBufs = DSFT_ZBUFS;        // Z buffers the bucket-prime pipeline rotates through (3: measured worse, L2)
 constexpr int kMaxRadix = 16;    // largest in-register FFT stage radix in K2
+constexpr double kK1OneLaunchBytes = 24.0e6;  // all primes' Z below this: one K1 launch (plan.cpp choose_order)
 
 // Per-bucket-prime tables (host copy + device pointers into plan->dev_tables).
 struct Bucket {
@@ -92,6 +94,18 @@ struct Bucket {
                                 // split mode: stage 0 holds exp(-2 pi i e / M) for all e < M
 };
 
+// what a captured execute graph depends on besides the plan (plan.cpp execute_impl)
+struct GraphKey {
+  const void* f = nullptr;
+  int64_t ld = 0, batch = 0;
+  void* freqs = nullptr;
+  void* coeffs = nullptr;
+  void* ws = nullptr;
+  bool operator==(const GraphKey& o) const {
+    return f == o.f && ld == o.ld && batch == o.batch && freqs == o.freqs && coeffs == o.coeffs && ws == o.ws;
+  }
+};
+
 struct Plan {
   dsft_plan_info info{};
   dsft_params params{};
@@ -104,11 +118,8 @@ struct Plan {
   int64_t sumP = 0, maxSP = 0;
   Bucket bk[DSFT_MAX_T];
   int order[DSFT_MAX_T] = {};   // processing order of the bucket primes (plan.cpp choose_order)
-  // K1 schedule: k1_groups[g] consecutive primes (in processing order) per K1 launch.
-  // One group per prime = the two-buffer pipeline (Z buffer k mod 2); otherwise every
-  // prime has its own Z region (z_off) and K1 launches need not wait for K3.
-  int n_k1_groups = 0;
-  int k1_groups[DSFT_MAX_T] = {};
+  // K1 schedule (k1_grouped): one launch per prime into two reused Z buffers, or one
+  // launch for all primes, every prime with its own Z region (z_off), when all fit L2
   int64_t z_off[DSFT_MAX_T] = {};  // per-prime Z region offsets (elements per vector) when grouped
   int64_t z_tot = 0;
   std::vector<double> k1tab;   // [J][kappa][2] cos/sin(q_j u 2pi/N), u = 1..kappa
@@ -134,6 +145,9 @@ struct Plan {
   // fork/join events, no timing)
   cudaStream_t aux = nullptr, aux3 = nullptr, aux2 = nullptr;  // aux2: every other K2 launch
   std::string jit_why;         // why some bucket runs the runtime-radix K2 ("" if none)
+  cudaStream_t capst = nullptr;      // graph capture stream
+  cudaGraphExec_t gexec = nullptr;   // the captured execute sequence (execute_impl)
+  GraphKey gkey;
   std::vector<cudaEvent_t> pipe_ev;
 };
 
@@ -150,6 +164,7 @@ struct WsLayout {
   int64_t bn_vec;    // elements per vector in band_n: J
 };
 WsLayout ws_layout(const Plan& p, int64_t nvec);
+bool k1_grouped(const Plan& p, int64_t nvec);
 
 // ---- kernel launchers (kernels.cu); all stream-ordered, return cudaError_t
 // K1 over the nodes of nprime bucket primes ts[] (one launch), prime i writing Zs[i]
@@ -193,4 +208,9 @@ struct dsft_plan {
 namespace dsft {
 // plan.cpp: K1..K45 for the bands j = rank (mod world) of vector 0; zeroes band counts first.
 dsft_status run_sharded_bands(dsft_plan* pl, const double2* f, int rank, int world, cudaStream_t st, int* nb_out);
+// plan.cpp: record msg for dsft_last_error and return st
+dsft_status set_error(dsft_status st, const std::string& msg);
+// plan.cpp: the stream-ordered batched execute (waves of the workspace batch)
+dsft_status execute_batched_impl(dsft_plan* pl, const double2* f, int64_t batch, int64_t ld, int64_t* freqs,
+                                 double2* coeffs, cudaStream_t st);
 }  // namespace dsft

@@ -23,6 +23,7 @@
 #include <algorithm>
 #include <climits>
 #include <cmath>
+#include <mutex>
 
 #include "internal.h"
 #ifndef K5_SUB
@@ -57,16 +58,20 @@ struct K1Params {
   int64_t ld;            // elements between vectors
   int64_t N;
   int nb, kappa, nprime, pad_;
+  // listed bands: global band jfirst + jj * jstride, jj < nb, of the plan's J (the
+  // sharded path lists j = rank mod world); every kernel forms the band phase
+  // e^{i q_j d0} by the same two recurrences over the GLOBAL band index (k1_phase_*),
+  // so a band's samples are bitwise the same whichever bands are listed
+  int J, jfirst, jstride, pad2_;
   int cta_off[DSFT_MAX_T + 1];
   double neg_half_inv_c1sq;  // -1 / (2 c1^2)
   double inv_c1N;            // 1 / (c1 N)
   double h_over_c1sq;        // (2 pi / N) / c1^2
-  double qfirst, qstep;      // q of the first listed band, spacing between listed bands
-  const double* tab_dev;     // rows of [J][kappa][2] (generic-kappa path)
-  int64_t tab_stride;        // doubles between listed bands in tab_dev
+  double q1, qspan;          // centre of global band 0 and the spacing 2w of the band centres
+  const double* tab_dev;     // [J][kappa][2] cos/sin(q_j u 2 pi / N) (generic-kappa path)
   const double* ctab_dev;    // [kappa+1]
   double ctab[8];
-  double tab[kK1TabMax];     // [nb][kappa][2] cos/sin(q_j u 2 pi / N) (fast path)
+  double tab[kK1TabMax];     // [J][kappa][2] cos/sin(q_j u 2 pi / N) (fast path)
   K1Prime pr[DSFT_MAX_T];
 };
 static_assert(sizeof(K1Params) <= 32764, "K1Params exceeds the kernel parameter limit");
@@ -106,8 +111,9 @@ __device__ __forceinline__ NodeGeo node_geo(const K1Prime& p, int64_t N, int sig
 // Fast path (KAPPA in {4, 6}): each warp stages the 32 windows of its nodes in
 // shared memory with coalesced half-warp loads (one 208-B window per half-warp
 // request instead of 32 scattered 16-B requests), then every lane runs the band
-// mix for its own node.  Index math is 32-bit (N < 2^31): the window start is
-// broadcast with one shuffle and only windows that wrap take the mod-N path.
+// mix for its own node.  Index math in IdxT: 32-bit when N < 2^31 (one shuffle per
+// window start), 64-bit otherwise (any N); only windows that wrap
+// take the mod-N path.
 constexpr int kK1FastThreads = 128;
 
 // j' = round(kN/L) from a double estimate, corrected exactly in integers so
@@ -128,6 +134,28 @@ __device__ __forceinline__ NodeGeo node_geo_fast(const K1Prime& p, int64_t N, in
     num0 += L;
   }
   return NodeGeo{jp, (double)num0 * __ldg(p.shift_scale + sigma)};
+}
+
+// Output slot of global band j in the listed bands, or -1
+__device__ __forceinline__ int k1_slot(const K1Params& p, int j) {
+  const int d = j - p.jfirst;
+  if (d < 0 || d % p.jstride) return -1;
+  const int sl = d / p.jstride;
+  return sl < p.nb ? sl : -1;
+}
+
+// The band phases e^{i q_j d0}, q_j = q1 + j qspan: two interleaved recurrences over
+// the global band index, ph (even j) and ph1 (odd j), each advanced by e^{2 i qspan d0}
+// per band pair (half the dependency depth of one chain).
+__device__ __forceinline__ void k1_phase_init(const K1Params& p, double d0, double2& ph, double2& ph1,
+                                              double2& step2) {
+  double sn, cs;
+  sincos(p.q1 * d0, &sn, &cs);
+  ph = make_double2(cs, sn);
+  sincos(p.qspan * d0, &sn, &cs);
+  const double2 step = make_double2(cs, sn);
+  step2 = cmul(step, step);
+  ph1 = cmul(ph, step);
 }
 
 // Band mix of one node from its window (2 kappa + 1 values at `win`, shared
@@ -159,21 +187,24 @@ __device__ __forceinline__ void k1_mix_node(const K1Params& p, const K1Prime& pp
     A[u - 1] = cadd(pu, mu);
     D[u - 1] = csub(pu, mu);
   }
-  double sn, cs;
-  sincos(p.qfirst * d0, &sn, &cs);
-  double2 ph = make_double2(cs, sn);
-  sincos(p.qstep * d0, &sn, &cs);
-  const double2 step = make_double2(cs, sn);
+  double2 ph, ph1, step2;
+  k1_phase_init(p, d0, ph, ph1, step2);
   const uint64_t pol_z = pp.keep_l2 ? l2_evict_last() : l2_evict_first();
   double2* zo = pp.Z + (int64_t)v * pp.z_vec_stride + (int64_t)sigma * pp.P + q;
   const int64_t band_stride = (int64_t)pp.S * pp.P;
-  // two bands per iteration, cos and sin parts in separate accumulators:
+  // two global bands per iteration, cos and sin parts in separate accumulators:
   // 8 independent DFMA chains instead of 2 (the FP64 latency, not its
-  // throughput, bounded the single-chain loop)
-  const double2 step2 = cmul(step, step);
-  double2 ph1 = cmul(ph, step);
+  // throughput, bounded the single-chain loop); unlisted bands only advance the
+  // phase recurrences
+  const bool all = p.jfirst == 0 && p.jstride == 1 && p.nb == p.J;
   int j = 0;
-  for (; j + 1 < p.nb; j += 2) {
+  for (; j + 1 < p.J; j += 2) {
+    const int s0 = all ? j : k1_slot(p, j), s1 = all ? j + 1 : k1_slot(p, j + 1);
+    if (s0 < 0 && s1 < 0) {
+      ph = cmul(ph, step2);
+      ph1 = cmul(ph1, step2);
+      continue;
+    }
     double rc0 = P0.x, rs0 = 0.0, ic0 = P0.y, is0 = 0.0;
     double rc1 = P0.x, rs1 = 0.0, ic1 = P0.y, is1 = 0.0;
     const double* tb = p.tab + j * KAPPA * 2;
@@ -190,12 +221,13 @@ __device__ __forceinline__ void k1_mix_node(const K1Params& p, const K1Prime& pp
       ic1 = fma(A[u].y, c1, ic1);
       is1 = fma(D[u].x, s1, is1);
     }
-    st_keep(zo + j * band_stride, cmul(make_double2(rc0 + rs0, ic0 - is0), ph), pol_z);
-    st_keep(zo + (j + 1) * band_stride, cmul(make_double2(rc1 + rs1, ic1 - is1), ph1), pol_z);
+    if (s0 >= 0) st_keep(zo + s0 * band_stride, cmul(make_double2(rc0 + rs0, ic0 - is0), ph), pol_z);
+    if (s1 >= 0) st_keep(zo + s1 * band_stride, cmul(make_double2(rc1 + rs1, ic1 - is1), ph1), pol_z);
     ph = cmul(ph, step2);
     ph1 = cmul(ph1, step2);
   }
-  if (j < p.nb) {
+  const int sl = j < p.J ? (all ? j : k1_slot(p, j)) : -1;
+  if (sl >= 0) {
     double rc = P0.x, rs = 0.0, ic = P0.y, is = 0.0;
     const double* tb = p.tab + j * KAPPA * 2;
 #pragma unroll
@@ -206,11 +238,11 @@ __device__ __forceinline__ void k1_mix_node(const K1Params& p, const K1Prime& pp
       ic = fma(A[u].y, c, ic);
       is = fma(D[u].x, sg, is);
     }
-    st_keep(zo + j * band_stride, cmul(make_double2(rc + rs, ic - is), ph), pol_z);
+    st_keep(zo + sl * band_stride, cmul(make_double2(rc + rs, ic - is), ph), pol_z);
   }
 }
 
-template <int KAPPA>
+template <int KAPPA, typename IdxT>
 __global__ void __launch_bounds__(kK1FastThreads) k1_gather_mix_fast(const __grid_constant__ K1Params p) {
   constexpr int W = 2 * KAPPA + 1;
   __shared__ double2 s_win[kK1FastThreads / 32][32][W];
@@ -224,9 +256,9 @@ __global__ void __launch_bounds__(kK1FastThreads) k1_gather_mix_fast(const __gri
   const int sigma = active ? gid / pp.P : 0;
   const int q = active ? gid - sigma * pp.P : 0;
   const NodeGeo g = active ? node_geo_fast(pp, p.N, sigma, rader_node(pp, q)) : NodeGeo{0, 0.0};
-  const int N = (int)p.N;
+  const IdxT N = (IdxT)p.N;
   // window start j' - kappa, or -1 - start for windows that wrap mod N
-  int st = (int)g.jp - KAPPA;
+  IdxT st = (IdxT)g.jp - KAPPA;
   if (st < 0 || st + W > N) st = -1 - ((st % N) + N) % N;
   const double2* fv = p.f + (int64_t)v * p.ld;
   {
@@ -237,9 +269,9 @@ __global__ void __launch_bounds__(kK1FastThreads) k1_gather_mix_fast(const __gri
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
       const int m = 2 * i + h;
-      const int stm = __shfl_sync(0xffffffffu, st, m);
+      const IdxT stm = __shfl_sync(0xffffffffu, st, m);
       if (lane_on && first + m < nodes) {
-        int idx;
+        IdxT idx;
         if (stm >= 0) {
           idx = stm + u;
         } else {
@@ -258,96 +290,99 @@ __global__ void __launch_bounds__(kK1FastThreads) k1_gather_mix_fast(const __gri
   k1_mix_node<KAPPA>(p, pp, v, sigma, q, g.d0, &s_win[warp][lane][0]);
 }
 
-// KAPPA > 0: compile-time window, table in kernel parameters (constant bank).
-// KAPPA == 0: runtime kappa (THM4 presets), tables in global memory.
-template <int KAPPA>
-__global__ void __launch_bounds__(256) k1_gather_mix(const __grid_constant__ K1Params p) {
-  constexpr int KM = KAPPA > 0 ? KAPPA : 32;
-  const int kappa = KAPPA > 0 ? KAPPA : p.kappa;
+// Any kappa (THM4: kappa = O(r log N) taps; kappa overrides): one
+// thread per node, the window read tap pair by tap pair (u, -u) outward from the
+// centre through L1 (a thread's window is contiguous: each 128-B line is fetched
+// once), the Gaussian taps by the recurrence G_u = G_0 E^u C_u, and the JB
+// listed bands of a chunk accumulated in registers: per tap pair and band 4 DFMA
+// on A_u = a_u + a_-u, D_u = a_u - a_-u with the band's cos/sin(q_j u h) staged in
+// shared memory ([u][band] rows: every lane reads the same entry, a broadcast).
+// Bands beyond JB run as further chunks over the same window (L1/L2-resident).
+constexpr int kK1GenThreads = 128;
+
+template <int JB>
+__global__ void __launch_bounds__(kK1GenThreads) k1_gather_mix_gen(const __grid_constant__ K1Params p) {
+  extern __shared__ double2 k1g_smem[];
+  double2* s_tab = k1g_smem;                            // [kappa][JB] (cos, sin)
+  double* s_ctab = (double*)(k1g_smem + p.kappa * JB);  // [kappa + 1]
+  const int kappa = p.kappa;
+  for (int u = threadIdx.x; u <= kappa; u += kK1GenThreads) s_ctab[u] = __ldg(p.ctab_dev + u);
   int lb;
   const K1Prime& pp = p.pr[k1_prime(p, lb)];
   const int64_t nodes = (int64_t)pp.node0 + pp.nnode;
-  const int64_t gid = (int64_t)pp.node0 + (int64_t)lb * blockDim.x + threadIdx.x;
-  if (gid >= nodes) return;
+  const int64_t gid = (int64_t)pp.node0 + (int64_t)lb * kK1GenThreads + threadIdx.x;
+  const bool active = gid < nodes;
   const int v = blockIdx.y;
-  const int sigma = (int)(gid / pp.P);
-  const int64_t q = gid - (int64_t)sigma * pp.P;
-  const int64_t n1 = rader_node(pp, (int)q);
-  const int64_t r = __ldg(pp.shift_r + sigma);
-  const int64_t L = (int64_t)pp.P * r;
-  int64_t k = r * n1 + (int64_t)pp.P * (int64_t)__ldg(pp.shift_n2 + sigma);
-  if (k >= L) k -= L;
+  const int sigma = active ? (int)(gid / pp.P) : 0;
+  const int64_t q = active ? gid - (int64_t)sigma * pp.P : 0;
+  const NodeGeo g = active ? node_geo(pp, p.N, sigma, rader_node(pp, (int)q)) : NodeGeo{0, 0.0};
   const int64_t N = p.N;
-  // j' = round(kN / L): L is odd, so 2kN + L is never an exact multiple tie (R3).
-  const int64_t jp = (2 * k * N + L) / (2 * L);
-  const int64_t num0 = k * N - jp * L;            // (x - y_j') N L / (2 pi), exact
-  const double d0 = (double)num0 * __ldg(pp.shift_scale + sigma);
-
-  // window f_{j'-kappa .. j'+kappa} (indices mod N)
   const double2* fv = p.f + (int64_t)v * p.ld;
-  double2 fw[2 * KM + 1];
-  const int64_t j0 = jp - kappa;
-  if (j0 >= 0 && jp + kappa < N) {
-#pragma unroll
-    for (int u = 0; u < 2 * KM + 1; ++u)
-      if (KAPPA > 0 || u <= 2 * kappa) fw[u] = ldg2(fv + j0 + u);
-  } else {
-#pragma unroll
-    for (int u = 0; u < 2 * KM + 1; ++u) {
-      if (KAPPA > 0 || u <= 2 * kappa) {
-        int64_t idx = (j0 + u) % N;
-        if (idx < 0) idx += N;
-        fw[u] = ldg2(fv + idx);
-      }
+  const int64_t j0 = g.jp - kappa;
+  const bool wraps = j0 < 0 || g.jp + kappa >= N;
+  auto fat = [&](int64_t idx) -> double2 {  // f_{idx mod N}
+    if (wraps) {
+      idx %= N;
+      if (idx < 0) idx += N;
     }
-  }
-
-  // Gaussian taps g(d_u)/N, d_u = d0 - u h, via G_u = G_0 E^u C_u (DESIGN.md §6 K1)
-  const double G0 = exp(d0 * d0 * p.neg_half_inv_c1sq) * p.inv_c1N;
-  const double E = exp(d0 * p.h_over_c1sq);
+    return ldg2(fv + idx);
+  };
+  const double G0 = exp(g.d0 * g.d0 * p.neg_half_inv_c1sq) * p.inv_c1N;
+  const double E = exp(g.d0 * p.h_over_c1sq);
   const double Ei = 1.0 / E;
-  const double2 P0 = cscale(fw[kappa], G0);
-  double2 A[KM], D[KM];
-  double ep = G0, em = G0;
-#pragma unroll
-  for (int u = 1; u <= KM; ++u) {
-    if (KAPPA > 0 || u <= kappa) {
-      ep *= E;
-      em *= Ei;
-      const double cu = KAPPA > 0 ? p.ctab[u] : __ldg(p.ctab_dev + u);
-      const double2 pp = cscale(fw[kappa + u], ep * cu);
-      const double2 pm = cscale(fw[kappa - u], em * cu);
-      A[u - 1] = cadd(pp, pm);
-      D[u - 1] = csub(pp, pm);
-    }
-  }
-
-  // per-node band phase e^{i q d0}, advanced by e^{i qstep d0} between bands
-  double sn, cs;
-  sincos(p.qfirst * d0, &sn, &cs);
-  double2 ph = make_double2(cs, sn);
-  sincos(p.qstep * d0, &sn, &cs);
-  const double2 step = make_double2(cs, sn);
-
+  const double2 P0 = active ? cscale(fat(g.jp), G0) : make_double2(0.0, 0.0);
   double2* zo = pp.Z + (int64_t)v * pp.z_vec_stride + (int64_t)sigma * pp.P + q;
   const int64_t band_stride = (int64_t)pp.S * pp.P;
-  for (int j = 0; j < p.nb; ++j) {
-    double re = P0.x, im = P0.y;
-    const double* tb = KAPPA > 0 ? (p.tab + j * KAPPA * 2) : (p.tab_dev + (int64_t)j * p.tab_stride);
+  const uint64_t pol_z = pp.keep_l2 ? l2_evict_last() : l2_evict_first();
+  for (int jb0 = 0; jb0 < p.nb; jb0 += JB) {  // CTA-uniform
+    const int nbc = min(JB, p.nb - jb0);
+    __syncthreads();
+    for (int e = threadIdx.x; e < kappa * JB; e += kK1GenThreads) {
+      const int u = e / JB, jj = e - u * JB;
+      double2 cs = make_double2(0.0, 0.0);
+      if (jj < nbc) {
+        const double* tb = p.tab_dev + (int64_t)(p.jfirst + (jb0 + jj) * p.jstride) * kappa * 2 + 2 * u;
+        cs = make_double2(__ldg(tb), __ldg(tb + 1));
+      }
+      s_tab[e] = cs;
+    }
+    __syncthreads();
+    if (!active) continue;
+    double2 acc[JB];
 #pragma unroll
-    for (int u = 0; u < KM; ++u) {
-      if (KAPPA > 0 || u < kappa) {
-        const double c = KAPPA > 0 ? tb[2 * u] : __ldg(tb + 2 * u);
-        const double s = KAPPA > 0 ? tb[2 * u + 1] : __ldg(tb + 2 * u + 1);
-        // A c - i D s
-        re = fma(A[u].x, c, re);
-        re = fma(D[u].y, s, re);
-        im = fma(A[u].y, c, im);
-        im = fma(-D[u].x, s, im);
+    for (int jj = 0; jj < JB; ++jj) acc[jj] = P0;
+    double ep = G0, em = G0;
+    for (int u = 1; u <= kappa; ++u) {
+      ep *= E;
+      em *= Ei;
+      const double cu = s_ctab[u];
+      const double2 pu = cscale(fat(g.jp + u), ep * cu);
+      const double2 mu = cscale(fat(g.jp - u), em * cu);
+      const double2 A = cadd(pu, mu), D = csub(pu, mu);
+      const double2* row = s_tab + (u - 1) * JB;
+#pragma unroll
+      for (int jj = 0; jj < JB; ++jj) {
+        const double2 cs = row[jj];  // A c - i D s
+        acc[jj].x = fma(A.x, cs.x, fma(D.y, cs.y, acc[jj].x));
+        acc[jj].y = fma(A.y, cs.x, fma(-D.x, cs.y, acc[jj].y));
       }
     }
-    zo[j * band_stride] = cmul(make_double2(re, im), ph);
-    ph = cmul(ph, step);
+    // band phases e^{i q_j d0} by the global recurrences (k1_phase_init), walked to
+    // each listed band's global index
+    double2 pe, po, step2;
+    k1_phase_init(p, g.d0, pe, po, step2);
+    int pair = 0;
+#pragma unroll
+    for (int jj = 0; jj < JB; ++jj) {
+      if (jj < nbc) {
+        const int gj = p.jfirst + (jb0 + jj) * p.jstride;
+        for (; pair < gj / 2; ++pair) {
+          pe = cmul(pe, step2);
+          po = cmul(po, step2);
+        }
+        st_keep(zo + (int64_t)(jb0 + jj) * band_stride, cmul(acc[jj], (gj & 1) ? po : pe), pol_z);
+      }
+    }
   }
 }
 
@@ -1268,10 +1303,17 @@ __global__ void k_debug_grid(const __grid_constant__ DbgParams p) {
 // ================================================================= launchers
 static inline unsigned cdiv(int64_t a, int64_t b) { return (unsigned)((a + b - 1) / b); }
 
+// Function attributes are per device: set them once for every device a plan is
+// created on (bit d of the mask), under a lock.
 cudaError_t kernels_init() {
-  static bool done = false;
-  if (done) return cudaSuccess;
-  cudaError_t e;
+  static std::mutex mu;
+  static uint64_t done_mask = 0;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+  std::lock_guard<std::mutex> lk(mu);
+  if (done_mask >> dev & 1) return cudaSuccess;
   const int maxsm = 227 * 1024 - 1024;  // leave room for the static reduction buffer
   if ((e = cudaFuncSetAttribute(k2_prime_dft<64, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm))) return e;
   if ((e = cudaFuncSetAttribute(k6_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, kK6Stage * 16))) return e;
@@ -1280,16 +1322,12 @@ cudaError_t kernels_init() {
   if ((e = cudaFuncSetAttribute(k2_prime_dft<256, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm))) return e;
   if ((e = cudaFuncSetAttribute(k2_prime_dft<512, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm))) return e;
   if ((e = cudaFuncSetAttribute(k2a_split<512, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm))) return e;
-  if (const char* co = getenv("DSFT_CARVEOUT")) {  // experiment: one shared-memory carveout for all kernels
-    const int pct = atoi(co);
-    const void* fs[] = {(const void*)k1_gather_mix_fast<6>, (const void*)k1_gather_mix_fast<4>,
-                        (const void*)k3_identify<7, 0>, (const void*)k3_identify<13, 0>, (const void*)k3_identify<17, 0>,
-                        (const void*)k3_identify<31, 0>, (const void*)k5s_scan, (const void*)k5a_medians,
-                        (const void*)k5b_select, (const void*)k6_merge};
-    for (const void* f : fs)
-      if ((e = cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, pct))) return e;
-  }
-  done = true;
+  const int k1g = kK1MaxKappa * 32 * 16 + (kK1MaxKappa + 1) * 8;
+  if ((e = cudaFuncSetAttribute(k1_gather_mix_gen<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, k1g))) return e;
+  if ((e = cudaFuncSetAttribute(k1_gather_mix_gen<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, k1g))) return e;
+  if ((e = cudaFuncSetAttribute(k1_gather_mix_gen<24>, cudaFuncAttributeMaxDynamicSharedMemorySize, k1g))) return e;
+  if ((e = cudaFuncSetAttribute(k1_gather_mix_gen<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, k1g))) return e;
+  done_mask |= 1ull << dev;
   return cudaSuccess;
 }
 
@@ -1309,21 +1347,24 @@ cudaError_t launch_k1(const Plan& p, int nprime, const int* ts, double2* const* 
   k.inv_c1N = 1.0 / (p.c1 * (double)p.N);
   const double h = 2.0 * M_PI / (double)p.N;
   k.h_over_c1sq = h / (p.c1 * p.c1);
-  k.qfirst = (double)band_q(p, bands[0]);
+  // listed band jj = global band bands[0] + jj * stride (the plan's band lists are
+  // arithmetic progressions: all bands, or j = rank mod world)
   const int stride = nbands > 1 ? bands[1] - bands[0] : 1;
-  k.qstep = (double)(2 * p.w * (int64_t)stride);
-  // device table: [J][kappa][2] then ctab[kappa+1]; listed band jj is row bands[0] + jj*stride
-  k.tab_dev = p.k1tab_dev + (size_t)bands[0] * p.kappa * 2;
-  k.tab_stride = (int64_t)stride * p.kappa * 2;
+  k.J = p.J;
+  k.jfirst = bands[0];
+  k.jstride = stride;
+  k.q1 = (double)band_q(p, 0);
+  k.qspan = (double)(2 * p.w);
+  // device table: [J][kappa][2] then ctab[kappa+1]
+  k.tab_dev = p.k1tab_dev;
   k.ctab_dev = p.k1tab_dev + (size_t)p.J * p.kappa * 2;
-  const bool fast = (p.kappa == 4 || p.kappa == 6) && nbands * p.kappa * 2 <= kK1TabMax;
+  const bool fast = (p.kappa == 4 || p.kappa == 6) && p.J * p.kappa * 2 <= kK1TabMax;
+  const bool big = p.N > (int64_t)INT32_MAX - 64;  // 64-bit window indices
   if (fast) {
     for (int u = 0; u <= p.kappa; ++u) k.ctab[u] = p.ctab[u];
-    for (int jj = 0; jj < nbands; ++jj)
-      for (int u = 0; u < p.kappa; ++u)
-        for (int c = 0; c < 2; ++c) k.tab[(jj * p.kappa + u) * 2 + c] = p.k1tab[((size_t)bands[jj] * p.kappa + u) * 2 + c];
+    for (size_t e = 0; e < (size_t)p.J * p.kappa * 2; ++e) k.tab[e] = p.k1tab[e];
   }
-  const int cta = fast ? kK1FastThreads : 256;
+  const int cta = fast ? kK1FastThreads : kK1GenThreads;
   k.cta_off[0] = 0;
   for (int i = 0; i < nprime; ++i) {
     const Bucket& b = p.bk[ts[i]];
@@ -1343,9 +1384,23 @@ cudaError_t launch_k1(const Plan& p, int nprime, const int* ts, double2* const* 
     k.cta_off[i + 1] = k.cta_off[i] + (int)cdiv((int64_t)q.nnode, cta);
   }
   const dim3 grid((unsigned)k.cta_off[nprime], nvec);
-  if (fast && p.kappa == 6) k1_gather_mix_fast<6><<<grid, kK1FastThreads, 0, st>>>(k);
-  else if (fast && p.kappa == 4) k1_gather_mix_fast<4><<<grid, kK1FastThreads, 0, st>>>(k);
-  else k1_gather_mix<0><<<grid, 256, 0, st>>>(k);
+  if (fast && p.kappa == 6 && !big) k1_gather_mix_fast<6, int><<<grid, kK1FastThreads, 0, st>>>(k);
+  else if (fast && p.kappa == 6) k1_gather_mix_fast<6, int64_t><<<grid, kK1FastThreads, 0, st>>>(k);
+  else if (fast && p.kappa == 4 && !big) k1_gather_mix_fast<4, int><<<grid, kK1FastThreads, 0, st>>>(k);
+  else if (fast && p.kappa == 4) k1_gather_mix_fast<4, int64_t><<<grid, kK1FastThreads, 0, st>>>(k);
+  else {
+    // band chunk: the smallest instantiation holding ceil(nb / ceil(nb / 32)) bands
+    // (43 bands run as two chunks of <= 24 instead of 32 + 11)
+    const int nch = (nbands + 31) / 32, per = (nbands + nch - 1) / nch;
+    const int jb = per <= 8 ? 8 : per <= 16 ? 16 : per <= 24 ? 24 : 32;
+    const size_t sm = (size_t)p.kappa * jb * 16 + (size_t)(p.kappa + 1) * 8;
+    switch (jb) {
+      case 8: k1_gather_mix_gen<8><<<grid, kK1GenThreads, sm, st>>>(k); break;
+      case 16: k1_gather_mix_gen<16><<<grid, kK1GenThreads, sm, st>>>(k); break;
+      case 24: k1_gather_mix_gen<24><<<grid, kK1GenThreads, sm, st>>>(k); break;
+      default: k1_gather_mix_gen<32><<<grid, kK1GenThreads, sm, st>>>(k); break;
+    }
+  }
   return cudaGetLastError();
 }
 
@@ -1409,12 +1464,11 @@ cudaError_t launch_k2(const Plan& p, int t, double2* Z, int64_t zstride, int nve
   // Shared-memory carveout: just enough for the resident rows, so the rest of
   // the unified 256 KB stays L1 for bhat and the twiddle tables (read by every
   // CTA on the SM).
-  auto carve = [&](const void* fn, int slot, int minb) -> cudaError_t {
-    static int last_pct[3] = {-1, -1, -1};
+  // (a host call per launch: the attribute is per device and per function, shared by
+  // every plan, so it is not cached here)
+  auto carve = [&](const void* fn, int /*slot*/, int minb) -> cudaError_t {
     const double need = (double)minb * ((double)smem + 1024.0 + 64.0);
     const int pct = std::min(100, (int)std::ceil(100.0 * need / (228.0 * 1024.0)));
-    if (last_pct[slot] == pct) return cudaSuccess;
-    last_pct[slot] = pct;
     return cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
   };
   cudaError_t e;
@@ -1507,13 +1561,10 @@ static K6Params k6_params(const int64_t* bw, const double2* bc, const double* bm
   return k;
 }
 
-// launch with programmatic stream serialization (DSFT_PDL=0: plain stream order)
+// launch with programmatic stream serialization (the kernel's griddepcontrol.wait
+// precedes its first read of the predecessor's output)
 template <typename... KArgs, typename... Args>
 static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 g, dim3 b, size_t smem, cudaStream_t st, Args... args) {
-  static const bool off = [] {
-    const char* e = getenv("DSFT_PDL");
-    return e && strcmp(e, "0") == 0;
-  }();
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = g;
   cfg.blockDim = b;
@@ -1521,7 +1572,7 @@ static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 g, dim3 b, size_t sme
   cfg.stream = st;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = off ? 0 : 1;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, kern, args...);

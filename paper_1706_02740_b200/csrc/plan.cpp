@@ -201,8 +201,6 @@ static void choose_k2_dims(Bucket& b, std::vector<int>& rad) {
   b.dim_s0[0] = 0;
   b.dim_s0[1] = (int)rad.size();
   b.twf = 0;
-  const char* env = getenv("DSFT_K2_PFA");  // "0": one dimension (experiments)
-  if (env && strcmp(env, "0") == 0) return;
   std::vector<int> comp;  // prime-power components
   for (int m = M, p = 2; m > 1; ++p)
     if (m % p == 0) {
@@ -263,7 +261,7 @@ static void choose_k2_dims(Bucket& b, std::vector<int>& rad) {
 // SM (8 warps, 128 registers: 4 warps per SM sub-partition), <512,1> one row per
 // SM.  (Measured alternative, round 1: the middle stages as independent
 // warp-group sub-FFTs with group barriers ran 1.2-1.4x slower per row.)
-bool choose_k2_layout(Bucket& b, std::vector<int>& rad) {
+bool choose_k2_layout(Bucket& b, std::vector<int>& rad, bool no_cluster) {
   const int M = b.M;
   b.split = 0;
   b.cl = 0;
@@ -274,8 +272,7 @@ bool choose_k2_layout(Bucket& b, std::vector<int>& rad) {
   // leave a sub-FFT of at least two passes); split mode with R0 = C is the fallback.
   // (Measured: for rows that fit one CTA, P ~ 7.5k-14.5k, the single-CTA kernel is
   // faster -- config 2, s = 1000: 2170 vs 1982 transforms/s; s = 4000: 332 -> 461.)
-  const char* clenv = getenv("DSFT_K2_CLUSTER");
-  if (!(clenv && strcmp(clenv, "0") == 0) && (size_t)M * 16 + 2048 > 227 * 1024) {
+  if (!no_cluster && (size_t)M * 16 + 2048 > 227 * 1024) {
     for (int c = 2; c <= 8; ++c) {
       if (M % c) continue;
       const int ms = M / c;
@@ -292,8 +289,7 @@ bool choose_k2_layout(Bucket& b, std::vector<int>& rad) {
       return true;
     }
   }
-  size_t split_above = 227 * 1024;  // DSFT_SPLIT_KB: experiments (split rows above this many KB)
-  if (const char* e = getenv("DSFT_SPLIT_KB")) split_above = (size_t)std::max(1, atoi(e)) * 1024;
+  const size_t split_above = 227 * 1024;
   if ((size_t)M * 16 + 2048 > split_above) {
     // split mode: the smallest R0 | M whose blocks of M/R0 fit one CTA (K2a), final
     // radix-R0 stage across blocks in K2b
@@ -329,6 +325,13 @@ bool choose_k2_layout(Bucket& b, std::vector<int>& rad) {
 // ======================================================================= layout
 namespace dsft {
 
+// One K1 launch for every bucket prime when the filtered samples of all of them
+// (nvec vectors) fit comfortably in L2; otherwise one launch per prime into two
+// reused Z buffers (plan.cpp choose_order, run_bands).
+bool k1_grouped(const Plan& p, int64_t nvec) {
+  return p.T > 1 && (double)nvec * (double)p.z_tot * 16.0 <= kK1OneLaunchBytes;
+}
+
 WsLayout ws_layout(const Plan& p, int64_t nvec) {
   WsLayout L{};
   L.z_vec = (int64_t)p.J * p.maxSP;
@@ -342,7 +345,7 @@ WsLayout ws_layout(const Plan& p, int64_t nvec) {
     return at;
   };
   L.z_buf = nvec * L.z_vec;
-  const bool grouped = p.n_k1_groups > 0 && p.n_k1_groups < p.T;
+  const bool grouped = k1_grouped(p, nvec);
   L.z = take(grouped ? (size_t)nvec * p.z_tot * 16 : (size_t)kZBufs * L.z_buf * 16);
   L.zs = take(p.any_split ? (size_t)L.z_buf * 16 : 0);
   L.cand_w = take((size_t)nvec * L.cw_vec * 8);
@@ -373,6 +376,8 @@ WsLayout ws_layout(const Plan& p, int64_t nvec) {
 // =================================================================== derivation
 static dsft_status derive(int64_t N, int64_t s, const dsft_params& prm, Plan& P) {
   if (N < 36) return fail(DSFT_ERR_CONFIG, "N must be >= 36 (PAPER.md:498)");
+  // K1's node geometry forms 2 k N + L in int64 (k < L < 2^21): N below 2^40
+  if (N > ((int64_t)1 << 40)) return fail(DSFT_ERR_UNSUPPORTED, "N > 2^40 (int64 node geometry)");
   if (s < 2 || s > N) return fail(DSFT_ERR_CONFIG, "s must lie in [2, N] (PAPER.md:40)");
   if (!(prm.tau > 0.0 && prm.tau < 1.0 / sqrt(2.0 * M_PI)))
     return fail(DSFT_ERR_CONFIG, "tau must lie in (0, 1/sqrt(2 pi)) (Lemma 3)");
@@ -392,7 +397,7 @@ static dsft_status derive(int64_t N, int64_t s, const dsft_params& prm, Plan& P)
   if (prm.kappa > 0) kappa = prm.kappa;
   if (beta < 0) beta = sqrt(4.0 * M_PI * kappa / lnN);  // reading R4
   if (2 * (int64_t)kappa + 2 > N) return fail(DSFT_ERR_CONFIG, "2 kappa + 2 > N");
-  if (kappa > 31) return fail(DSFT_ERR_UNSUPPORTED, "kappa > 31 not supported by K1");
+  if (kappa > kK1MaxKappa) return fail(DSFT_ERR_UNSUPPORTED, "kappa > 256 not supported by K1");
   const double c1 = beta * sqrt(lnN) / (double)N;  // Algorithm 1 line 2
   if (!(c1 < 0.5)) return fail(DSFT_ERR_CONFIG, "c1 >= 0.5 (reading R5)");
   const double lg = log(1.0 / (prm.tau * sqrt(2.0 * M_PI)));
@@ -407,11 +412,13 @@ static dsft_status derive(int64_t N, int64_t s, const dsft_params& prm, Plan& P)
   const int64_t halfN_up = (N + 1) / 2;
   if (prm.n_bucket_primes < 0) return fail(DSFT_ERR_CONFIG, "need at least one bucket prime");
   // bucket-prime pool (reading R6)
+  if (prm.pool_rule != DSFT_POOL_FULL && prm.pool_rule != DSFT_POOL_SMOOTH)
+    return fail(DSFT_ERR_CONFIG, "unknown pool_rule");
   const int64_t lo = (int64_t)ceil(prm.bucket_factor * (double)s);
   const int64_t hi = 2 * lo;
   std::vector<int64_t> pool;
   for (int64_t pr : primes_below(hi))
-    if (pr >= lo && largest_prime_factor(pr - 1) <= 13) pool.push_back(pr);
+    if (pr >= lo && (prm.pool_rule == DSFT_POOL_FULL || largest_prime_factor(pr - 1) <= 13)) pool.push_back(pr);
   // T = 0: the deterministic variant (reading R13) -- every prime of the pool
   const int T = prm.n_bucket_primes == 0 ? (int)pool.size() : prm.n_bucket_primes;
   if (T < 1) return fail(DSFT_ERR_CONFIG, "need at least one bucket prime");
@@ -546,7 +553,7 @@ static dsft_status derive(int64_t N, int64_t s, const dsft_params& prm, Plan& P)
     }
     b.g = g;
     std::vector<int> rad;
-    if (!choose_k2_layout(b, rad)) return fail(DSFT_ERR_INTERNAL, "P-1 not 13-smooth or too many FFT stages");
+    if (!choose_k2_layout(b, rad, (prm.flags & DSFT_FLAG_NO_CLUSTER) != 0)) return fail(DSFT_ERR_UNSUPPORTED, "bucket prime whose P-1 is not 13-smooth (no general-prime K2 yet) or too many FFT stages");
     b.nfac = (int)rad.size();
     for (int i = 0; i < b.nfac; ++i) b.fac[i] = rad[i];
     if (b.ndim == 1) {
@@ -734,9 +741,8 @@ static dsft_status upload_tables(Plan& P) {
 // tuple, bucket primes compiled in parallel threads.  Rows of the runtime-radix
 // instantiation <64,8> (M <= 1200: cheap) and split-mode rows stay generic.
 static void specialise_k2(Plan& P) {
-  const char* env = getenv("DSFT_JIT");
-  if (env && strcmp(env, "0") == 0) {
-    P.jit_why = "disabled by DSFT_JIT=0";
+  if (P.params.flags & DSFT_FLAG_NO_JIT) {
+    P.jit_why = "disabled by DSFT_FLAG_NO_JIT";
     return;
   }
   int dev = 0;
@@ -744,9 +750,7 @@ static void specialise_k2(Plan& P) {
   std::vector<std::thread> th;
   std::vector<std::string> why(P.T);
   std::vector<std::string> why3(P.T);
-  const char* k3e = getenv("DSFT_K3_JIT");  // "0": runtime-residue K3 (experiments)
-  const bool k3jit = !(k3e && strcmp(k3e, "0") == 0);
-  for (int t = 0; t < P.T && k3jit; ++t)
+  for (int t = 0; t < P.T; ++t)
     th.emplace_back([&, t, dev] {
       cudaSetDevice(dev);
       Bucket& bb = P.bk[t];
@@ -764,14 +768,6 @@ static void specialise_k2(Plan& P) {
         bb.k2_jit = jit_k2(256, 2, bb.fac, bb.nfac, (size_t)(bb.M / bb.cl) * 16, &why[t], true);
         return;
       }
-      // DSFT_K2_JIT="threads,ctas_per_sm" (experiments): other occupancy for the rows
-      // that run two CTAs per SM, when that many rows fit in shared memory
-      if (const char* o = getenv("DSFT_K2_JIT")) {
-        int a = 0, c = 0;
-        if (sscanf(o, "%d,%d", &a, &c) == 2 && bb.fft_variant == 1 && a % 32 == 0 && a >= 64 && a <= 1024 &&
-            c >= 1 && (size_t)c * ((size_t)bb.M * 16 + 1088) <= 228 * 1024)
-          nt = a, minb = c;
-      }
       bb.jit_threads = nt;
       bb.k2_jit = jit_k2(nt, minb, bb.fac, bb.nfac, (size_t)bb.M * 16, &why[t], false, bb.twf);
     });
@@ -788,66 +784,21 @@ static void specialise_k2(Plan& P) {
 // Processing order of the bucket primes (results do not depend on it: K3's vote is
 // order-free): by K1/K3 work S_t P_t ascending, then the largest moved to the
 // second-to-last position, so the last (exposed) K3 is not the largest one and the
-// largest K2 overlaps the last K1.  (Measured at BASELINE config 2 with the
+// largest K2 overlaps the last K1.  (Measured round 1 at BASELINE config 2 with the
 // four-stream pipeline, twelve orders: ascending 2356, largest second-to-last
-// 2452-2458, largest first 2355-2365 transforms/s.)  DSFT_ORDER="i,j,..." overrides
-// (experiments); DSFT_ORDER_SWAP=0 keeps plain ascending order.
+// 2452-2458, largest first 2355-2365 transforms/s.)
+// K1 schedule: one launch per prime into two reused Z buffers (the working set of a
+// prime stays in L2), unless the filtered samples of ALL primes fit comfortably in L2
+// (small s): then one K1 launch covers every prime, each prime with its own Z region,
+// and no K1 waits for a K3 (fewer launches on the latency-bound small plans).
 static void choose_order(Plan& P) {
   std::vector<int> ord(P.T);
   for (int t = 0; t < P.T; ++t) ord[t] = t;
   std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) {
     return (int64_t)P.bk[a].S * P.bk[a].P < (int64_t)P.bk[b].S * P.bk[b].P;
   });
-  const char* sw = getenv("DSFT_ORDER_SWAP");
-  if (P.T >= 3 && !(sw && strcmp(sw, "0") == 0)) std::swap(ord[P.T - 1], ord[P.T - 2]);
-  if (const char* env = getenv("DSFT_ORDER")) {
-    std::vector<int> o;
-    std::string tok;
-    for (const char* c = env;; ++c) {
-      if (*c == ',' || *c == 0) {
-        if (!tok.empty()) o.push_back(atoi(tok.c_str()));
-        tok.clear();
-        if (!*c) break;
-      } else {
-        tok += *c;
-      }
-    }
-    std::vector<int> chk = o;
-    std::sort(chk.begin(), chk.end());
-    bool ok = (int)o.size() == P.T;
-    for (int i = 0; ok && i < P.T; ++i) ok = chk[i] == i;
-    if (ok) ord = o;
-  }
+  if (P.T >= 3) std::swap(ord[P.T - 1], ord[P.T - 2]);
   for (int k = 0; k < P.T; ++k) P.order[k] = ord[k];
-  // K1 schedule: one launch per prime (two reused Z buffers) unless DSFT_K1GROUPS =
-  // "a,b,..." (consecutive group sizes summing to T; experiments)
-  P.n_k1_groups = P.T;
-  for (int g = 0; g < P.T; ++g) P.k1_groups[g] = 1;
-  if (const char* env = getenv("DSFT_K1GROUPS")) {
-    std::vector<int> gs;
-    int sum = 0, cur = 0;
-    bool any = false;
-    for (const char* c = env;; ++c) {
-      if (*c >= '0' && *c <= '9') {
-        cur = cur * 10 + (*c - '0');
-        any = true;
-      } else {
-        if (any) {
-          gs.push_back(cur);
-          sum += cur;
-        }
-        cur = 0;
-        any = false;
-        if (!*c) break;
-      }
-    }
-    bool ok = sum == P.T && !gs.empty();
-    for (int g : gs) ok = ok && g >= 1;
-    if (ok) {
-      P.n_k1_groups = (int)gs.size();
-      for (size_t g = 0; g < gs.size(); ++g) P.k1_groups[g] = gs[g];
-    }
-  }
 }
 
 // =============================================================== ABI: basics
@@ -866,6 +817,8 @@ void dsft_params_default(dsft_params* p) {
   p->vote_min = 3;
   p->band_budget = 0;
   p->seed = 0;
+  p->pool_rule = DSFT_POOL_SMOOTH;
+  p->flags = 0;
 }
 
 const char* dsft_status_string(dsft_status st) {
@@ -957,6 +910,8 @@ void dsft_plan_destroy(dsft_plan* pl) {
   if (pl->p.aux) cudaStreamDestroy(pl->p.aux);
   if (pl->p.aux3) cudaStreamDestroy(pl->p.aux3);
   if (pl->p.aux2) cudaStreamDestroy(pl->p.aux2);
+  if (pl->p.gexec) cudaGraphExecDestroy(pl->p.gexec);
+  if (pl->p.capst) cudaStreamDestroy(pl->p.capst);
   if (pl->p.dev_tables) cudaFree(pl->p.dev_tables);
   if (pl->p.ws_owned && pl->p.ws) cudaFree(pl->p.ws);
   if (pl->p.io_dev) cudaFree(pl->p.io_dev);
@@ -997,14 +952,11 @@ static int64_t choose_wave(const Plan& p, int64_t batch) {
   // measured at config 4 (256 x 2^24): 64 MB waves (Z in L2) 8587 transforms/s,
   // 512 MB 10470, 1 GB 10718, 2 GB 10681 -- K2 is FP64-bound, Z may come from DRAM.
   const double zbytes = (double)p.J * p.maxSP * 16.0;
-  double budget = 1.0e9;
-  if (const char* e = getenv("DSFT_WAVE_MB")) budget = std::max(1.0, atof(e)) * 1e6;  // experiments
+  const double budget = 1.0e9;
   int64_t vb = (int64_t)(budget / std::max(zbytes, 1.0));
   // at most kMaxWave vectors (grid y); config 0 batched (4096 x N = 4096): cap 64 ->
   // 206k transforms/s, 4096 -> 255k (fewer fills / drains of the pipeline)
-  int64_t cap = kMaxWave;
-  if (const char* e = getenv("DSFT_WAVE_MAX")) cap = std::max<int64_t>(1, std::min<int64_t>(atoll(e), kMaxWave));
-  vb = std::max<int64_t>(1, std::min<int64_t>(vb, cap));
+  vb = std::max<int64_t>(1, std::min<int64_t>(vb, kMaxWave));
   return std::min<int64_t>(vb, std::max<int64_t>(batch, 1));
 }
 
@@ -1107,19 +1059,16 @@ static dsft_status run_bands(Plan& p, const double2* f, int64_t ld, int nv, cons
                              cudaStream_t st, int64_t* freqs = nullptr, double2* coeffs = nullptr) {
   dsft_status stt = ensure_pipe(p);
   if (stt != DSFT_OK) return stt;
-  const char* ser = getenv("DSFT_SERIAL");  // experiment knob: every launch on the caller's stream
-  const bool serial = ser && strcmp(ser, "1") == 0;
+  const bool serial = (p.params.flags & DSFT_FLAG_SERIAL) != 0;  // every launch on the caller's stream
   cudaStream_t a1 = serial ? st : p.aux, a3 = serial ? st : p.aux3;
   cudaEvent_t* evK1 = p.pipe_ev.data();            // [T] K1(t) done (aux)
   cudaEvent_t* evK2 = p.pipe_ev.data() + p.T;      // [T] K2(t) done (st)
   cudaEvent_t* evK3 = p.pipe_ev.data() + 2 * p.T;  // [T] K3(t) done (aux3)
   cudaEvent_t evFork = p.pipe_ev[3 * p.T], evJoin1 = p.pipe_ev[3 * p.T + 1], evJoin3 = p.pipe_ev[3 * p.T + 2];
   cudaEvent_t evJoin2 = p.pipe_ev[3 * p.T + 3];
-  // K2 launches alternate between the caller's stream and aux2 (DSFT_K2_STREAMS=1:
-  // all on the caller's stream): K2(k+1) depends only on K1(k+1), so its CTAs fill
-  // the SMs K2(k)'s last wave leaves idle
-  const char* k2s = getenv("DSFT_K2_STREAMS");
-  bool k2alt = !serial && !(k2s && strcmp(k2s, "1") == 0);
+  // K2 launches alternate between the caller's stream and aux2: K2(k+1) depends only
+  // on K1(k+1), so its CTAs fill the SMs K2(k)'s last wave leaves idle
+  bool k2alt = !serial;
   for (int t = 0; t < p.T; ++t)  // split-mode rows share one scratch region (Zs): one K2 at a time
     if (p.bk[t].split && !(p.bk[t].cl && p.bk[t].k2_jit)) k2alt = false;
   cudaStream_t a2 = k2alt ? p.aux2 : st;
@@ -1131,7 +1080,8 @@ static dsft_status run_bands(Plan& p, const double2* f, int64_t ld, int nv, cons
   // K1 launch per prime): Z buffer k % kZBufs, K1(k) waits for K3(k - kZBufs).
   // Grouped K1 (every prime its own Z region): one launch per group, no K3 wait.
   const WsLayout L = ws_layout(p, p.ws_batch);
-  const bool grouped = p.n_k1_groups < p.T;
+  const bool grouped = k1_grouped(p, p.ws_batch);
+  const int n_groups = grouped ? 1 : p.T;
   auto zfor = [&](int k, int t, double2*& Z, int64_t& zs) {
     if (grouped) {
       Z = (double2*)((char*)p.ws + L.z) + (int64_t)p.ws_batch * p.z_off[t];
@@ -1143,12 +1093,12 @@ static dsft_status run_bands(Plan& p, const double2* f, int64_t ld, int nv, cons
   };
   int gfirst[DSFT_MAX_T + 1], gof[DSFT_MAX_T];  // first position of group g; group of position k
   gfirst[0] = 0;
-  for (int g = 0; g < p.n_k1_groups; ++g) {
-    gfirst[g + 1] = gfirst[g] + p.k1_groups[g];
+  for (int g = 0; g < n_groups; ++g) {
+    gfirst[g + 1] = gfirst[g] + (grouped ? p.T : 1);
     for (int k = gfirst[g]; k < gfirst[g + 1]; ++k) gof[k] = g;
   }
   auto k1 = [&](int g) -> dsft_status {
-    const int k0 = gfirst[g], n = p.k1_groups[g];
+    const int k0 = gfirst[g], n = gfirst[g + 1] - gfirst[g];
     if (!grouped && k0 >= kZBufs) CU(cudaStreamWaitEvent(a1, evK3[k0 - kZBufs], 0), "K1 waits K3");
     int ts[DSFT_MAX_T], keep[DSFT_MAX_T];
     double2* Zs[DSFT_MAX_T];
@@ -1166,7 +1116,7 @@ static dsft_status run_bands(Plan& p, const double2* f, int64_t ld, int nv, cons
   if ((stt = k1(0)) != DSFT_OK) return stt;
   for (int k = 0; k < p.T; ++k) {
     const int t = p.order[k];
-    if (k == gfirst[gof[k]] && gof[k] + 1 < p.n_k1_groups && (stt = k1(gof[k] + 1)) != DSFT_OK) return stt;
+    if (k == gfirst[gof[k]] && gof[k] + 1 < n_groups && (stt = k1(gof[k] + 1)) != DSFT_OK) return stt;
     double2* Z;
     int64_t zs;
     zfor(k, t, Z, zs);
@@ -1202,15 +1152,56 @@ static dsft_status execute_impl(dsft_plan* pl, const dsft_c128* f, int64_t batch
   if (batch < 1 || ld < p.N) return fail(DSFT_ERR_ARG, "batch >= 1 and ld >= N required");
   dsft_status stt = ensure_ws(p, choose_wave(p, batch));
   if (stt != DSFT_OK) return stt;
+  if ((stt = ensure_pipe(p)) != DSFT_OK) return stt;
   cudaStream_t st = (cudaStream_t)stream;
   std::vector<int> bands(p.J);
   for (int j = 0; j < p.J; ++j) bands[j] = j;
-  for (int64_t v0 = 0; v0 < batch; v0 += p.ws_batch) {
-    const int nv = (int)std::min<int64_t>(p.ws_batch, batch - v0);
-    stt = run_bands(p, (const double2*)f + v0 * ld, ld, nv, bands.data(), p.J, st, freqs + v0 * p.s,
-                    (double2*)coeffs + v0 * p.s);
-    if (stt != DSFT_OK) return stt;
+  auto waves = [&](cudaStream_t s0) -> dsft_status {
+    for (int64_t v0 = 0; v0 < batch; v0 += p.ws_batch) {
+      const int nv = (int)std::min<int64_t>(p.ws_batch, batch - v0);
+      dsft_status r = run_bands(p, (const double2*)f + v0 * ld, ld, nv, bands.data(), p.J, s0, freqs + v0 * p.s,
+                                (double2*)coeffs + v0 * p.s);
+      if (r != DSFT_OK) return r;
+    }
+    return DSFT_OK;
+  };
+  // CUDA graph replay: the whole stream-ordered sequence (every wave,
+  // the four pipeline streams, the PDL tail) is captured once per (pointers, batch)
+  // and launched as one graph into the caller's stream -- one host call instead of
+  // ~19 launches and ~30 event operations per transform.  Per-launch timing, or
+  // DSFT_FLAG_NO_GRAPH, launches directly.
+  if (p.timing || (p.params.flags & DSFT_FLAG_NO_GRAPH)) return waves(st);
+  const GraphKey key{(const void*)f, ld, batch, (void*)freqs, (void*)coeffs, p.ws};
+  if (!p.gexec || !(key == p.gkey)) {
+    if (!p.capst) CU(cudaStreamCreateWithFlags(&p.capst, cudaStreamNonBlocking), "create capture stream");
+    CU(cudaStreamBeginCapture(p.capst, cudaStreamCaptureModeThreadLocal), "begin graph capture");
+    stt = waves(p.capst);
+    cudaGraph_t graph = nullptr;
+    const cudaError_t ce = cudaStreamEndCapture(p.capst, &graph);
+    if (stt != DSFT_OK) {
+      if (graph) cudaGraphDestroy(graph);
+      return stt;
+    }
+    CU(ce, "end graph capture");
+    bool updated = false;
+    if (p.gexec) {
+      cudaGraphExecUpdateResultInfo info;
+      updated = cudaGraphExecUpdate(p.gexec, graph, &info) == cudaSuccess;
+      if (!updated) {
+        cudaGetLastError();
+        cudaGraphExecDestroy(p.gexec);
+        p.gexec = nullptr;
+      }
+    }
+    cudaError_t ie = updated ? cudaSuccess : cudaGraphInstantiate(&p.gexec, graph, cudaGraphInstantiateFlagUseNodePriority);
+    cudaGraphDestroy(graph);
+    if (ie != cudaSuccess) {
+      p.gexec = nullptr;
+      return cuda_fail(ie, "instantiate execute graph");
+    }
+    p.gkey = key;
   }
+  CU(cudaGraphLaunch(p.gexec, st), "launch execute graph");
   return DSFT_OK;
 }
 
@@ -1234,8 +1225,7 @@ static int64_t window_bytes(const Plan& p) {
 // Device alias of f_host when K1 should read it in place over the host link
 // (page-locked, mapped; the windows cover at most half of f), else nullptr.
 static const void* host_alias(const Plan& p, const void* f_host) {
-  const char* env = getenv("DSFT_HOST_ZERO_COPY");  // "0" never, "1" whenever mapped
-  if (env && strcmp(env, "0") == 0) return nullptr;
+  if (p.params.flags & DSFT_FLAG_HOST_COPY) return nullptr;
   cudaPointerAttributes pa{};
   if (cudaPointerGetAttributes(&pa, f_host) != cudaSuccess) {
     cudaGetLastError();
@@ -1243,7 +1233,7 @@ static const void* host_alias(const Plan& p, const void* f_host) {
   }
   if (pa.type != cudaMemoryTypeHost || !pa.devicePointer) return nullptr;
   const bool sparse = 2 * window_bytes(p) <= p.N * 16;
-  return (sparse || (env && strcmp(env, "1") == 0)) ? pa.devicePointer : nullptr;
+  return (sparse || (p.params.flags & DSFT_FLAG_HOST_MAPPED)) ? pa.devicePointer : nullptr;
 }
 
 int32_t dsft_plan_host_zero_copy(const dsft_plan* pl, const dsft_c128* f_host, int64_t* h2d_bytes) {
@@ -1374,8 +1364,12 @@ dsft_status dsft_debug_copy(dsft_plan* pl, int32_t which, void* dst, size_t byte
 // ============================================================ sharded execution
 // (comm.cpp provides the NCCL handle; this part needs only the plan internals)
 namespace dsft {
+dsft_status set_error(dsft_status st, const std::string& msg) { return fail(st, msg); }
+
 dsft_status run_sharded_bands(dsft_plan* pl, const double2* f, int rank, int world, cudaStream_t st, int* nb_out) {
   Plan& p = pl->p;
+  if (world < 1 || rank < 0 || rank >= world) return fail(DSFT_ERR_ARG, "rank/world out of range");
+  if (!f) return fail(DSFT_ERR_ARG, "NULL device pointer");
   std::vector<int> bands;
   for (int j = rank; j < p.J; j += world) bands.push_back(j);
   *nb_out = (int)bands.size();
@@ -1386,5 +1380,56 @@ dsft_status run_sharded_bands(dsft_plan* pl, const double2* f, int rank, int wor
   CU(cudaMemsetAsync((char*)p.ws + L.band_nz, 0, (size_t)L.bn_vec * 4, st), "zero band counts");
   if (bands.empty()) return DSFT_OK;
   return run_bands(p, f, p.N, 1, bands.data(), (int)bands.size(), st);
+}
+}  // namespace dsft
+
+// ---- the two halves of dsft_execute_sharded (comm.cpp), as ABI entry points
+extern "C" {
+
+int64_t dsft_shard_block_entries(const dsft_plan* pl, int32_t world) {
+  if (!pl || world < 1) return 0;
+  return (int64_t)((pl->p.J + world - 1) / world) * pl->p.info.band_budget;
+}
+
+dsft_status dsft_execute_sharded_local(dsft_plan* pl, int32_t rank, int32_t world, const dsft_c128* f_dev,
+                                       int64_t* w_out, dsft_c128* c_out, double* m_out, int32_t* nz_out,
+                                       void* stream) {
+  if (!pl || !w_out || !c_out || !m_out || !nz_out) return fail(DSFT_ERR_ARG, "NULL argument");
+  Plan& p = pl->p;
+  cudaStream_t st = (cudaStream_t)stream;
+  int nb = 0;
+  dsft_status stt = run_sharded_bands(pl, (const double2*)f_dev, rank, world, st, &nb);
+  if (stt != DSFT_OK) return stt;
+  const int nbmax = (p.J + world - 1) / world;
+  const int64_t ent = (int64_t)nbmax * p.info.band_budget;
+  const WsLayout L = ws_layout(p, p.ws_batch);
+  const char* ws = (const char*)p.ws;
+  CU(cudaMemcpyAsync(w_out, ws + L.band_w, (size_t)ent * 8, cudaMemcpyDeviceToDevice, st), "copy band omegas");
+  CU(cudaMemcpyAsync(c_out, ws + L.band_c, (size_t)ent * 16, cudaMemcpyDeviceToDevice, st), "copy band coeffs");
+  CU(cudaMemcpyAsync(m_out, ws + L.band_m, (size_t)ent * 8, cudaMemcpyDeviceToDevice, st), "copy band keys");
+  CU(cudaMemcpyAsync(nz_out, ws + L.band_nz, (size_t)nbmax * 4, cudaMemcpyDeviceToDevice, st), "copy band counts");
+  return DSFT_OK;
+}
+
+dsft_status dsft_merge_sharded(dsft_plan* pl, int32_t world, const int64_t* w_all, const dsft_c128* c_all,
+                               const double* m_all, const int32_t* nz_all, int64_t* freqs_out, dsft_c128* coeffs_out,
+                               void* stream) {
+  if (!pl || world < 1 || !w_all || !c_all || !m_all || !nz_all || !freqs_out || !coeffs_out)
+    return fail(DSFT_ERR_ARG, "NULL argument or world < 1");
+  Plan& p = pl->p;
+  const int nbmax = (p.J + world - 1) / world;
+  // gathered layout [world][nbmax][budget]: world * nbmax sorted band blocks of one vector
+  CU(launch_k6_blocks(w_all, (const double2*)c_all, m_all, nz_all, world * nbmax, p.info.band_budget, 0, 0, p.s, 1,
+                      freqs_out, (double2*)coeffs_out, (cudaStream_t)stream),
+     "K6 merge launch");
+  return DSFT_OK;
+}
+
+}  // extern "C"
+
+namespace dsft {
+dsft_status execute_batched_impl(dsft_plan* pl, const double2* f, int64_t batch, int64_t ld, int64_t* freqs,
+                                 double2* coeffs, cudaStream_t st) {
+  return execute_impl(pl, (const dsft_c128*)f, batch, ld, freqs, (dsft_c128*)coeffs, (void*)st);
 }
 }  // namespace dsft

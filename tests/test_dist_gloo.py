@@ -1,9 +1,14 @@
-"""Multi-process (world size 2, gloo, CPU) test of the band-sharded protocol of
+"""Multi-process (world size 2, gloo, CPU) test of the band-sharded PROTOCOL of
 dsft_execute_sharded: the band partition comes from the library's
-host function dsft_shard_bands; each rank computes its bands (the oracle stands
-in for K1-K5 on CPU), packs fixed-capacity per-band blocks padded with the
-sentinel, all_gathers them, and merges.  The merged result must be identical to
-the single-process transform on every rank."""
+host function dsft_shard_bands; each rank computes its bands with the oracle
+standing in for K1-K5 (there is no GPU here), packs fixed-capacity per-band blocks
+padded with the sentinel, all_gathers them, and merges.  The merged result must be
+identical to the single-process transform on every rank.
+
+The library's own sharded code (dsft_execute_sharded_local -> rank-major gather
+layout -> dsft_merge_sharded, the halves of dsft_execute_sharded) is driven on the
+GPU by tests/test_gpu_parity.py::test_sharded_virtual_ranks_equal_execute (R
+virtual ranks on one GPU, bitwise against dsft_execute)."""
 
 import os
 import socket

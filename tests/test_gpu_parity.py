@@ -222,15 +222,13 @@ def test_host_path_equals_device_path():
 
 
 @pytest.mark.parametrize("mode", ["zero_copy", "copy_pinned", "copy_pageable"])
-def test_host_path_modes_equal_device_path(mode, monkeypatch):
+def test_host_path_modes_equal_device_path(mode):
     """dsft_execute_host reads a sparse-sampled pinned f in place (zero copy), copies
     pageable memory, and gives bitwise the device path's result in every mode."""
     N, s = 2**22, 50  # BASELINE config 1: windows cover ~2 % of f
     pl = planted(N, s, cfg=36, trial=0)
-    plan = d.Plan(N, s)
+    plan = d.Plan(N, s, d.make_params(flags=d.FLAG_HOST_COPY if mode == "copy_pinned" else 0))
     f1, c1 = run_gpu(plan, pl.f)
-    if mode == "copy_pinned":
-        monkeypatch.setenv("DSFT_HOST_ZERO_COPY", "0")
     fh = torch.from_numpy(pl.f.copy())
     if mode != "copy_pageable":
         fh = fh.pin_memory()
@@ -244,11 +242,9 @@ def test_host_path_modes_equal_device_path(mode, monkeypatch):
     assert np.array_equal(frh.numpy(), f1) and np.array_equal(coh.numpy(), c1)
 
 
-def test_k2_specialised_equals_runtime_radix(monkeypatch):
+def test_k2_specialised_equals_runtime_radix():
     """The plan-time NVRTC specialisation of K2 and the runtime-radix kernel run the
     same passes in the same arithmetic order: outputs bitwise identical."""
-    if os.environ.get("DSFT_JIT") == "0":
-        pytest.skip("NVRTC specialisation disabled by DSFT_JIT=0 in the environment")
     N, s = 2**20, 300  # bucket primes in [1200, 2400): runtime-radix <256,2> rows -> specialised
     pl = planted(N, s, cfg=38, trial=0)
     plan = d.Plan(N, s)
@@ -256,8 +252,7 @@ def test_k2_specialised_equals_runtime_radix(monkeypatch):
     big = sum(1 for P in plan.primes() if P - 1 > 1200)  # rows of the <64,8> instantiation stay generic
     assert nspec == big and big >= 1 and why == "", why
     a = run_gpu(plan, pl.f)
-    monkeypatch.setenv("DSFT_JIT", "0")
-    plan0 = d.Plan(N, s)
+    plan0 = d.Plan(N, s, d.make_params(flags=d.FLAG_NO_JIT))
     assert plan0.dsft_plan_k2_specialized()[0] == 0
     b = run_gpu(plan0, pl.f)
     assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
@@ -329,14 +324,13 @@ def test_deterministic_variant_headline_size():
 
 
 @pytest.mark.parametrize("N,s,cfg,trial", [(2**20, 2000, 2, 0), (2**21, 4000, 2, 1)])
-def test_split_mode_fallback(N, s, cfg, trial, monkeypatch):
+def test_split_mode_fallback(N, s, cfg, trial):
     """Rows above one CTA's shared memory run the thread-block-cluster K2 by default;
-    DSFT_K2_CLUSTER=0 selects the two-launch split mode (the fallback when the
+    DSFT_FLAG_NO_CLUSTER selects the two-launch split mode (the fallback when the
     cluster kernel is unavailable): same oracle parity."""
-    monkeypatch.setenv("DSFT_K2_CLUSTER", "0")
     pl = planted(N, s, cfg=cfg, trial=trial)
     ref = dsft(pl.f, s, OracleParams(seed=trial))
-    plan = d.Plan(N, s, d.make_params(seed=trial))
+    plan = d.Plan(N, s, d.make_params(seed=trial, flags=d.FLAG_NO_CLUSTER))
     assert plan.launches_per_execute() > 4 + 3 * plan.info.T  # K2a + K2b launches
     assert_parity(run_gpu(plan, pl.f), ref, s)
 
@@ -358,3 +352,191 @@ def test_band_budget_and_edge_tones_parity():
                 assert sorted(ref.freqs.tolist()) == freqs
             else:
                 assert q[9] not in ref.freqs.tolist() and q[9] + 30 in ref.freqs.tolist()
+
+
+# ------------------------------------------------------------------ multi-GPU protocol
+@pytest.mark.parametrize("world", [2, 3, 4, 16])
+def test_sharded_virtual_ranks_equal_execute(world):
+    """The band-sharded protocol of dsft_execute_sharded driven through the library on
+    one GPU ("virtual ranks"): dsft_execute_sharded_local for ranks 0..R-1
+    (each rank's bands j = rank mod R, K1..K5) writes its blocks into its slot of the
+    rank-major gather layout, exactly what ncclAllGather produces, and
+    dsft_merge_sharded (K6 over the gathered blocks) must equal dsft_execute bitwise.
+    J = 15 is not divisible by 2 or 4 (ranks with a zeroed tail block); R = 16 > J
+    leaves one rank without bands."""
+    N, s = 2**16, 50
+    pl = planted(N, s, cfg=37, trial=world)
+    plan = d.Plan(N, s)
+    ref = run_gpu(plan, pl.f)
+    f = to_dev(pl.f)
+    n = plan.dsft_shard_block_entries(world)
+    nb = n // plan.info.band_budget
+    assert nb == -(-plan.info.J // world)
+    w = torch.full((world, n), 7, dtype=torch.int64, device=DEV)
+    c = torch.full((world, n), 3 + 1j, dtype=torch.complex128, device=DEV)
+    m = torch.full((world, n), 5.0, dtype=torch.float64, device=DEV)
+    z = torch.full((world, nb), 99, dtype=torch.int32, device=DEV)
+    for r in range(world):
+        plan.dsft_execute_sharded_local(r, world, f, w[r], c[r], m[r], z[r])
+        assert int(z[r].sum().item()) <= nb * plan.info.band_budget
+    fr = torch.empty(s, dtype=torch.int64, device=DEV)
+    co = torch.empty(s, dtype=torch.complex128, device=DEV)
+    plan.dsft_merge_sharded(world, w, c, m, z, fr, co)
+    torch.cuda.synchronize()
+    assert np.array_equal(fr.cpu().numpy(), ref[0]) and np.array_equal(co.cpu().numpy(), ref[1])
+    if world == 16:
+        assert int(z[15].sum().item()) == 0  # rank 15 owns no band
+
+
+def test_batched_sharded_world1_and_comm_wait():
+    """dsft_execute_batched_sharded at world 1 (NCCL communicator, no peer) equals the
+    batched execute, and dsft_comm_wait returns once the stream is idle."""
+    N, s, B = 4096, 8, 6
+    fs = np.stack([planted(N, s, cfg=34, trial=1, vector=v).f for v in range(B)])
+    plan = d.Plan(N, s)
+    fdev = to_dev(fs.reshape(-1))
+    fr = torch.empty(B * s, dtype=torch.int64, device=DEV)
+    co = torch.empty(B * s, dtype=torch.complex128, device=DEV)
+    plan.dsft_execute_batched(fdev, B, N, fr, co)
+    try:
+        comm = d.Comm(0, 1, d.Comm.unique_id())
+    except d.DsftError as e:  # NCCL unavailable on this box
+        pytest.skip(str(e))
+    fr2 = torch.empty_like(fr)
+    co2 = torch.empty_like(co)
+    plan.dsft_execute_batched_sharded(comm, fdev, B, N, fr2, co2)
+    comm.wait(timeout_ms=60_000)
+    torch.cuda.synchronize()
+    assert torch.equal(fr, fr2) and torch.equal(co, co2)
+    comm.close()
+
+
+def test_binding_rejects_bad_tensors():
+    """The binding checks dtype / contiguity / device / size before a pointer crosses
+    the ABI (no silent out-of-bounds access)."""
+    plan = d.Plan(4096, 8)
+    f = torch.zeros(4096, dtype=torch.complex128, device=DEV)
+    fr = torch.empty(8, dtype=torch.int64, device=DEV)
+    co = torch.empty(8, dtype=torch.complex128, device=DEV)
+    for bad in (f.to(torch.complex64), f[:4000], f.cpu(), torch.zeros(8192, dtype=torch.complex128, device=DEV)[::2]):
+        with pytest.raises(d.DsftError):
+            plan.dsft_execute(bad, fr, co)
+    with pytest.raises(d.DsftError):
+        plan.dsft_execute(f, fr[:4], co)
+
+
+# ------------------------------------------------------------- any length N >= 2^31
+class LazyPlanted:
+    """f_j = sum_omega c_omega exp(2 pi i omega j / N) evaluated on demand for the
+    oracle (no 32 GiB host array): the same formula as the device synthesis below."""
+
+    def __init__(self, N, freqs, c):
+        self.N, self.freqs, self.c = N, np.asarray(freqs, dtype=np.int64), np.asarray(c)
+        self.shape = (N,)
+
+    def __getitem__(self, idx):
+        idx = np.asarray(idx, dtype=np.int64)
+        out = np.zeros(idx.shape, dtype=np.complex128)
+        for om, cc in zip(self.freqs, self.c):
+            out += cc * np.exp(2j * math.pi * ((om * idx) % self.N) / self.N)
+        return out
+
+
+def test_length_above_2_31():
+    """Any length N: N = 2^31 + 11 (32 GiB of complex128; K1's window
+    indices no longer fit 32 bits).  f is synthesised on the device from 8 planted tones
+    (torch, exact int64 phase reduction); the oracle evaluates the same formula lazily
+    at the entries its windows read.  Support exact against the planted spectrum,
+    end-to-end oracle parity, and K1's filtered samples of one band element-wise."""
+    N, s = 2**31 + 11, 8
+    free, _ = torch.cuda.mem_get_info()
+    if free < N * 16 + (4 << 30):
+        pytest.skip("needs ~36 GB of free device memory")
+    rng = np.random.default_rng(2031)
+    freqs = np.sort(rng.choice(N, s, replace=False).astype(np.int64) - (N + 1) // 2 + 1)
+    c = np.exp(2j * math.pi * rng.random(s))
+    f = torch.zeros(N, dtype=torch.complex128, device=DEV)
+    chunk = 1 << 27
+    for a in range(0, N, chunk):
+        j = torch.arange(a, min(N, a + chunk), dtype=torch.int64, device=DEV)
+        for om, cc in zip(freqs.tolist(), c.tolist()):
+            ph = ((om * j) % N).to(torch.float64) * (2 * math.pi / N)
+            f[a:a + j.numel()] += cc * torch.exp(1j * ph)
+        del j
+    lazy = LazyPlanted(N, freqs, c)
+    op = derive_plan(N, s, OracleParams(seed=5))
+    plan = d.Plan(N, s, d.make_params(seed=5))
+    assert plan.primes() == op.primes
+    fr = torch.empty(s, dtype=torch.int64, device=DEV)
+    co = torch.empty(s, dtype=torch.complex128, device=DEV)
+    plan.dsft_execute(f, fr, co)
+    torch.cuda.synchronize()
+    gpu = (fr.cpu().numpy(), co.cpu().numpy())
+    assert sorted(gpu[0].tolist()) == freqs.tolist()
+    ref = dsft(lazy, s, plan=op)
+    assert_parity(gpu, ref, s)
+    band = op.J // 2
+    for t in (0, op.T - 1):
+        i = len(op.residues[t]) - 1
+        L = op.primes[t] * op.residues[t][i]
+        out = torch.empty(L, dtype=torch.complex128, device=DEV)
+        plan.dsft_debug_grid(f, band, t, i, 0, out)
+        h_ref = filtered_samples(lazy, op, op.q[band], L)
+        h = out.cpu().numpy()
+        assert np.max(np.abs(h - h_ref)) <= 1e-12 * max(1.0, np.max(np.abs(h_ref)))
+    del f
+    torch.cuda.empty_cache()
+
+
+# ----------------------------------------------------------- THM4 (kappa = O(log N))
+@pytest.mark.parametrize("N,s,r", [(2**22, 50, 1.0), (2**18, 20, 2.0)])
+def test_thm4_parity_large_kappa(N, s, r):
+    """The guaranteed preset (Theorem 4) at kappa = 22 (N = 2^22,
+    J = 40) and kappa = 35 > 31 (r = 2): the generic-kappa K1 element-wise against O2
+    on the first and last band, and end-to-end parity."""
+    kw = dict(preset="thm4", r=r, seed=1)
+    op = derive_plan(N, s, OracleParams(**kw))
+    plan = d.Plan(N, s, d.make_params(**kw))
+    assert plan.info.kappa == op.kappa and plan.info.J == op.J
+    pl = planted(N, s, cfg=42, trial=int(r))
+    f = to_dev(pl.f)
+    for band in (0, op.J - 1):
+        for t in (0, op.T - 1):
+            i = len(op.residues[t]) - 1
+            L = op.primes[t] * op.residues[t][i]
+            out = torch.empty(L, dtype=torch.complex128, device=DEV)
+            plan.dsft_debug_grid(f, band, t, i, 0, out)
+            h_ref = filtered_samples(pl.f, op, op.q[band], L)
+            assert np.max(np.abs(out.cpu().numpy() - h_ref)) <= 1e-13 * max(1.0, np.max(np.abs(h_ref)))
+    ref = dsft(pl.f, s, OracleParams(**kw))
+    assert_parity(run_gpu(plan, pl.f), ref, s)
+    assert sorted(ref.freqs.tolist()) == pl.freqs.tolist()
+
+
+@pytest.mark.parametrize("N", [4096, 2**20])
+def test_theorem5_tail_bound_gpu(N):
+    """Theorem 5 on the GPU path, THM4 r = 2 (SPEC.md:462 setup:
+    16 unit heads + 48 tail entries of magnitude 0.01): ||fhat - v||_2 <=
+    ||fhat - fhat_s^opt||_2 + 33/sqrt(s) ||fhat - fhat_s^opt||_1 + 198 sqrt(s) ||f||_inf N^-r,
+    and parity with the oracle."""
+    from dsft_synth import planted_with_tail
+    s, tail = 16, 48
+    kw = dict(preset="thm4", r=2.0, seed=3)
+    plan = d.Plan(N, s, d.make_params(**kw))
+    for trial in range(2):
+        pl = planted_with_tail(N, s, tail, 0.01, cfg=18, trial=trial)
+        fr, co = run_gpu(plan, pl.f)
+        ref = dsft(pl.f, s, OracleParams(**kw))
+        assert_parity((fr, co), ref, s)
+        dense = dict(zip(pl.freqs.tolist(), pl.fhat))
+        mags = sorted(((abs(v), w) for w, v in dense.items()), key=lambda p: (-p[0], p[1]))
+        head = {w for _, w in mags[:s]}
+        tail_v = np.array([dense[w] for w in dense if w not in head])
+        valid = fr != SENTINEL
+        v = dict(zip(fr[valid].tolist(), co[valid]))
+        diff = [dense.get(w, 0) - v.get(w, 0) for w in set(dense) | set(v)]
+        lhs = np.linalg.norm(diff)
+        rhs = (np.linalg.norm(tail_v) + 33 / math.sqrt(s) * np.sum(np.abs(tail_v))
+               + 198 * math.sqrt(s) * np.max(np.abs(pl.f)) * N ** -2.0)
+        assert lhs <= rhs, (lhs, rhs)
+        assert head <= set(v)  # the 16 heads are recovered
