@@ -340,6 +340,23 @@ def run_ours(a):
         band = {"value": 1.0 / (bms / 1e3), "unit": UNIT, "ms_per_step": bms, "scaling": "strong",
                 "path": "dsft_execute_sharded: one vector, bands j = rank mod N, one NCCL allgather of band blocks"}
 
+    # ---- the other bucket-prime pool (reading R6) on the same vector, same protocol
+    other_pool = None
+    if world == 1 and mode == "single" and a.pool is None:
+        op_ = "full" if pool == "smooth" else "smooth"
+        plan2 = d.Plan(N, s, d.make_params(seed=a.seed, pool_rule=op_))
+        for _ in range(a.warmup):
+            step(plan2, f, "single")
+        torch.cuda.synchronize()
+        fr2 = freqs[:s].cpu().numpy()
+        oms = timed_loop(max(10, a.steps // 2), md="single", p=plan2)
+        other_pool = {"pool": op_, "value": 1.0 / (oms / 1e3), "unit": UNIT, "ms_per_step": oms,
+                      "primes": list(plan2.info.primes[:plan2.info.T]),
+                      "support_exact": sorted(fr2[fr2 != d.SENTINEL].tolist()) == pl.freqs.tolist(),
+                      "note": "full = every prime in [4s, 8s) (general primes: zero-padded Rader, FFT length "
+                              ">= 2(P-1)-1); smooth = primes with 13-smooth P-1 (DESIGN.md R6)"}
+        plan2.close()
+
     # ---- kernel breakdown: a second pass with per-launch CUDA events on each launch's stream
     plan.dsft_plan_set_timing(True)
     kpass = max(10, min(a.steps, 50))
@@ -486,6 +503,7 @@ def run_ours(a):
         "filtered_samples_per_s": units * info.J * info.nodes / (ms / 1e3),
         "support_exact": bool(support_exact),
         "band_sharded": band,
+        "other_pool": other_pool,
         "e2e": e2e,
         "cpu_baseline": cpu,
         "clocks": clocks,

@@ -39,7 +39,9 @@ constexpr int64_t kMaxWave = 4096;  // vectors processed concurrently by one bat
 #endif
 constexpr int kZBufs = DSFT_ZBUFS;        // Z buffers the bucket-prime pipeline rotates through (3: measured worse, L2)
 constexpr int kMaxRadix = 16;    // largest in-register FFT stage radix in K2
-constexpr double kK1OneLaunchBytes = 24.0e6;  // all primes' Z below this: one K1 launch (plan.cpp choose_order)
+constexpr int kMultiMaxT = 12;   // bucket primes of one-launch K2 / K3 (small plans; kernel-parameter limit)
+constexpr int64_t kTailMergeMaxS = 256;  // the fused small-plan tail merges in its last CTA up to this s
+constexpr double kK1OneLaunchBytes = 48.0e6;  // all primes' Z below this: one K1 launch (plan.cpp choose_order)
 
 // Per-bucket-prime tables (host copy + device pointers into plan->dev_tables).
 struct Bucket {
@@ -53,8 +55,12 @@ struct Bucket {
   int64_t off = 0;           // sum_{t'<t} P_t'
   int64_t crtM = 0;          // P * prod r
   int64_t crtE[DSFT_MAX_K + 1] = {};  // CRT coefficients for moduli (P, r_0, ...)
-  // Rader / FFT of length M = P - 1
+  // Rader: cyclic convolution of length Mv = P - 1, evaluated by FFTs of length M
+  // (M = Mv when P - 1 is 13-smooth; else pad: a 13-smooth M >= 2 Mv - 1, zero-padded
+  // input, natural-order rows)
   int M = 0;
+  int Mv = 0;
+  bool pad = false;
   int g = 0;                 // primitive root mod P
   int nfac = 0;
   int fac[kMaxFac] = {};
@@ -158,7 +164,9 @@ struct WsLayout {
       band_z, band_m, band_n, band_nz, total;
   int64_t z_vec;     // complex128 elements per vector in Z:        J * max_t S_t P_t
   int64_t z_buf;     // elements per Z buffer (nvec * z_vec); kZBufs buffers (prime t uses t % kZBufs)
-  // zs: K2 split-mode scratch (one Z buffer, only when some bucket prime is split)
+  // zs: K2 split-mode scratch (only when some bucket prime is split): per vector
+  // J * Smax rows of zs_row >= M + 1 elements (padded rows are longer than P)
+  int64_t zs_row, zs_vec;
   int64_t cw_vec;    // elements per vector in cand_w / acc_w / acc_z: J * sum_t P_t
   int64_t band_vec;  // elements per vector in band_w / band_c / band_z: J * budget
   int64_t bn_vec;    // elements per vector in band_n: J
@@ -182,7 +190,15 @@ cudaError_t launch_k3(const Plan& p, int t, const double2* Z, int64_t zstride, i
 // K4..K6 in one cooperative launch; freqs == nullptr: no merge (sharded path merges
 // after the allgather with launch_k6_blocks)
 cudaError_t launch_k45(const Plan& p, int nvec, void* ws, const int* band_list, int nbands, cudaStream_t st,
-                       int64_t* freqs, double2* coeffs);
+                       int64_t* freqs, double2* coeffs, bool probe = false);
+// small plans (plan.cpp run_bands, grouped K1): every bucket prime in one K2 launch
+// (k2_multi_ok: all on the runtime <64,8> rows) and one K3 launch (candidates only;
+// the vote is counted by K5s, launch_k45(probe = true))
+bool k2_multi_ok(const Plan& p);
+cudaError_t launch_k2_multi(const Plan& p, int n, const int* ts, double2* const* Zs, const int64_t* zst, int nvec,
+                            void* ws, int nbands, cudaStream_t st);
+cudaError_t launch_k3_multi(const Plan& p, int n, const int* ts, double2* const* Zs, const int64_t* zst, int nvec,
+                            void* ws, const int* bands, int nbands, cudaStream_t st);
 cudaError_t launch_k6(const Plan& p, int nvec, void* ws, int64_t* freqs, double2* coeffs,
                       cudaStream_t st);
 cudaError_t launch_debug_grid(const Plan& p, int t, const double2* Z, int i, int band, int what, double2* out,

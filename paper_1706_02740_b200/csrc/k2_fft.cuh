@@ -13,7 +13,10 @@ namespace dsft {
 struct K2Params {
   double2* Z;
   int64_t z_vec_stride;
-  int P, M, nfac, t;     // t: bucket-prime index (trace builds only)
+  int P, M, nfac, t;     // M: FFT length; t: bucket-prime index (trace builds only)
+  int Mv;                // valid Rader length P - 1 (< M for zero-padded rows; x0 at row[Mv])
+  int zs_row;            // split mode: scratch row stride (elements, >= M + 1)
+  int64_t zs_vec;        // split mode: scratch elements per vector
   int fac[kMaxFac];
   int toff[kMaxFac];
   int S, sig0, nsig, band0;  // rows of this launch: bands band0 + blockIdx.x / nsig, shifts sig0 + blockIdx.x % nsig
@@ -28,9 +31,11 @@ __device__ __forceinline__ int k2_row(const K2Params& p, int b) {
   return (p.band0 + bl) * p.S + p.sig0 + (b - bl * p.nsig);
 }
 
-// TW = false: a stage that ends its Good-Thomas dimension (twiddles all 1, skipped)
-template <int NT, int M, int N, int R, bool GSRC, bool TW = true>
-__device__ __forceinline__ void dif_ct(const double2* __restrict__ src, double2* s, const double2* __restrict__ tw) {
+// TW = false: a stage that ends its Good-Thomas dimension (twiddles all 1, skipped);
+// PADV: zero-padded row (global reads at index >= mv return 0)
+template <int NT, int M, int N, int R, bool GSRC, bool TW = true, bool PADV = false>
+__device__ __forceinline__ void dif_ct(const double2* __restrict__ src, double2* s, const double2* __restrict__ tw,
+                                       int mv = M) {
   constexpr int m = N / R, nbf = M / R, iters = (nbf + NT - 1) / NT;
 #pragma unroll
   for (int it = 0; it < iters; ++it) {
@@ -41,7 +46,9 @@ __device__ __forceinline__ void dif_ct(const double2* __restrict__ src, double2*
       const int base = blk * N + k;
       double2 v[R];
 #pragma unroll
-      for (int r = 0; r < R; ++r) v[r] = GSRC ? ldcg2(src + base + r * m) : s[base + r * m];
+      for (int r = 0; r < R; ++r)
+        v[r] = GSRC ? ((!PADV || base + r * m < mv) ? ldcg2(src + base + r * m) : make_double2(0.0, 0.0))
+                    : s[base + r * m];
       dft<R>(v);
       if constexpr (!TW) {
 #pragma unroll
@@ -66,8 +73,9 @@ __device__ __forceinline__ void dif_ct(const double2* __restrict__ src, double2*
   }
 }
 
-template <int NT, int M, int N, int R, bool GDST, bool TW = true>
-__device__ __forceinline__ void dit_ct(double2* s, double2* __restrict__ dst, const double2* __restrict__ tw, double2 x0) {
+template <int NT, int M, int N, int R, bool GDST, bool TW = true, bool PADV = false>
+__device__ __forceinline__ void dit_ct(double2* s, double2* __restrict__ dst, const double2* __restrict__ tw, double2 x0,
+                                       int mv = M) {
   constexpr int m = N / R, nbf = M / R, iters = (nbf + NT - 1) / NT;
   const uint64_t pol = l2_evict_last();
 #pragma unroll
@@ -96,8 +104,11 @@ __device__ __forceinline__ void dit_ct(double2* s, double2* __restrict__ dst, co
       dft<R>(v);
 #pragma unroll
       for (int c = 0; c < R; ++c) {
-        if (GDST) st_keep(dst + base + c * m, cadd(x0, cconj(v[c])), pol);
-        else s[base + c * m] = v[c];
+        if (GDST) {
+          if (!PADV || base + c * m < mv) st_keep(dst + base + c * m, cadd(x0, cconj(v[c])), pol);
+        } else {
+          s[base + c * m] = v[c];
+        }
       }
     }
   }
@@ -182,34 +193,38 @@ __device__ __forceinline__ void dit_mid(double2* sm, const K2Params& p, double2 
 }
 
 // NT threads, MINB CTAs per SM (register cap 65536 / (NT MINB)), radices Rs...;
-// TWF: twiddle-free stages (bit i: stage i ends its Good-Thomas dimension)
+// TWF: twiddle-free stages (bit i: stage i ends its Good-Thomas dimension); bit 31:
+// zero-padded row (general bucket prime: FFT length M >= 2 (P - 1) - 1, the P - 1
+// valid samples first, x0 at row[P - 1])
 template <int NT, int MINB, unsigned TWF, int... Rs>
 __global__ void __launch_bounds__(NT) __maxnreg__(((65536 / (NT * MINB)) & ~7) > 255 ? 255 : ((65536 / (NT * MINB)) & ~7))
     k2_ct(const __grid_constant__ K2Params p) {
   using L = RadixList<Rs...>;
   constexpr int M = L::M, F = L::F;
+  constexpr bool PADV = (TWF >> 31) & 1u;
+  const int Mv = PADV ? p.Mv : M;
   extern __shared__ double2 sm[];
   __shared__ double2 sX0;
   double2* row = p.Z + (int64_t)blockIdx.y * p.z_vec_stride + (int64_t)k2_row(p, blockIdx.x) * p.P;
-  const double2 x0 = ldcg2(row + M);
+  const double2 x0 = ldcg2(row + Mv);
   if constexpr (F == 1) {
-    for (int i = threadIdx.x; i < M; i += NT) sm[i] = ldcg2(row + i);
+    for (int i = threadIdx.x; i < M; i += NT) sm[i] = i < Mv ? ldcg2(row + i) : make_double2(0.0, 0.0);
     __syncthreads();
     turn_ct<NT, M, L::R[0]>(sm, p.bhat, &sX0);
     __syncthreads();
     const uint64_t pol = l2_evict_last();
-    for (int i = threadIdx.x; i < M; i += NT) st_keep(row + i, cadd(x0, cconj(sm[i])), pol);
+    for (int i = threadIdx.x; i < Mv; i += NT) st_keep(row + i, cadd(x0, cconj(sm[i])), pol);
   } else {
     constexpr bool tw0 = !(TWF & 1u);
-    dif_ct<NT, M, M, L::R[0], true, tw0>(row, sm, p.tw + p.toff[0]);
+    dif_ct<NT, M, M, L::R[0], true, tw0, PADV>(row, sm, p.tw + p.toff[0], Mv);
     __syncthreads();
-    dif_mid<NT, L, 1, TWF>(sm, p);
+    dif_mid<NT, L, 1, TWF & 0x7fffffffu>(sm, p);
     turn_ct<NT, M, L::R[F - 1]>(sm, p.bhat, &sX0);
     __syncthreads();
-    dit_mid<NT, L, F - 2, TWF>(sm, p, x0);
-    dit_ct<NT, M, M, L::R[0], true, tw0>(sm, row, p.tw + p.toff[0], x0);
+    dit_mid<NT, L, F - 2, TWF & 0x7fffffffu>(sm, p, x0);
+    dit_ct<NT, M, M, L::R[0], true, tw0, PADV>(sm, row, p.tw + p.toff[0], x0, Mv);
   }
-  if (threadIdx.x == 0) row[M] = cadd(x0, sX0);  // X[0] = x0 + sum_q a_q
+  if (threadIdx.x == 0) row[Mv] = cadd(x0, sX0);  // X[0] = x0 + sum_q a_q
 }
 
 // ------------------------------------------------------------ cluster mode
@@ -276,9 +291,10 @@ __global__ void __launch_bounds__(NT) __maxnreg__(((65536 / (NT * MINB)) & ~7) >
   extern __shared__ double2 sm[];
   __shared__ double2 sX0;
   const int c = (int)cl_rank();
+  const int Mv = p.Mv;  // valid samples (< M for a zero-padded row); x0 at row[Mv]
   double2* row = p.Z + (int64_t)blockIdx.y * p.z_vec_stride + (int64_t)k2_row(p, blockIdx.x / C) * p.P;
-  const double2 x0 = ldcg2(row + M);
-  for (int i = threadIdx.x; i < Ms; i += NT) sm[i] = ldcg2(row + c * Ms + i);
+  const double2 x0 = ldcg2(row + Mv);
+  for (int i = threadIdx.x; i < Ms; i += NT) sm[i] = c * Ms + i < Mv ? ldcg2(row + c * Ms + i) : make_double2(0.0, 0.0);
   unsigned rb[C];  // DSMEM address of element 0 of every block
   const unsigned me = smem_u32(sm);
 #pragma unroll
@@ -322,9 +338,10 @@ __global__ void __launch_bounds__(NT) __maxnreg__(((65536 / (NT * MINB)) & ~7) >
     }
     dft<C>(v);
 #pragma unroll
-    for (int r = 0; r < C; ++r) st_keep(row + r * Ms + k, cadd(x0, cconj(v[r])), pol);
+    for (int r = 0; r < C; ++r)
+      if (r * Ms + k < Mv) st_keep(row + r * Ms + k, cadd(x0, cconj(v[r])), pol);
   }
-  if (c == 0 && threadIdx.x == 0) row[M] = cadd(x0, sX0);  // X[0] = x0 + sum_q a_q
+  if (c == 0 && threadIdx.x == 0) row[Mv] = cadd(x0, sX0);  // X[0] = x0 + sum_q a_q
   cl_sync();  // keep this CTA's shared memory alive until the cluster is done with it
 }
 

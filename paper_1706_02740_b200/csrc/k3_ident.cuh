@@ -42,6 +42,7 @@ struct K3Params {
   int prev[kK3MaxT];   // ... in processing order
   int64_t Pt[kK3MaxT], offt[kK3MaxT];  // all bucket primes and their slot offsets
   uint64_t* vmask;        // [vec][band][sum_t P_t] vote mask per candidate slot (reading R9)
+  int defer_vote;         // 1: candidates only; K5s counts the votes by probing (one-launch K3)
 };
 
 template <int R>
@@ -83,9 +84,8 @@ __device__ __forceinline__ void k3_res(const K3Params& p, int64_t P, const doubl
 // primes as compile-time constants (plan-common tuples; empty = runtime path)
 // PC > 0: the bucket prime as a constant (plan-time kernels), 0: p.P
 template <int RMAX, int PC, int... Rs>
-__global__ void __launch_bounds__(256, sizeof...(Rs) > 0 ? 2 : 1) k3_identify(const __grid_constant__ K3Params p) {
+__device__ __forceinline__ void k3_body(const K3Params& p, int64_t gid) {
   const int64_t P = PC > 0 ? (int64_t)PC : p.P;
-  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (gid >= (int64_t)p.nb * P) return;
   const int v = blockIdx.y;
   const int jl = (int)(gid / P);
@@ -140,6 +140,7 @@ __global__ void __launch_bounds__(256, sizeof...(Rs) > 0 ? 2 : 1) k3_identify(co
     // that produced it; K3 of every later producing prime ORs its bit into that
     // mask (K3 launches are sequential, so the earlier primes' candidates are final
     // here).  The accepted set and the masks do not depend on the order.
+    if (p.defer_vote) return;  // one-launch K3: K5s counts the votes by probing
     const int64_t bb = (int64_t)v * p.cw_vec_stride + (int64_t)j * p.sumP;
     int t0 = p.t;
     for (int k = 0; k < p.nprev; ++k) {
@@ -152,7 +153,12 @@ __global__ void __launch_bounds__(256, sizeof...(Rs) > 0 ? 2 : 1) k3_identify(co
     if (t0 == p.t) mk = 1ull << p.t;
     else atomicOr((unsigned long long*)(p.vmask + bb + p.offt[t0] + pmod(om, p.Pt[t0])), 1ull << p.t);
   }
-  p.vmask[slot] = mk;  // this prime's slots: written only here, OR-ed only by later K3s
+  if (!p.defer_vote) p.vmask[slot] = mk;  // this prime's slots: written only here, OR-ed only by later K3s
+}
+
+template <int RMAX, int PC, int... Rs>
+__global__ void __launch_bounds__(256, sizeof...(Rs) > 0 ? 2 : 1) k3_identify(const __grid_constant__ K3Params p) {
+  k3_body<RMAX, PC, Rs...>(p, (int64_t)blockIdx.x * blockDim.x + threadIdx.x);
 }
 
 

@@ -405,7 +405,7 @@ __global__ void __launch_bounds__(kK1GenThreads) k1_gather_mix_gen(const __grid_
 // sub-FFT), butterflies strided over `nth` threads with index `t`.
 template <int R, bool GSRC>
 __device__ __forceinline__ void dif_stage(const double2* __restrict__ src, double2* s, int len, int n,
-                                          const double2* __restrict__ tw, int t, int nth) {
+                                          const double2* __restrict__ tw, int t, int nth, int mv) {
   const int m = n / R;
   const int nbf = len / R;
   const unsigned magic = 0xffffffffu / (unsigned)m + 1u;  // beta / m == umulhi(beta, magic) for beta*m < 2^32
@@ -416,7 +416,8 @@ __device__ __forceinline__ void dif_stage(const double2* __restrict__ src, doubl
     const double2 w1 = ldg2(tw + k);
     double2 v[R];
 #pragma unroll
-    for (int r = 0; r < R; ++r) v[r] = GSRC ? ldcg2(src + base + r * m) : s[base + r * m];
+    for (int r = 0; r < R; ++r)
+      v[r] = GSRC ? (base + r * m < mv ? ldcg2(src + base + r * m) : make_double2(0.0, 0.0)) : s[base + r * m];
     dft<R>(v);
     // W^c by two interleaved recurrences W^c = W^{c-2} W^2 (half the dependency depth)
     const double2 w2 = cmul(w1, w1);
@@ -437,7 +438,7 @@ __device__ __forceinline__ void dif_stage(const double2* __restrict__ src, doubl
 
 template <int R, bool GDST>
 __device__ __forceinline__ void dit_stage(double2* s, double2* __restrict__ dst, int len, int n,
-                                          const double2* __restrict__ tw, double2 x0, int t, int nth) {
+                                          const double2* __restrict__ tw, double2 x0, int t, int nth, int mv) {
   const int m = n / R;
   const int nbf = len / R;
   const unsigned magic = 0xffffffffu / (unsigned)m + 1u;
@@ -465,8 +466,11 @@ __device__ __forceinline__ void dit_stage(double2* s, double2* __restrict__ dst,
     dft<R>(v);
 #pragma unroll
     for (int c = 0; c < R; ++c) {
-      if (GDST) st_keep(dst + base + c * m, cadd(x0, cconj(v[c])), pol);
-      else s[base + c * m] = v[c];
+      if (GDST) {
+        if (base + c * m < mv) st_keep(dst + base + c * m, cadd(x0, cconj(v[c])), pol);
+      } else {
+        s[base + c * m] = v[c];
+      }
     }
   }
 }
@@ -497,10 +501,10 @@ __device__ __forceinline__ void turn_stage(double2* s, int len, const double2* _
 
 template <bool G>
 __device__ __forceinline__ void run_dif(int R, const double2* src, double2* s, int len, int n, const double2* tw,
-                                        int t, int nth) {
+                                        int t, int nth, int mv = 1 << 30) {
   switch (R) {
 #define DSFT_C(RR) \
-  case RR: dif_stage<RR, G>(src, s, len, n, tw, t, nth); break;
+  case RR: dif_stage<RR, G>(src, s, len, n, tw, t, nth, mv); break;
     DSFT_RADICES(DSFT_C)
 #undef DSFT_C
     default: break;
@@ -509,10 +513,10 @@ __device__ __forceinline__ void run_dif(int R, const double2* src, double2* s, i
 
 template <bool G>
 __device__ __forceinline__ void run_dit(int R, double2* s, double2* dst, int len, int n, const double2* tw, double2 x0,
-                                        int t, int nth) {
+                                        int t, int nth, int mv = 1 << 30) {
   switch (R) {
 #define DSFT_C(RR) \
-  case RR: dit_stage<RR, G>(s, dst, len, n, tw, x0, t, nth); break;
+  case RR: dit_stage<RR, G>(s, dst, len, n, tw, x0, t, nth, mv); break;
     DSFT_RADICES(DSFT_C)
 #undef DSFT_C
     default: break;
@@ -554,55 +558,93 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
   } while (0)
 #endif
 
+// one (band, shift) row `blk` of the launch's rows (runtime radices), by the whole
+// CTA or (WARP) by one warp with its own shared-memory row (tiny rows: the passes are
+// latency-bound, so a warp per row with warp barriers finishes a row sooner and
+// keeps many rows in flight)
+template <bool WARP>
+__device__ __forceinline__ void k2_sync() {
+  if constexpr (WARP) __syncwarp();
+  else __syncthreads();
+}
+
+template <bool WARP = false>
+__device__ __forceinline__ void k2_rt_row(const K2Params& p, int blk, double2* sm, double2& sX0) {
+  [[maybe_unused]] int tslot = 0;
+  K2T();
+  const int M = p.M, F = p.nfac, Mv = p.Mv;  // FFT length, valid (Rader) length P - 1
+  const int NT = WARP ? 32 : (int)blockDim.x, tid = WARP ? (int)(threadIdx.x & 31) : (int)threadIdx.x;
+  double2* row = p.Z + (int64_t)blockIdx.y * p.z_vec_stride + (int64_t)k2_row(p, blk) * p.P;
+  const double2 x0 = ldcg2(row + Mv);
+  int n = M;
+  if (F >= 2) {
+    run_dif<true>(p.fac[0], row, sm, M, n, p.tw + p.toff[0], tid, NT, Mv);
+    n /= p.fac[0];
+  } else {
+    for (int i = tid; i < M; i += NT) sm[i] = i < Mv ? ldcg2(row + i) : make_double2(0.0, 0.0);
+  }
+  k2_sync<WARP>();
+  K2T();
+  for (int st = 1; st < F - 1; ++st) {
+    run_dif<false>(p.fac[st], sm, sm, M, n, p.tw + p.toff[st], tid, NT);
+    n /= p.fac[st];
+    k2_sync<WARP>();
+    K2T();
+  }
+  run_turn(p.fac[F - 1], sm, M, p.bhat, 0, M / p.fac[F - 1], &sX0, tid, NT);
+  k2_sync<WARP>();
+  K2T();
+  n = p.fac[F - 1];
+  for (int st = F - 2; st >= 1; --st) {
+    n *= p.fac[st];
+    run_dit<false>(p.fac[st], sm, sm, M, n, p.tw + p.toff[st], x0, tid, NT);
+    k2_sync<WARP>();
+    K2T();
+  }
+  if (F >= 2) {
+    n *= p.fac[0];
+    run_dit<true>(p.fac[0], sm, row, M, n, p.tw + p.toff[0], x0, tid, NT, Mv);
+  } else {
+    const uint64_t pol = l2_evict_last();
+    for (int i = tid; i < Mv; i += NT) st_keep(row + i, cadd(x0, cconj(sm[i])), pol);
+  }
+  if (tid == 0) row[Mv] = cadd(x0, sX0);  // X[0] = x0 + sum_q a_q
+#ifdef DSFT_K2_TRACE
+  k2_sync<WARP>();
+  K2T();
+#endif
+}
+
 // register cap: 65536 / (MAXT * MINB) rounded down to a multiple of 8
 template <int MAXT, int MINB>
 __global__ void __launch_bounds__(MAXT) __maxnreg__(((65536 / (MAXT * MINB)) & ~7) > 255 ? 255 : ((65536 / (MAXT * MINB)) & ~7))
     k2_prime_dft(const __grid_constant__ K2Params p) {
   extern __shared__ double2 sm[];
   __shared__ double2 sX0;
-  [[maybe_unused]] int tslot = 0;
-  K2T();
-  const int M = p.M, F = p.nfac;
-  const int NT = blockDim.x, tid = threadIdx.x;
-  double2* row = p.Z + (int64_t)blockIdx.y * p.z_vec_stride + (int64_t)k2_row(p, blockIdx.x) * p.P;
-  const double2 x0 = ldcg2(row + M);
-  int n = M;
-  if (F >= 2) {
-    run_dif<true>(p.fac[0], row, sm, M, n, p.tw + p.toff[0], tid, NT);
-    n /= p.fac[0];
-  } else {
-    for (int i = tid; i < M; i += NT) sm[i] = ldcg2(row + i);
-  }
-  __syncthreads();
-  K2T();
-  for (int st = 1; st < F - 1; ++st) {
-    run_dif<false>(p.fac[st], sm, sm, M, n, p.tw + p.toff[st], tid, NT);
-    n /= p.fac[st];
-    __syncthreads();
-    K2T();
-  }
-  run_turn(p.fac[F - 1], sm, M, p.bhat, 0, M / p.fac[F - 1], &sX0, tid, NT);
-  __syncthreads();
-  K2T();
-  n = p.fac[F - 1];
-  for (int st = F - 2; st >= 1; --st) {
-    n *= p.fac[st];
-    run_dit<false>(p.fac[st], sm, sm, M, n, p.tw + p.toff[st], x0, tid, NT);
-    __syncthreads();
-    K2T();
-  }
-  if (F >= 2) {
-    n *= p.fac[0];
-    run_dit<true>(p.fac[0], sm, row, M, n, p.tw + p.toff[0], x0, tid, NT);
-  } else {
-    const uint64_t pol = l2_evict_last();
-    for (int i = tid; i < M; i += NT) st_keep(row + i, cadd(x0, cconj(sm[i])), pol);
-  }
-  if (tid == 0) row[M] = cadd(x0, sX0);  // X[0] = x0 + sum_q a_q
-#ifdef DSFT_K2_TRACE
-  __syncthreads();
-  K2T();
-#endif
+  k2_rt_row(p, blockIdx.x, sm, sX0);
+}
+
+// Small plans (every bucket prime on runtime rows of M <= 1200, all primes' Z in
+// L2): one launch for the rows of every bucket prime, a warp per row, kK2RowsPerCta
+// rows per CTA; rows [row_off[i], row_off[i+1]) belong to prime i, each warp owns a
+// shared-memory row of mmax elements.
+constexpr int kK2RowsPerCta = 4;
+struct K2Multi {
+  int nprime, mmax;
+  int row_off[kMultiMaxT + 1];
+  K2Params pr[kMultiMaxT];
+};
+static_assert(sizeof(K2Multi) <= 32764, "K2Multi exceeds the kernel parameter limit");
+
+__global__ void __launch_bounds__(32 * kK2RowsPerCta) k2_prime_dft_multi(const __grid_constant__ K2Multi p) {
+  extern __shared__ double2 sm[];
+  __shared__ double2 sX0[kK2RowsPerCta];
+  const int w = threadIdx.x >> 5;
+  const int gr = (int)blockIdx.x * kK2RowsPerCta + w;
+  if (gr >= p.row_off[p.nprime]) return;  // (warp-uniform; no CTA barrier below)
+  int i = 0;
+  while (i + 1 < p.nprime && gr >= p.row_off[i + 1]) ++i;
+  k2_rt_row<true>(p.pr[i], gr - p.row_off[i], sm + (size_t)w * p.mmax, sX0[w]);
 }
 
 
@@ -618,24 +660,23 @@ __global__ void __launch_bounds__(MAXT) __maxnreg__(((65536 / (MAXT * MINB)) & ~
     k2a_split(const __grid_constant__ K2Params p) {
   extern __shared__ double2 sm[];
   __shared__ double2 sX0;
-  const int M = p.M, F = p.nfac, R0 = p.fac[0], RL = p.fac[F - 1];
+  const int M = p.M, F = p.nfac, R0 = p.fac[0], RL = p.fac[F - 1], Mv = p.Mv;
   const int Msub = M / R0;
   const int NT = blockDim.x, tid = threadIdx.x;
   const int rowl = blockIdx.x / R0, c = blockIdx.x - rowl * R0;
   const int rowi = k2_row(p, rowl);
-  const int64_t roff = (int64_t)blockIdx.y * p.z_vec_stride + (int64_t)rowi * p.P;
-  const double2* row = p.Z + roff;
-  double2* srow = p.Zs + roff;
+  const double2* row = p.Z + (int64_t)blockIdx.y * p.z_vec_stride + (int64_t)rowi * p.P;
+  double2* srow = p.Zs + (int64_t)blockIdx.y * p.zs_vec + (int64_t)rowi * p.zs_row;  // M + 1 entries
   const double2* twf = p.tw + p.toff[0];  // exp(-2 pi i e / M), e < M
   double sn, cs;
   sincospi(-2.0 * (double)c / (double)R0, &sn, &cs);
   const double2 wc = make_double2(cs, sn);  // W_R0^c
   for (int k = tid; k < Msub; k += NT) {
-    double2 acc = ldcg2(row + k);
+    double2 acc = k < Mv ? ldcg2(row + k) : make_double2(0.0, 0.0);
     double2 w = wc;
 #pragma unroll 4
     for (int r = 1; r < R0; ++r) {
-      acc = cadd(acc, cmul(ldcg2(row + k + r * Msub), w));
+      if (k + r * Msub < Mv) acc = cadd(acc, cmul(ldcg2(row + k + r * Msub), w));
       w = cmul(w, wc);
     }
     sm[k] = c == 0 ? acc : cmul(acc, ldg2(twf + (int64_t)c * k));
@@ -658,22 +699,21 @@ __global__ void __launch_bounds__(MAXT) __maxnreg__(((65536 / (MAXT * MINB)) & ~
   const uint64_t pol = l2_evict_last();
   for (int k = tid; k < Msub; k += NT) st_keep(srow + (int64_t)c * Msub + k, sm[k], pol);
   if (c == 0 && tid == 0) {
-    const double2 x0 = ldcg2(row + M);
+    const double2 x0 = ldcg2(row + Mv);
     srow[M] = x0;                                // x0 for K2b
-    ((double2*)row)[M] = cadd(x0, sX0);          // X[0] = x0 + sum_q a_q (no other CTA reads row[M])
+    ((double2*)row)[Mv] = cadd(x0, sX0);         // X[0] = x0 + sum_q a_q (no other CTA reads row[Mv])
   }
 }
 
 __global__ void __launch_bounds__(256) k2b_split(const __grid_constant__ K2Params p) {
-  const int M = p.M, R0 = p.fac[0];
+  const int M = p.M, R0 = p.fac[0], Mv = p.Mv;
   const int Msub = M / R0;
   const int nchunk = (Msub + 255) / 256;
   const int rowl = blockIdx.x / nchunk, k = (blockIdx.x - rowl * nchunk) * 256 + threadIdx.x;
   const int rowi = k2_row(p, rowl);
   if (k >= Msub) return;
-  const int64_t roff = (int64_t)blockIdx.y * p.z_vec_stride + (int64_t)rowi * p.P;
-  double2* row = p.Z + roff;
-  const double2* srow = p.Zs + roff;
+  double2* row = p.Z + (int64_t)blockIdx.y * p.z_vec_stride + (int64_t)rowi * p.P;
+  const double2* srow = p.Zs + (int64_t)blockIdx.y * p.zs_vec + (int64_t)rowi * p.zs_row;
   const double2* twf = p.tw + p.toff[0];
   const double2 x0 = ldcg2(srow + M);
   const uint64_t pol = l2_evict_last();
@@ -686,7 +726,7 @@ __global__ void __launch_bounds__(256) k2b_split(const __grid_constant__ K2Param
       v[r] = cmul(ldcg2(srow + k + r * Msub), ldg2(twf + (int64_t)r * k));        \
     dft<RR>(v);                                                                    \
     _Pragma("unroll") for (int cc = 0; cc < RR; ++cc)                              \
-      st_keep(row + k + cc * Msub, cadd(x0, cconj(v[cc])), pol);                   \
+      if (k + cc * Msub < Mv) st_keep(row + k + cc * Msub, cadd(x0, cconj(v[cc])), pol); \
   } break;
     DSFT_RADICES(DSFT_C)
 #undef DSFT_C
@@ -698,6 +738,22 @@ __global__ void __launch_bounds__(256) k2b_split(const __grid_constant__ K2Param
 #include "k3_ident.cuh"  // K3 (also compiled per residue tuple by NVRTC, jit.cpp)
 namespace dsft {
 static_assert(kK3MaxK == DSFT_MAX_K && kK3MaxT == DSFT_MAX_T, "k3_ident.cuh limits");
+
+// Small plans: K3 of every bucket prime in one launch (candidates only; the vote is
+// counted by K5s probing every prime's bucket of each candidate, K5Params.probe).
+struct K3Multi {
+  int nprime, pad_;
+  int cta_off[kMultiMaxT + 1];
+  K3Params pr[kMultiMaxT];
+};
+static_assert(sizeof(K3Multi) <= 32764, "K3Multi exceeds the kernel parameter limit");
+
+template <int RMAX>
+__global__ void __launch_bounds__(256) k3_identify_multi(const __grid_constant__ K3Multi p) {
+  int i = 0;
+  while (i + 1 < p.nprime && (int)blockIdx.x >= p.cta_off[i + 1]) ++i;
+  k3_body<RMAX, 0>(p.pr[i], (int64_t)((int)blockIdx.x - p.cta_off[i]) * blockDim.x + threadIdx.x);
+}
 
 
 // =========================================================== K5a medians
@@ -1203,6 +1259,7 @@ struct K5Params {
   int32_t* work_n;   // [vec]
   int32_t* ticket;   // [vec]
   int vote_min, nb;
+  int probe;         // 1: K3 wrote candidates only (one-launch K3); count the votes here
 };
 
 // Programmatic dependent launch inside the tail (K5s -> K5a -> K5b -> K6): each
@@ -1218,7 +1275,26 @@ __global__ void __launch_bounds__(256) k5s_scan(const __grid_constant__ K5Params
   const int v = blockIdx.y;
   const int j = (int)(gid / p.b.sumP);
   const int64_t base = (int64_t)v * p.b.cw_vec_stride + (int64_t)j * p.b.sumP;
-  const uint64_t mk = __ldcg((const unsigned long long*)(p.vmask + (int64_t)v * p.b.cw_vec_stride + gid));
+  uint64_t mk;
+  if (p.probe) {
+    // reading R9 by probing: the bucket primes whose bucket omega mod P_t produced
+    // omega; the slot of the smallest such prime owns the entry
+    const int64_t om = __ldcg(p.cand_w + (int64_t)v * p.b.cw_vec_stride + gid);
+    if (om == kSentinel) return;
+    const int64_t pos = gid - (int64_t)j * p.b.sumP;
+    mk = 0;
+    int owner = -1, self = -1;
+    for (int t = 0; t < p.a.T; ++t) {
+      if (pos >= p.a.off[t] && pos < p.a.off[t] + p.a.P[t]) self = t;
+      if (__ldcg(p.cand_w + base + p.a.off[t] + pmod(om, p.a.P[t])) == om) {
+        mk |= 1ull << t;
+        if (owner < 0) owner = t;
+      }
+    }
+    if (owner != self) return;
+  } else {
+    mk = __ldcg((const unsigned long long*)(p.vmask + (int64_t)v * p.b.cw_vec_stride + gid));
+  }
   if (__popcll(mk) < p.vote_min) return;
   const int pos = atomicAdd(p.acc_n + (int64_t)v * p.b.bn_vec + j, 1);
   p.acc_w[base + pos] = __ldcg(p.cand_w + (int64_t)v * p.b.cw_vec_stride + gid);
@@ -1258,6 +1334,51 @@ __global__ void __launch_bounds__(kK5Threads) k5b_select(const __grid_constant__
   __syncthreads();
   K5T(5);
   if (!s_last) return;
+  for (int b = tid; b < p.nb; b += kK5Threads) p.acc_n[(int64_t)v * p.b.bn_vec + b] = 0;
+  if (tid == 0) {
+    p.work_n[v] = 0;
+    p.ticket[v] = 0;
+  }
+}
+
+// ====================================================== fused tail (small plans)
+// After K5s (the vote, here by probing every prime's bucket, over many CTAs), one
+// CTA per (band, vector) runs the rest of the band tail with no grid-wide
+// dependency: Re/Im medians (R10, a warp per accepted omega), band top-budget +
+// unbias (R11, line 11); the last band CTA of the vector (ticket, after a
+// __threadfence) merges the band blocks (line 13) when `merge` is set and re-zeroes
+// the counters.  Two launches instead of four for the latency-bound small plans
+// (plan.cpp run_bands_small).
+struct K5TailParams {
+  K5Params f;
+  K6Params m;
+  int merge;
+};
+
+__global__ void __launch_bounds__(kK5Threads) k5_tail_small(const __grid_constant__ K5TailParams q) {
+  pdl_wait();
+  extern __shared__ unsigned char k5_smem[];
+  __shared__ int s_nz, s_last;
+  __shared__ int32_t pre[kK6MaxBlocks + 1];
+  const K5Params& p = q.f;
+  const int j = blockIdx.x, v = blockIdx.y, tid = threadIdx.x;
+  const int n = __ldcg(p.acc_n + (int64_t)v * p.b.bn_vec + j);
+  for (int e = tid >> 5; e < n; e += kK5Threads / 32) median_warp(p.a, v, j, e, tid & 31);
+  __syncthreads();
+  double* sm_m = (double*)k5_smem;
+  int64_t* sm_w = (int64_t*)(sm_m + 2 * kRankTile);
+  select_band(p.b, v, j, sm_m, sm_w, &s_nz);
+  __syncthreads();
+  __threadfence();  // band block visible before the ticket
+  if (tid == 0) s_last = atomicAdd(p.ticket + v, 1) == p.nb - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  if (q.merge) {
+    const int64_t cap = (int64_t)p.nb * p.b.budget > q.m.s ? (int64_t)p.nb * p.b.budget : q.m.s;
+    merge_range(q.m, v, 0, cap, sm_m, (int64_t*)(sm_m + kK6Stage), pre);
+  }
+  __syncthreads();
   for (int b = tid; b < p.nb; b += kK5Threads) p.acc_n[(int64_t)v * p.b.bn_vec + b] = 0;
   if (tid == 0) {
     p.work_n[v] = 0;
@@ -1318,6 +1439,10 @@ cudaError_t kernels_init() {
   if ((e = cudaFuncSetAttribute(k2_prime_dft<64, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm))) return e;
   if ((e = cudaFuncSetAttribute(k6_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, kK6Stage * 16))) return e;
   if ((e = cudaFuncSetAttribute(k5b_select, cudaFuncAttributeMaxDynamicSharedMemorySize, kRankTile * 64))) return e;
+  if ((e = cudaFuncSetAttribute(k5_tail_small, cudaFuncAttributeMaxDynamicSharedMemorySize, kRankTile * 64))) return e;
+  if ((e = cudaFuncSetAttribute(k2_prime_dft_multi, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                kK2RowsPerCta * 1200 * 16)))
+    return e;
 
   if ((e = cudaFuncSetAttribute(k2_prime_dft<256, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm))) return e;
   if ((e = cudaFuncSetAttribute(k2_prime_dft<512, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm))) return e;
@@ -1404,8 +1529,8 @@ cudaError_t launch_k1(const Plan& p, int nprime, const int* ts, double2* const* 
   return cudaGetLastError();
 }
 
-cudaError_t launch_k2(const Plan& p, int t, double2* Z, int64_t zstride, int nvec, void* ws, const int* /*bands*/,
-                      int nbands, cudaStream_t st, int band0, int nb_launch, int sig0, int nsig) {
+static K2Params k2_params(const Plan& p, int t, double2* Z, int64_t zstride, void* ws, int nbands, int& band0,
+                          int& nb_launch, int& sig0, int& nsig) {
   const Bucket& b = p.bk[t];
   const WsLayout L = ws_layout(p, p.ws_batch);
   K2Params k{};
@@ -1413,6 +1538,7 @@ cudaError_t launch_k2(const Plan& p, int t, double2* Z, int64_t zstride, int nve
   k.z_vec_stride = zstride;
   k.P = (int)b.P;
   k.M = b.M;
+  k.Mv = b.Mv;
   k.nfac = b.nfac;
   k.t = t;
   k.S = b.S;
@@ -1428,6 +1554,40 @@ cudaError_t launch_k2(const Plan& p, int t, double2* Z, int64_t zstride, int nve
   k.bhat = b.bhat;
   k.tw = b.tw;
   k.Zs = L.zs ? (double2*)((char*)ws + L.zs) : nullptr;
+  k.zs_row = (int)L.zs_row;
+  k.zs_vec = L.zs_vec;
+  return k;
+}
+
+// one-launch K2 of several bucket primes (all on the runtime <64,8> rows)
+bool k2_multi_ok(const Plan& p) {
+  if (p.T > kMultiMaxT) return false;
+  for (int t = 0; t < p.T; ++t)
+    if (p.bk[t].fft_variant != 0 || p.bk[t].split || p.bk[t].k2_jit) return false;
+  return true;
+}
+
+cudaError_t launch_k2_multi(const Plan& p, int n, const int* ts, double2* const* Zs, const int64_t* zst, int nvec,
+                            void* ws, int nbands, cudaStream_t st) {
+  K2Multi m{};
+  m.nprime = n;
+  m.row_off[0] = 0;
+  m.mmax = 0;
+  for (int i = 0; i < n; ++i) {
+    int b0 = 0, nbl = 0, s0 = 0, ns = 0;
+    m.pr[i] = k2_params(p, ts[i], Zs[i], zst[i], ws, nbands, b0, nbl, s0, ns);
+    m.row_off[i + 1] = m.row_off[i] + nbl * ns;
+    m.mmax = std::max(m.mmax, p.bk[ts[i]].M);
+  }
+  const size_t smem = (size_t)kK2RowsPerCta * m.mmax * sizeof(double2);
+  k2_prime_dft_multi<<<dim3(cdiv(m.row_off[n], kK2RowsPerCta), nvec), 32 * kK2RowsPerCta, smem, st>>>(m);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_k2(const Plan& p, int t, double2* Z, int64_t zstride, int nvec, void* ws, const int* /*bands*/,
+                      int nbands, cudaStream_t st, int band0, int nb_launch, int sig0, int nsig) {
+  const Bucket& b = p.bk[t];
+  const K2Params k = k2_params(p, t, Z, zstride, ws, nbands, band0, nb_launch, sig0, nsig);
   if (b.cl && b.k2_jit) {  // cluster mode: C CTAs per row (thread-block cluster, DSMEM)
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(nb_launch * nsig * b.cl), nvec);
@@ -1486,8 +1646,8 @@ cudaError_t launch_k2(const Plan& p, int t, double2* Z, int64_t zstride, int nve
   return cudaGetLastError();
 }
 
-cudaError_t launch_k3(const Plan& p, int t, const double2* Z, int64_t zstride, int nvec, void* ws, const int* bands,
-                      int nbands, cudaStream_t st, const int* prev, int nprev, int j0, int nb_launch) {
+static K3Params k3_params(const Plan& p, int t, const double2* Z, int64_t zstride, void* ws, const int* bands,
+                          int nbands, const int* prev, int nprev, int j0, int nb_launch) {
   const Bucket& b = p.bk[t];
   const WsLayout L = ws_layout(p, p.ws_batch);
   K3Params k{};
@@ -1529,6 +1689,33 @@ cudaError_t launch_k3(const Plan& p, int t, const double2* Z, int64_t zstride, i
   k.cw_vec_stride = L.cw_vec;
   k.sumP = p.sumP;
   k.off = b.off;
+  return k;
+}
+
+// one-launch K3 of several bucket primes (candidates only; K5s probes the votes)
+cudaError_t launch_k3_multi(const Plan& p, int n, const int* ts, double2* const* Zs, const int64_t* zst, int nvec,
+                            void* ws, const int* bands, int nbands, cudaStream_t st) {
+  if (n > kMultiMaxT) return cudaErrorInvalidValue;
+  K3Multi m{};
+  m.nprime = n;
+  m.cta_off[0] = 0;
+  for (int i = 0; i < n; ++i) {
+    m.pr[i] = k3_params(p, ts[i], Zs[i], zst[i], ws, bands, nbands, nullptr, 0, 0, 0);
+    m.pr[i].defer_vote = 1;
+    m.cta_off[i + 1] = m.cta_off[i] + (int)cdiv((int64_t)nbands * p.bk[ts[i]].P, 256);
+  }
+  const dim3 grid((unsigned)m.cta_off[n], nvec);
+  if (p.Rmax <= 7) k3_identify_multi<7><<<grid, 256, 0, st>>>(m);
+  else if (p.Rmax <= 13) k3_identify_multi<13><<<grid, 256, 0, st>>>(m);
+  else if (p.Rmax <= 17) k3_identify_multi<17><<<grid, 256, 0, st>>>(m);
+  else k3_identify_multi<31><<<grid, 256, 0, st>>>(m);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_k3(const Plan& p, int t, const double2* Z, int64_t zstride, int nvec, void* ws, const int* bands,
+                      int nbands, cudaStream_t st, const int* prev, int nprev, int j0, int nb_launch) {
+  const Bucket& b = p.bk[t];
+  const K3Params k = k3_params(p, t, Z, zstride, ws, bands, nbands, prev, nprev, j0, nb_launch);
   dim3 grid(cdiv((int64_t)k.nb * b.P, 256), nvec);
   // the plan's NVRTC kernel with this prime's residue tuple as constants (2.0 %
   // faster at c2 s = 1000 than the runtime-residue kernel below)
@@ -1579,7 +1766,7 @@ static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 g, dim3 b, size_t sme
 }
 
 cudaError_t launch_k45(const Plan& p, int nvec, void* ws, const int* bands, int nbands, cudaStream_t st,
-                       int64_t* freqs, double2* coeffs) {
+                       int64_t* freqs, double2* coeffs, bool probe) {
   const WsLayout L = ws_layout(p, p.ws_batch);
   K5Params f{};
   f.vmask = (const uint64_t*)((char*)ws + L.vmask);
@@ -1592,6 +1779,7 @@ cudaError_t launch_k45(const Plan& p, int nvec, void* ws, const int* bands, int 
   f.ticket = (int32_t*)((char*)ws + L.ticket);
   f.vote_min = p.params.vote_min;
   f.nb = nbands;
+  f.probe = probe ? 1 : 0;
 
   K5aParams& ka = f.a;
   ka.cand_v = (const double2*)((char*)ws + L.cand_v);
@@ -1631,6 +1819,22 @@ cudaError_t launch_k45(const Plan& p, int nvec, void* ws, const int* bands, int 
   k.band_nz = (int32_t*)((char*)ws + L.band_nz);
 
   cudaError_t e;
+  if (probe) {  // small plans: the fused per-band tail (+ merge by the last band CTA for small s)
+    K5TailParams q{};
+    q.f = f;
+    q.merge = freqs && nbands == p.J && p.s <= kTailMergeMaxS;
+    if (q.merge)
+      q.m = k6_params(k.band_w, k.band_c, k.band_m, k.band_nz, p.J, p.info.band_budget, L.band_vec, L.bn_vec, p.s,
+                      freqs, coeffs);
+    k5s_scan<<<dim3(cdiv((int64_t)nbands * p.sumP, 256), nvec), 256, 0, st>>>(f);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if ((e = launch_pdl(k5_tail_small, dim3(nbands, nvec), dim3(kK5Threads), kRankTile * 64, st, q)) != cudaSuccess ||
+        !freqs || q.merge)
+      return e;
+    if (nbands != p.J) return cudaErrorInvalidValue;
+    return launch_k6_blocks(k.band_w, k.band_c, k.band_m, k.band_nz, p.J, p.info.band_budget, L.band_vec, L.bn_vec,
+                            p.s, nvec, freqs, coeffs, st);
+  }
   k5s_scan<<<dim3(cdiv((int64_t)nbands * p.sumP, 256), nvec), 256, 0, st>>>(f);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   if ((e = launch_pdl(k5a_medians, dim3(2 * 148, nvec), dim3(256), 0, st, f)) != cudaSuccess) return e;

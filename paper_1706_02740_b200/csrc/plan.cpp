@@ -184,6 +184,29 @@ bool choose_radices(int M, std::vector<int>& out) {
   return true;
 }
 
+// FFT length of the zero-padded Rader convolution for a bucket prime whose P - 1 = Mv
+// has a prime factor above 13 (the general primes of DSFT_POOL_FULL): the cyclic
+// convolution of length Mv equals the first Mv outputs of a cyclic convolution of
+// any length M >= 2 Mv - 1 of the zero-padded input with the Rader kernel b extended
+// to the negative lags (b_ext[m] = b_m, b_ext[M - j] = b_{Mv - j}).  Chosen: the
+// fewest radix <= 16 passes, then the shortest M, over 13-smooth M in
+// [2 Mv - 1, 2.5 Mv].  (Same cost as Bluestein's chirp-z, without the two chirp
+// multiplies: K1 already writes the samples in Rader order.)
+int choose_pad_len(int Mv) {
+  int best = -1;
+  size_t best_np = 1000;
+  for (int m = 2 * Mv - 1; m <= 2 * Mv - 1 + Mv / 2 + 64; ++m) {
+    if (largest_prime_factor(m) > 13) continue;
+    std::vector<int> r;
+    if (!choose_radices(m, r)) continue;
+    if (r.size() < best_np) {
+      best_np = r.size();
+      best = m;
+    }
+  }
+  return best;
+}
+
 // Good-Thomas dimensions of the length-M FFT (DESIGN.md §6 K2).  The prime-power
 // components of M are grouped into coprime dimensions m_1 .. m_D; each dimension
 // gets the radices of choose_radices(m_d), and the radix list is their
@@ -311,7 +334,7 @@ bool choose_k2_layout(Bucket& b, std::vector<int>& rad, bool no_cluster) {
   // small rows (M <= 1200) run the runtime-radix kernel, which multiplies by the
   // all-ones tables of twiddle-free stages: one dimension there (c2 s = 50: 6975
   // vs 7115 transforms/s with Good-Thomas dimensions)
-  if (M > 1200) choose_k2_dims(b, rad);
+  if (M > 1200 && !b.pad) choose_k2_dims(b, rad);  // padded rows: natural order (zero tail)
   if ((int)rad.size() > kMaxFac) return false;
   if (M <= 1200) b.fft_variant = 0, b.fft_threads = 64;
   else if ((size_t)2 * ((size_t)M * 16 + 2048) <= 228 * 1024) b.fft_variant = 1, b.fft_threads = 256;
@@ -347,7 +370,11 @@ WsLayout ws_layout(const Plan& p, int64_t nvec) {
   L.z_buf = nvec * L.z_vec;
   const bool grouped = k1_grouped(p, nvec);
   L.z = take(grouped ? (size_t)nvec * p.z_tot * 16 : (size_t)kZBufs * L.z_buf * 16);
-  L.zs = take(p.any_split ? (size_t)L.z_buf * 16 : 0);
+  L.zs_row = 0;
+  for (int t = 0; t < p.T; ++t)
+    if (p.bk[t].split) L.zs_row = std::max<int64_t>(L.zs_row, (int64_t)p.bk[t].M + 1);
+  L.zs_vec = (int64_t)p.J * p.Smax * L.zs_row;
+  L.zs = take(p.any_split ? (size_t)nvec * L.zs_vec * 16 : 0);
   L.cand_w = take((size_t)nvec * L.cw_vec * 8);
   L.cand_v = take((size_t)nvec * L.cw_vec * p.Kmax * 16);
   L.vmask = take((size_t)nvec * L.cw_vec * 8);
@@ -537,15 +564,20 @@ static dsft_status derive(int64_t N, int64_t s, const dsft_params& prm, Plan& P)
     P.Kmax = std::max(P.Kmax, K);
     P.Rmax = std::max(P.Rmax, b.r[K - 1]);
     P.Smax = std::max(P.Smax, S);
-    // Rader setup: M = P - 1, primitive root g
-    b.M = (int)(b.P - 1);
+    // Rader setup: cyclic convolution of length Mv = P - 1, primitive root g; the
+    // convolution runs as FFTs of length M = Mv (13-smooth P - 1) or, for a general
+    // prime, of a 13-smooth M >= 2 Mv - 1 with zero-padded input (choose_pad_len)
+    b.Mv = (int)(b.P - 1);
     if (b.P > 65535) return fail(DSFT_ERR_UNSUPPORTED, "bucket prime >= 2^16 (16-bit Rader tables)");
-    const auto pf = prime_factors(b.M);
+    b.pad = largest_prime_factor(b.Mv) > 13;
+    b.M = b.pad ? choose_pad_len(b.Mv) : b.Mv;
+    if (b.M <= 0) return fail(DSFT_ERR_INTERNAL, "no 13-smooth convolution length for a general bucket prime");
+    const auto pf = prime_factors(b.Mv);
     int g = 2;
     for (;; ++g) {
       bool ok = true;
       for (int64_t qf : pf)
-        if (powmod(g, b.M / qf, b.P) == 1) {
+        if (powmod(g, b.Mv / qf, b.P) == 1) {
           ok = false;
           break;
         }
@@ -553,7 +585,7 @@ static dsft_status derive(int64_t N, int64_t s, const dsft_params& prm, Plan& P)
     }
     b.g = g;
     std::vector<int> rad;
-    if (!choose_k2_layout(b, rad, (prm.flags & DSFT_FLAG_NO_CLUSTER) != 0)) return fail(DSFT_ERR_UNSUPPORTED, "bucket prime whose P-1 is not 13-smooth (no general-prime K2 yet) or too many FFT stages");
+    if (!choose_k2_layout(b, rad, (prm.flags & DSFT_FLAG_NO_CLUSTER) != 0)) return fail(DSFT_ERR_UNSUPPORTED, "too many K2 FFT stages");
     b.nfac = (int)rad.size();
     for (int i = 0; i < b.nfac; ++i) b.fac[i] = rad[i];
     if (b.ndim == 1) {
@@ -667,8 +699,9 @@ static dsft_status upload_tables(Plan& P) {
     };
     const int64_t ginv = invmod(b.g, b.P);
     int64_t gp = 1, gn = 1;
+    const int Mv = b.Mv;
     std::vector<cld> bseq(M), bf(M);
-    for (int q = 0; q < M; ++q) {
+    for (int q = 0; q < Mv; ++q) {
       const int64_t x = pos_time(q);
       posn[gp] = (uint16_t)x;        // node g^q = gp: K1 input of Rader index q
       gpow[x] = (uint16_t)gp;
@@ -678,6 +711,8 @@ static dsft_status upload_tables(Plan& P) {
       gp = gp * b.g % b.P;
       gn = gn * ginv % b.P;
     }
+    if (b.pad)  // negative lags of the Rader kernel (choose_pad_len): b_ext[M - j] = b_{Mv - j}
+      for (int j = 1; j < Mv; ++j) bseq[M - j] = bseq[Mv - j];
     fft_rec(bseq.data(), bf.data(), M, 1);
     const int RL = b.fac[b.nfac - 1], nblk = M / RL;
     for (int c = 0; c < M; ++c) {
@@ -769,7 +804,8 @@ static void specialise_k2(Plan& P) {
         return;
       }
       bb.jit_threads = nt;
-      bb.k2_jit = jit_k2(nt, minb, bb.fac, bb.nfac, (size_t)bb.M * 16, &why[t], false, bb.twf);
+      bb.k2_jit = jit_k2(nt, minb, bb.fac, bb.nfac, (size_t)bb.M * 16, &why[t], false,
+                         bb.twf | (bb.pad ? 0x80000000u : 0u));  // bit 31: zero-padded rows
     });
   }
   for (auto& x : th) x.join();
@@ -1055,10 +1091,49 @@ static dsft_status ensure_pipe(Plan& p) {
   return DSFT_OK;
 }
 
+// Small plans (every prime's filtered samples fit L2, T <= kMultiMaxT): one launch
+// per stage on the caller's stream -- K1 for every prime, K2 for every prime (one
+// launch when all rows are runtime <64,8> rows), K3 for every prime (candidates
+// only), then K5s (the vote by probing) and the fused per-band tail (medians, band
+// select, and the merge in its last CTA): 5 launches instead of 3T + 4, no
+// cross-stream events (latency-bound regime).
+static dsft_status run_bands_small(Plan& p, const double2* f, int64_t ld, int nv, const int* bands, int nb,
+                                   cudaStream_t st, int64_t* freqs, double2* coeffs) {
+  const WsLayout L = ws_layout(p, p.ws_batch);
+  int ts[DSFT_MAX_T], keep[DSFT_MAX_T];
+  double2* Zs[DSFT_MAX_T];
+  int64_t zst[DSFT_MAX_T];
+  for (int k = 0; k < p.T; ++k) {
+    ts[k] = p.order[k];
+    Zs[k] = (double2*)((char*)p.ws + L.z) + (int64_t)p.ws_batch * p.z_off[ts[k]];
+    zst[k] = (int64_t)p.J * p.bk[ts[k]].S * p.bk[ts[k]].P;
+    keep[k] = 1;
+  }
+  CU(timed(p, 0, st, [&] { return launch_k1(p, p.T, ts, Zs, zst, keep, f, ld, nv, bands, nb, st); }),
+     "K1 gather_mix launch");
+  if (k2_multi_ok(p)) {
+    CU(timed(p, 1, st, [&] { return launch_k2_multi(p, p.T, ts, Zs, zst, nv, p.ws, nb, st); }), "K2 launch");
+  } else {
+    for (int k = 0; k < p.T; ++k)
+      CU(timed(p, 1, st, [&] { return launch_k2(p, ts[k], Zs[k], zst[k], nv, p.ws, bands, nb, st); }),
+         "K2 prime_dft launch");
+  }
+  CU(timed(p, 2, st, [&] { return launch_k3_multi(p, p.T, ts, Zs, zst, nv, p.ws, bands, nb, st); }),
+     "K3 identify launch");
+  CU(timed(p, 3, st, [&] { return launch_k45(p, nv, p.ws, bands, nb, st, freqs, coeffs, true); }),
+     "K456 vote/estimate/merge launch");
+  return DSFT_OK;
+}
+
+static bool small_plan(const Plan& p) {
+  return k1_grouped(p, p.ws_batch) && p.T <= kMultiMaxT && !(p.params.flags & DSFT_FLAG_SERIAL);
+}
+
 static dsft_status run_bands(Plan& p, const double2* f, int64_t ld, int nv, const int* bands, int nb,
                              cudaStream_t st, int64_t* freqs = nullptr, double2* coeffs = nullptr) {
   dsft_status stt = ensure_pipe(p);
   if (stt != DSFT_OK) return stt;
+  if (small_plan(p)) return run_bands_small(p, f, ld, nv, bands, nb, st, freqs, coeffs);
   const bool serial = (p.params.flags & DSFT_FLAG_SERIAL) != 0;  // every launch on the caller's stream
   cudaStream_t a1 = serial ? st : p.aux, a3 = serial ? st : p.aux3;
   cudaEvent_t* evK1 = p.pipe_ev.data();            // [T] K1(t) done (aux)
@@ -1314,6 +1389,8 @@ int64_t dsft_plan_collect_timeline(dsft_plan* pl, double* rows, int64_t n) {
 
 int64_t dsft_plan_launches_per_execute(const dsft_plan* pl) {
   if (!pl) return 0;
+  if (small_plan(pl->p))  // K1, K2 (one or per prime), K3, fused tail (+ K6 above kTailMergeMaxS)
+    return 2 + (k2_multi_ok(pl->p) ? 1 : pl->p.T) + (pl->p.s <= kTailMergeMaxS ? 2 : 3);
   int64_t n = 4;  // K5 scan, K5 medians, K5 select, K6 merge
   for (int t = 0; t < pl->p.T; ++t) n += 3 + (pl->p.bk[t].split ? 1 : 0);  // K1, K2 (K2a + K2b), K3
   return n;

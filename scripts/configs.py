@@ -175,7 +175,7 @@ def det(quick):
     (n_bucket_primes = 0), majority vote; throughput and exact support at c1 / c2 sizes,
     oracle parity where the oracle finishes in seconds (c1)."""
     out = []
-    prm = dict(n_bucket_primes=0, vote_min=0)
+    prm = dict(n_bucket_primes=0, vote_min=0, pool_rule="smooth")
     for N, s, cfg in ((2 ** 22, 50, 1), (2 ** 26, 200, 2), (2 ** 26, 1000, 2)):
         pl = planted(N, s, cfg=cfg, trial=0)
         f = torch.from_numpy(pl.f).to(DEV)

@@ -13,7 +13,7 @@ from dsft_synth import planted  # noqa: E402
 N, s = 2 ** 26, int(sys.argv[1]) if len(sys.argv) > 1 else 1000
 pl = planted(N, s, cfg=2, trial=0)
 f = torch.from_numpy(pl.f).cuda()
-plan = d.Plan(N, s, d.make_params(n_bucket_primes=0, vote_min=0))
+plan = d.Plan(N, s, d.make_params(n_bucket_primes=0, vote_min=0, pool_rule="smooth"))
 fr = torch.empty(s, dtype=torch.int64, device="cuda")
 co = torch.empty(s, dtype=torch.complex128, device="cuda")
 st = torch.cuda.current_stream()

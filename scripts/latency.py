@@ -23,8 +23,9 @@ import torch  # noqa: E402
 import paper_1706_02740_b200 as d  # noqa: E402
 from dsft_synth import planted  # noqa: E402
 
-CONFIGS = [("c0", 4096, 8), ("c1", 2**22, 50), ("c2_s50", 2**26, 50), ("c3", 6000011, 100),
-           ("c2_s1000", 2**26, 1000)]
+CONFIGS = [("c0", 4096, 8, {}), ("c1", 2**22, 50, {}), ("c2_s50", 2**26, 50, {}), ("c3", 6000011, 100, {}),
+           ("c2_s1000", 2**26, 1000, {}), ("c2_s1000_thm4", 2**26, 1000, {"preset": "thm4"}),
+           ("c1_thm4", 2**22, 50, {"preset": "thm4"})]
 
 
 def time_ms(fn, reps, flush):
@@ -51,16 +52,16 @@ def main():
     dev = torch.device("cuda:0")
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     rows = []
-    for name, N, s in CONFIGS:
+    for name, N, s, kw in CONFIGS:
         if a.only and name not in a.only.split(","):
             continue
         pl = planted(N, s, cfg=50, trial=0)
         f = torch.from_numpy(pl.f).to(dev)
         fr = torch.empty(s, dtype=torch.int64, device=dev)
         co = torch.empty(s, dtype=torch.complex128, device=dev)
-        row = {"config": name, "N": N, "s": s}
+        row = {"config": name, "N": N, "s": s, **kw}
         for tag, flags in (("graph", 0), ("no_graph", d.FLAG_NO_GRAPH)):
-            plan = d.Plan(N, s, d.make_params(flags=flags))
+            plan = d.Plan(N, s, d.make_params(flags=flags, **kw))
             ms = time_ms(lambda: plan.dsft_execute(f, fr, co), a.reps, flush)
             ok = sorted(x for x in fr.cpu().tolist() if x != d.SENTINEL) == pl.freqs.tolist()
             row[tag] = {"ms": ms, "support_exact": ok, "launches": plan.launches_per_execute()}

@@ -37,14 +37,14 @@ def test_plan_matches_oracle(N, s, seed, preset):
 
 def test_literal_alpha_and_kappa_override_match():
     for kw in (dict(alpha_rule="literal"), dict(kappa=5), dict(tau=0.1), dict(bucket_factor=5.0, n_bucket_primes=7, vote_min=4),
-               dict(n_bucket_primes=0, vote_min=0), dict(n_bucket_primes=0, vote_min=5), dict(vote_min=0)):
+               dict(n_bucket_primes=0, vote_min=0, pool_rule="smooth"), dict(n_bucket_primes=0, vote_min=5, pool_rule="smooth"), dict(vote_min=0)):
         info = d.dsft_plan_derive_info(2**20, 100, d.make_params(**kw))
         p = derive_plan(2**20, 100, OracleParams(**kw))
         assert (info.w, info.J, info.kappa, list(info.primes[:info.T])) == (p.w, p.J, p.kappa, p.primes)
         assert (info.T, info.vote_min) == (len(p.primes), p.vote_min)
     # the deterministic variant at the headline s: T = 37 bucket primes (<= DSFT_MAX_T)
-    info = d.dsft_plan_derive_info(2**26, 1000, d.make_params(n_bucket_primes=0, vote_min=0))
-    p = derive_plan(2**26, 1000, OracleParams(n_bucket_primes=0, vote_min=0))
+    info = d.dsft_plan_derive_info(2**26, 1000, d.make_params(n_bucket_primes=0, vote_min=0, pool_rule="smooth"))
+    p = derive_plan(2**26, 1000, OracleParams(n_bucket_primes=0, vote_min=0, pool_rule="smooth"))
     assert info.T == len(p.primes) == 37 and list(info.primes[:info.T]) == p.primes and info.vote_min == 19
 
 
@@ -57,6 +57,17 @@ def test_config_errors_match_oracle(N, s, kw):
     with pytest.raises(d.DsftError) as ei:
         d.dsft_plan_derive_info(N, s, d.make_params(**kw))
     assert ei.value.status == d.DSFT_ERR_CONFIG
+
+
+@pytest.mark.parametrize("rule", ["full", "smooth"])
+def test_pool_rule_matches_oracle(rule):
+    """Reading R6 on both sides: the same pool and the same seeded draw (DSFT_POOL_FULL:
+    every prime in range -- general primes run the zero-padded Rader K2)."""
+    for N, s, seed in ((2**26, 1000, 0), (2**22, 50, 3), (4096, 8, 1), (2**21, 4000, 2)):
+        info = d.dsft_plan_derive_info(N, s, d.make_params(seed=seed, pool_rule=rule))
+        p = derive_plan(N, s, OracleParams(seed=seed, pool_rule=rule))
+        assert list(info.primes[:info.T]) == p.primes
+    assert d.default_pool_rule() == OracleParams().pool_rule == "smooth"
 
 
 def test_shard_bands_partition():
@@ -83,4 +94,7 @@ def test_k2_specialisation_compiles_with_nvrtc(tmp_path, monkeypatch):
     for rad, twf in (([8, 3, 13, 13], 0b011), ([9, 11, 10, 5], 0b011)):
         st, log = d.dsft_debug_jit_compile(256, 2, rad, twf=twf)
         assert st == 0, log
-    assert len(list(tmp_path.glob("k2_*.cubin"))) == 8
+    # zero-padded Rader rows of a general bucket prime (bit 31 of twf): M = 8192 >= 2 (P - 1) - 1
+    st, log = d.dsft_debug_jit_compile(512, 1, [16, 16, 8, 4], twf=0x80000000)
+    assert st == 0, log
+    assert len(list(tmp_path.glob("k2_*.cubin"))) == 9

@@ -301,9 +301,9 @@ def test_deterministic_variant_parity(N, s):
     """Reading R13 (every pool prime, majority vote): T = 12 and 28 bucket primes --
     64-bit vote masks, T K > 32 median values per frequency (warp rank selection)."""
     pl = planted(N, s, cfg=41, trial=0)
-    plan = d.Plan(N, s, d.make_params(n_bucket_primes=0, vote_min=0))
-    ref = dsft(pl.f, s, OracleParams(n_bucket_primes=0, vote_min=0))
-    dp = derive_plan(N, s, OracleParams(n_bucket_primes=0, vote_min=0))
+    plan = d.Plan(N, s, d.make_params(n_bucket_primes=0, vote_min=0, pool_rule="smooth"))
+    ref = dsft(pl.f, s, OracleParams(n_bucket_primes=0, vote_min=0, pool_rule="smooth"))
+    dp = derive_plan(N, s, OracleParams(n_bucket_primes=0, vote_min=0, pool_rule="smooth"))
     assert plan.info.T == len(dp.primes) > 5 and plan.primes() == dp.primes
     assert_parity(run_gpu(plan, pl.f), ref, s)
 
@@ -314,7 +314,7 @@ def test_deterministic_variant_headline_size():
     above)."""
     N, s = 2**26, 1000
     pl = planted(N, s, cfg=2, trial=0)
-    plan = d.Plan(N, s, d.make_params(n_bucket_primes=0, vote_min=0))
+    plan = d.Plan(N, s, d.make_params(n_bucket_primes=0, vote_min=0, pool_rule="smooth"))
     assert plan.info.T == 37 and plan.info.vote_min == 19
     fr, co = run_gpu(plan, pl.f)
     assert sorted(fr.tolist()) == pl.freqs.tolist()
@@ -540,3 +540,78 @@ def test_theorem5_tail_bound_gpu(N):
                + 198 * math.sqrt(s) * np.max(np.abs(pl.f)) * N ** -2.0)
         assert lhs <= rhs, (lhs, rhs)
         assert head <= set(v)  # the 16 heads are recovered
+
+
+# ------------------------------------------- general bucket primes (DSFT_POOL_FULL)
+@pytest.mark.parametrize("N,s,seed", [(2**16, 50, 4), (2**20, 300, 1), (2**21, 1000, 2), (2**21, 4000, 3)])
+def test_full_pool_stage_parity(N, s, seed):
+    """Reading R6 with pool_rule = full: bucket primes whose P - 1 has a prime factor
+    above 13 run the zero-padded Rader convolution (FFT length M >= 2 (P - 1) - 1;
+    runtime, specialised, one-CTA and cluster rows).  K1 and K1+K2(+fold) element by
+    element against O2 / O3 for every bucket prime of one band."""
+    op = derive_plan(N, s, OracleParams(seed=seed, pool_rule="full"))
+    plan = d.Plan(N, s, d.make_params(seed=seed, pool_rule="full"))
+    assert plan.primes() == op.primes
+    general = [P for P in op.primes if max(q for q in range(2, P) if (P - 1) % q == 0 and
+                                           all(q % r for r in range(2, int(q ** 0.5) + 1))) > 13]
+    assert general, op.primes
+    pl = planted(N, s, cfg=43, trial=seed)
+    f = to_dev(pl.f)
+    band = op.J // 3
+    for t in range(op.T):
+        for i in (0, len(op.residues[t]) - 1):
+            L = op.primes[t] * op.residues[t][i]
+            out = torch.empty(L, dtype=torch.complex128, device=DEV)
+            plan.dsft_debug_grid(f, band, t, i, 1, out)
+            Y_ref = alias_dft(filtered_samples(pl.f, op, op.q[band], L))
+            assert np.max(np.abs(out.cpu().numpy() - Y_ref)) <= 1e-13 * max(1.0, np.max(np.abs(Y_ref)))
+
+
+FULL_E2E = [(4096, 8, 0, None), (2**16, 50, 5, None), (2**22, 50, 1, None), (6000011, 100, 3, 20.0),
+            (2**20, 2000, 2, None), (2**21, 4000, 2, None)]
+
+
+@pytest.mark.parametrize("N,s,trial,snr", FULL_E2E)
+def test_full_pool_end_to_end(N, s, trial, snr):
+    pl = planted(N, s, cfg=44, trial=trial, snr_db=snr)
+    ref = dsft(pl.f, s, OracleParams(seed=trial, pool_rule="full"))
+    plan = d.Plan(N, s, d.make_params(seed=trial, pool_rule="full"))
+    assert_parity(run_gpu(plan, pl.f), ref, s)
+
+
+@pytest.mark.parametrize("flags", ["NO_JIT", "NO_CLUSTER"])
+def test_full_pool_fallback_kernels(flags):
+    """Zero-padded rows through the runtime-radix K2 (no NVRTC) and the two-launch
+    split mode (no cluster): same oracle parity."""
+    N, s = 2**20, 2000
+    pl = planted(N, s, cfg=45, trial=0)
+    ref = dsft(pl.f, s, OracleParams(seed=7, pool_rule="full"))
+    plan = d.Plan(N, s, d.make_params(seed=7, pool_rule="full", flags=getattr(d, "FLAG_" + flags)))
+    assert_parity(run_gpu(plan, pl.f), ref, s)
+
+
+def test_full_pool_headline_size():
+    """BASELINE config 2 (N = 2^26, s = 1000) with the full prime pool: oracle parity."""
+    N, s = 2**26, 1000
+    pl = planted(N, s, cfg=2, trial=0)
+    ref = dsft(pl.f, s, OracleParams(seed=0, pool_rule="full"))
+    plan = d.Plan(N, s, d.make_params(seed=0, pool_rule="full"))
+    assert_parity(run_gpu(plan, pl.f), ref, s)
+    assert sorted(ref.freqs.tolist()) == pl.freqs.tolist()
+
+
+@pytest.mark.parametrize("N,s,kw", [(4096, 8, {}), (2**22, 50, {}), (6000011, 100, {}), (2**20, 300, {}),
+                                    (2**22, 50, {"pool_rule": "full"}), (2**16, 50, {"n_bucket_primes": 9})])
+def test_small_plan_path_equals_pipeline(N, s, kw):
+    """Small plans run one launch per stage (K1, K2 and K3 over every bucket prime,
+    the vote counted by K5s probing); DSFT_FLAG_SERIAL forces the
+    per-prime pipeline with K3's incremental vote: bitwise identical results, and
+    oracle parity."""
+    pl = planted(N, s, cfg=46, trial=1)
+    plan = d.Plan(N, s, d.make_params(seed=2, **kw))
+    ser = d.Plan(N, s, d.make_params(seed=2, flags=d.FLAG_SERIAL, **kw))
+    a, b = run_gpu(plan, pl.f), run_gpu(ser, pl.f)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    assert_parity(a, dsft(pl.f, s, OracleParams(seed=2, **kw)), s)
+    if N <= 2**22 and s <= 50:
+        assert plan.launches_per_execute() <= 2 + plan.info.T + 3 < ser.launches_per_execute()

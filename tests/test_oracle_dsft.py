@@ -228,7 +228,7 @@ def test_deterministic_variant_vs_bruteforce_dft(N, s):
     """Reading R13, the deterministic variant (n_bucket_primes = 0: every pool prime,
     PAPER.md:40-44, 604-610; vote_min = 0: more than half): exactly
     s-sparse input, the output set is R_s^opt of the O(N^2) brute-force DFT."""
-    prm = OracleParams(n_bucket_primes=0, vote_min=0)
+    prm = OracleParams(n_bucket_primes=0, vote_min=0, pool_rule="smooth")
     plan = derive_plan(N, s, prm)
     assert len(plan.primes) > 5 and plan.vote_min == len(plan.primes) // 2 + 1
     for trial in range(2):

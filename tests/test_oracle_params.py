@@ -102,6 +102,17 @@ def test_pool_rule_bruteforce():
         assert pool == ref
 
 
+@pytest.mark.parametrize("s", [4, 8, 50, 1000])
+def test_full_pool_is_every_prime_in_range(s):
+    """Reading R6, DSFT_POOL_FULL: every prime in [ceil(c_b s), 2 ceil(c_b s))
+    by trial division (a random subset of the deterministic
+    measurements); the smooth pool is its subset with 13-smooth P - 1."""
+    ref = [p for p in range(4 * s, 8 * s) if _is_prime_naive(p)]
+    assert bucket_pool(s, 4.0, "full") == ref
+    assert set(bucket_pool(s, 4.0, "smooth")) <= set(ref)
+    assert derive_plan(2**20, max(s, 8), OracleParams(pool_rule="full")).pool == bucket_pool(max(s, 8), 4.0, "full")
+
+
 def test_draw_is_distinct_sorted_seeded():
     pool = bucket_pool(1000, 4.0)
     a = draw_distinct(pool, 5, 7)
@@ -150,8 +161,8 @@ def test_residue_rule(N, s, seed):
 def test_residue_rule_headline_values():
     """BASELINE config 2 (N = 2^26, s = 1000, seed 0): P = 4051, 4057, 4357 need
     prod r >= 16567, 16542, 15403 -> {3,5,7,11,17} (38 extra rows) rather than the
-    consecutive {3,...,17} (50); P = 4951, 7561 -> {3,5,7,11,13}."""
-    p = derive_plan(2**26, 1000, OracleParams(seed=0))
+    consecutive {3,...,17} (50); P = 4951, 7561 -> {3,5,7,11,13} (13-smooth pool)."""
+    p = derive_plan(2**26, 1000, OracleParams(seed=0, pool_rule="smooth"))
     assert p.primes == [4051, 4057, 4357, 4951, 7561]
     assert p.residues == [[3, 5, 7, 11, 17]] * 3 + [[3, 5, 7, 11, 13]] * 2
 
@@ -175,6 +186,6 @@ def test_deterministic_variant_plan(s):
     ref = [p for p in range(4 * s, 8 * s) if _is_prime_naive(p)
            and max(d for d in range(2, p) if (p - 1) % d == 0 and _is_prime_naive(d)) <= 13]
     for seed in (0, 7):
-        p = derive_plan(2**20, s, OracleParams(n_bucket_primes=0, vote_min=0, seed=seed))
+        p = derive_plan(2**20, s, OracleParams(n_bucket_primes=0, vote_min=0, seed=seed, pool_rule="smooth"))
         assert p.primes == ref and p.vote_min == len(ref) // 2 + 1
-    assert derive_plan(2**20, s, OracleParams(n_bucket_primes=0, vote_min=2)).vote_min == 2
+    assert derive_plan(2**20, s, OracleParams(n_bucket_primes=0, vote_min=2, pool_rule="smooth")).vote_min == 2
