@@ -16,6 +16,22 @@ typedef unsigned short uint16_t;
 
 namespace dsft {
 
+// DSFT_CHECKED builds: device-side bounds checks (trap on violation; see
+// internal.h kGuardBytes).  Compiled out otherwise.
+#ifdef DSFT_CHECKED
+#define DSFT_CHECK(cond)                                                                      \
+  do {                                                                                        \
+    if (!(cond)) {                                                                            \
+      printf("dsft check failed: %s (%s:%d)\n", #cond, __FILE__, __LINE__);                   \
+      __trap();                                                                               \
+    }                                                                                         \
+  } while (0)
+#else
+#define DSFT_CHECK(cond) \
+  do {                   \
+  } while (0)
+#endif
+
 // ---------------------------------------------------------------- complex helpers
 __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }

@@ -170,7 +170,17 @@ struct WsLayout {
   int64_t cw_vec;    // elements per vector in cand_w / acc_w / acc_z: J * sum_t P_t
   int64_t band_vec;  // elements per vector in band_w / band_c / band_z: J * budget
   int64_t bn_vec;    // elements per vector in band_n: J
+  // DSFT_CHECKED builds: a kGuardBytes guard zone after every region (pattern 0xA5),
+  // verified after every execute (the substitute for compute-sanitizer memcheck,
+  // which this GPU pool does not allow)
+  int nguard;
+  size_t guard[32];
 };
+#ifdef DSFT_CHECKED
+constexpr size_t kGuardBytes = 256;
+#else
+constexpr size_t kGuardBytes = 0;
+#endif
 WsLayout ws_layout(const Plan& p, int64_t nvec);
 bool k1_grouped(const Plan& p, int64_t nvec);
 
@@ -204,6 +214,8 @@ cudaError_t launch_k6(const Plan& p, int nvec, void* ws, int64_t* freqs, double2
 cudaError_t launch_debug_grid(const Plan& p, int t, const double2* Z, int i, int band, int what, double2* out,
                               cudaStream_t st);
 cudaError_t kernels_init();  // one-time attribute setup (dynamic smem limits)
+// DSFT_CHECKED: trap if any guard zone of the workspace lost its pattern
+cudaError_t launch_check_guards(const WsLayout& L, void* ws, cudaStream_t st);
 // jit.cpp: k2_ct<nt, minb, fac...> compiled with NVRTC (cudaKernel_t), or nullptr + *why
 const void* jit_k2(int nt, int minb, const int* fac, int nfac, size_t smem_bytes, std::string* why, bool cluster = false,
                    unsigned twf = 0);

@@ -27,6 +27,7 @@ struct K2Params {
 
 // global row index (band * S + shift) of the launch's local block b
 __device__ __forceinline__ int k2_row(const K2Params& p, int b) {
+  DSFT_CHECK(b >= 0 && p.nsig > 0 && p.sig0 + p.nsig <= p.S);
   const int bl = b / p.nsig;
   return (p.band0 + bl) * p.S + p.sig0 + (b - bl * p.nsig);
 }

@@ -125,6 +125,7 @@ __device__ __forceinline__ void k3_body(const K3Params& p, int64_t gid) {
   const int64_t om = lo + d;
   const bool ok = (om <= q + p.halfN_dn) && (om >= q - p.w) && (om < q + p.w) && (om >= p.B_lo) && (om <= p.B_hi);
   const int64_t slot = (int64_t)v * p.cw_vec_stride + (int64_t)j * p.sumP + p.off + a;
+  DSFT_CHECK(a >= 0 && a < P && p.off + a < p.sumP && j >= 0);
   p.cand_w[slot] = ok ? om : kK3Sentinel;
   uint64_t mk = 0;
   if (ok) {

@@ -197,6 +197,7 @@ __device__ __forceinline__ void k1_mix_node(const K1Params& p, const K1Prime& pp
   // throughput, bounded the single-chain loop); unlisted bands only advance the
   // phase recurrences
   const bool all = p.jfirst == 0 && p.jstride == 1 && p.nb == p.J;
+  DSFT_CHECK(sigma >= 0 && sigma < pp.S && q >= 0 && q < pp.P);
   int j = 0;
   for (; j + 1 < p.J; j += 2) {
     const int s0 = all ? j : k1_slot(p, j), s1 = all ? j + 1 : k1_slot(p, j + 1);
@@ -278,6 +279,7 @@ __global__ void __launch_bounds__(kK1FastThreads) k1_gather_mix_fast(const __gri
           idx = -1 - stm + u;
           if (idx >= N) idx -= N;
         }
+        DSFT_CHECK(idx >= 0 && idx < N);
         buf[i] = ld_stream(fv + idx);
       }
     }
@@ -325,6 +327,7 @@ __global__ void __launch_bounds__(kK1GenThreads) k1_gather_mix_gen(const __grid_
       idx %= N;
       if (idx < 0) idx += N;
     }
+    DSFT_CHECK(idx >= 0 && idx < N);
     return ldg2(fv + idx);
   };
   const double G0 = exp(g.d0 * g.d0 * p.neg_half_inv_c1sq) * p.inv_c1N;
@@ -882,6 +885,7 @@ __device__ __forceinline__ void median_warp(const K5aParams& p, int v, int j, in
       double re = INFINITY, im = INFINITY;
       if (my_t >= 0) {
         const int64_t slot = p.off[my_t] + pmod(om, p.P[my_t]);
+        DSFT_CHECK(slot >= 0 && slot < p.sumP && my_i < p.Kmax);
         const double2 y = p.cand_v[(base + slot) * p.Kmax + my_i];
         re = sgn * y.x;
         im = sgn * y.y;
@@ -1216,6 +1220,7 @@ __device__ void merge_range(const K6Params& p, int v, int64_t e_lo, int64_t e_hi
     if (sub != 0 || e >= hi) continue;
     if (e < n) {
       rank += i;
+      DSFT_CHECK(rank >= 0);
       if (rank < p.s) {
         ow[rank] = w;
         oc[rank] = ldcg2(bc + sl);
@@ -1297,9 +1302,11 @@ __global__ void __launch_bounds__(256) k5s_scan(const __grid_constant__ K5Params
   }
   if (__popcll(mk) < p.vote_min) return;
   const int pos = atomicAdd(p.acc_n + (int64_t)v * p.b.bn_vec + j, 1);
+  DSFT_CHECK(pos >= 0 && pos < p.b.sumP);
   p.acc_w[base + pos] = __ldcg(p.cand_w + (int64_t)v * p.b.cw_vec_stride + gid);
   p.acc_mask[base + pos] = mk;
   const int gpos = atomicAdd(p.work_n + v, 1);
+  DSFT_CHECK(gpos >= 0 && gpos < p.b.cw_vec_stride);
   p.work[(int64_t)v * p.b.cw_vec_stride + gpos] = ((int64_t)j << 32) | (int64_t)pos;
 }
 
@@ -1419,6 +1426,31 @@ __global__ void k_debug_grid(const __grid_constant__ DbgParams p) {
     }
     p.out[k] = cscale(acc, 1.0 / (double)p.L);
   }
+}
+
+// ================================================================ guard check
+struct GuardParams {
+  const unsigned char* ws;
+  size_t off[32];
+};
+
+__global__ void k_check_guards(const __grid_constant__ GuardParams p) {
+  const unsigned char* g = p.ws + p.off[blockIdx.x];
+  for (int i = threadIdx.x; i < (int)kGuardBytes; i += blockDim.x)
+    if (g[i] != 0xA5) {
+      printf("dsft: workspace guard zone %d (offset %llu) overwritten at byte %d\n", (int)blockIdx.x,
+             (unsigned long long)p.off[blockIdx.x], i);
+      __trap();
+    }
+}
+
+cudaError_t launch_check_guards(const WsLayout& L, void* ws, cudaStream_t st) {
+  if (!kGuardBytes || L.nguard == 0) return cudaSuccess;
+  GuardParams g{};
+  g.ws = (const unsigned char*)ws;
+  for (int i = 0; i < L.nguard; ++i) g.off[i] = L.guard[i];
+  k_check_guards<<<L.nguard, 64, 0, st>>>(g);
+  return cudaGetLastError();
 }
 
 // ================================================================= launchers

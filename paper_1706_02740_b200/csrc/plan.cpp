@@ -362,9 +362,14 @@ WsLayout ws_layout(const Plan& p, int64_t nvec) {
   L.band_vec = (int64_t)p.J * p.info.band_budget;
   L.bn_vec = p.J;
   size_t o = 0;
+  L.nguard = 0;
   auto take = [&](size_t bytes) {
     size_t at = o;
     o = align256(o + bytes);
+    if (kGuardBytes && L.nguard < 32) {  // DSFT_CHECKED: guard zone after the region
+      L.guard[L.nguard++] = o;
+      o += kGuardBytes;
+    }
     return at;
   };
   L.z_buf = nvec * L.z_vec;
@@ -797,7 +802,10 @@ static void specialise_k2(Plan& P) {
     th.emplace_back([&, t, dev] {
       cudaSetDevice(dev);
       Bucket& bb = P.bk[t];
+      // (measured round 2: three CTAs per SM at an 80-register cap where three rows fit
+      // shared memory -- no spills -- ran 2706 vs 2823 transforms/s at BASELINE config 2)
       int nt = bb.fft_threads, minb = bb.fft_variant == 1 ? 2 : 1;
+
       if (bb.cl) {  // cluster kernel: blocks of M / C elements, 256 threads, 2 CTAs per SM
         bb.jit_threads = 256;
         bb.k2_jit = jit_k2(256, 2, bb.fac, bb.nfac, (size_t)(bb.M / bb.cl) * 16, &why[t], true);
@@ -1004,7 +1012,15 @@ size_t dsft_plan_workspace_bytes(const dsft_plan* pl, int64_t batch) {
 // K5 counters start at zero (the last K5b CTA of a vector re-zeroes them after use)
 static dsft_status zero_tickets(Plan& p) {
   const WsLayout L = ws_layout(p, p.ws_batch);
-  CU(cudaMemset((char*)p.ws + L.acc_n, 0, L.work - L.acc_n), "zero K5 counters");
+#ifdef DSFT_CHECKED
+  // poison the whole workspace (0xFF bytes: NaN doubles, -1 integers) so a read of a
+  // value no kernel wrote corrupts the result, then lay the guard patterns
+  CU(cudaMemset(p.ws, 0xFF, L.total), "poison workspace");
+  for (int g = 0; g < L.nguard; ++g) CU(cudaMemset((char*)p.ws + L.guard[g], 0xA5, kGuardBytes), "guard zone");
+#endif
+  CU(cudaMemset((char*)p.ws + L.acc_n, 0, (size_t)p.ws_batch * L.bn_vec * 4), "zero K5 counters");
+  CU(cudaMemset((char*)p.ws + L.work_n, 0, (size_t)p.ws_batch * 4), "zero K5 counters");
+  CU(cudaMemset((char*)p.ws + L.ticket, 0, (size_t)p.ws_batch * 4), "zero merge tickets");
   CU(cudaDeviceSynchronize(), "zero merge tickets (sync)");
   return DSFT_OK;
 }
@@ -1237,6 +1253,7 @@ static dsft_status execute_impl(dsft_plan* pl, const dsft_c128* f, int64_t batch
       dsft_status r = run_bands(p, (const double2*)f + v0 * ld, ld, nv, bands.data(), p.J, s0, freqs + v0 * p.s,
                                 (double2*)coeffs + v0 * p.s);
       if (r != DSFT_OK) return r;
+      if (kGuardBytes) CU(launch_check_guards(ws_layout(p, p.ws_batch), p.ws, s0), "workspace guard check");
     }
     return DSFT_OK;
   };
@@ -1390,9 +1407,14 @@ int64_t dsft_plan_collect_timeline(dsft_plan* pl, double* rows, int64_t n) {
 int64_t dsft_plan_launches_per_execute(const dsft_plan* pl) {
   if (!pl) return 0;
   if (small_plan(pl->p))  // K1, K2 (one or per prime), K3, fused tail (+ K6 above kTailMergeMaxS)
-    return 2 + (k2_multi_ok(pl->p) ? 1 : pl->p.T) + (pl->p.s <= kTailMergeMaxS ? 2 : 3);
+  {
+    int64_t k2n = 0;  // K2 launches: one multi-prime launch, or per prime (split rows: K2a + K2b)
+    for (int t = 0; t < pl->p.T; ++t) k2n += (pl->p.bk[t].split && !(pl->p.bk[t].cl && pl->p.bk[t].k2_jit)) ? 2 : 1;
+    return 2 + (k2_multi_ok(pl->p) ? 1 : k2n) + (pl->p.s <= kTailMergeMaxS ? 2 : 3);
+  }
   int64_t n = 4;  // K5 scan, K5 medians, K5 select, K6 merge
-  for (int t = 0; t < pl->p.T; ++t) n += 3 + (pl->p.bk[t].split ? 1 : 0);  // K1, K2 (K2a + K2b), K3
+  for (int t = 0; t < pl->p.T; ++t)  // K1, K2 (split rows: K2a + K2b), K3
+    n += 3 + ((pl->p.bk[t].split && !(pl->p.bk[t].cl && pl->p.bk[t].k2_jit)) ? 1 : 0);
   return n;
 }
 
