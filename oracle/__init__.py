@@ -32,7 +32,10 @@ Parity status per function (DESIGN.md §4 lists the pin for each):
   dsft.merge               pinned (brute-force sort, zero drop)
   dsft.dsft (end to end)   pinned (brute-force DFT on tiny N; Theorem 5 bound;
                            passband-edge and B-extreme tones)
-  scripts/mutation_check.py applies 18 plausible mistakes to the oracle; every one
+  dsft.clw_decode / identify_clw (CLW-style inner SFT, reading R14)
+                           pinned (exhaustive decoding of exact shifted measurements on
+                           tiny N, shifted-grid closed form, brute-force DFT end to end)
+  scripts/mutation_check.py applies 24 plausible mistakes to the oracle; every one
   fails at least one `-m "not gpu"` test.
   inner-SFT design constants (c_b, T, v_min, pool rule, residue rule):
                            parity unpinned -- the paper prints no values for

@@ -38,25 +38,28 @@ def nearest_grid_index(k, N: int, L: int):
     return (2 * k * N + L) // (2 * L)
 
 
-def filtered_samples(f: np.ndarray, plan: Plan, q: int, L: int) -> np.ndarray:
-    """h_q(x_k) for the L nodes x_k = -pi + 2 pi k / L, k = 0..L-1.
+def filtered_samples(f: np.ndarray, plan: Plan, q: int, L: int, m: int = 0) -> np.ndarray:
+    """h_q(x_k) for the L nodes x_k = -pi + 2 pi k / L + 2 pi m / N, k = 0..L-1
+    (m = 0: the aliasing grid itself; m > 0: the grid shifted by m steps of f, the
+    shifted measurements of the CLW-style inner SFT, reading R14).
 
     h_q(x) = (1/N) sum_{u=-kappa..kappa} f_{(j'+u) mod N} exp(i q d_u) g(d_u),
     d_u = x - y_{j'+u},  j' = argmin_j |x - y_j|  (Lemma 10, PAPER.md:454-457;
     indices mod N as in PAPER.md:477), g restricted to its n = 0 image (R5),
     modulation exp(+i q d) so that the passband is centred at q (R1).
-    j' = round(kN/L) computed exactly in integers; L is odd so no ties (R3).
-    The offset d_u is formed from the exact integer num = kN - jL.
+    j' = round(kN/L) computed exactly in integers; L is odd so no ties (R3).  A shift
+    by m whole steps of f moves the nearest grid point by exactly m: j' + m.
+    The offset d_u is formed from the exact integer num = kN + mL - jL.
     """
     N = plan.N
     c1 = plan.c1
     NL = N * L
     k = np.arange(L, dtype=np.int64)
-    jp = nearest_grid_index(k, N, L)
+    jp = nearest_grid_index(k, N, L) + m
     acc = np.zeros(L, dtype=np.complex128)
     for u in range(-plan.kappa, plan.kappa + 1):
         j = jp + u
-        num = k * N - j * L
+        num = k * N + m * L - j * L
         d = 2.0 * math.pi * num / NL
         G = np.exp(-(d * d) / (2.0 * c1 * c1)) / c1
         rho = (q * num) % NL
@@ -72,8 +75,12 @@ def alias_dft(h: np.ndarray) -> np.ndarray:
 
 
 def band_measurements(f: np.ndarray, plan: Plan, j: int) -> list[list[np.ndarray]]:
-    """Y[t][i] = alias_dft(filtered_samples(f, q_j, L_{t,i})) for every grid."""
+    """Y[t][i] = alias_dft(filtered_samples(f, q_j, L_{t,i})) for every grid.
+    CLW (reading R14): Y[t][sigma] for the grid of length P_t shifted by m_sigma."""
     q = plan.q[j]
+    if plan.inner == "clw":
+        return [[alias_dft(filtered_samples(f, plan, q, plan.primes[t], m)) for m in plan.shifts[t]]
+                for t in range(plan.T)]
     return [[alias_dft(filtered_samples(f, plan, q, L)) for L in plan.grid_lengths(t)]
             for t in range(plan.T)]
 
@@ -142,6 +149,74 @@ def identify(plan: Plan, j: int, t: int, Yt: list[np.ndarray]) -> Identification
     ok = om != SENTINEL
     ok &= (om >= q - plan.w) & (om < q + plan.w) & (om >= plan.B_lo) & (om <= plan.B_hi)
     cand = np.where(ok, om, SENTINEL)
+    return Identification(cand=cand, gap=gap)
+
+
+def clw_decode(E: list[complex], shifts: list[int], b: int, P: int, q: int, N: int) -> tuple[int, float]:
+    """Reading R14 (the CLW-style phase-encoding identification, SPEC.md
+    Design Decisions of the inner SFT): one bucket b of a length-P grid.  For an
+    isolated omega' in bucket b the shifted measurements satisfy
+    E_sigma[b] = E_0[b] exp(2 pi i omega' m_sigma / N) (aliasing identity,
+    PAPER.md:847, on the shifted grid), so with n = omega' - lo, lo = min(q + B):
+      theta_sigma = arg(E_sigma conj(E_0)) / (2 pi) = m_sigma n / N + m_sigma lo / N  (mod 1).
+    Scales m = 1, 2, 4, ... refine v ~ n / N coarse to fine: the first gives
+    v = phi = theta - frac(m lo / N) (mod 1); each next one v <- (phi + k) / m with the
+    integer k nearest to m v - phi.  The phases fix n only modulo N, so the estimate
+    n_est = N (v mod 1) is circular: the bucket fixes the low digits by taking, over the
+    three lifts n_est - N, n_est, n_est + N, the integer c = b - lo (mod P) nearest to
+    each that lies in [0, N), and keeping the closest.  omega' = lo + c.  Returns
+    (omega' or SENTINEL for an empty bucket, decision margin: the smallest distance of a
+    rounded quantity from its rounding boundary, in units of its step)."""
+    E0 = E[0]
+    if E0.real == 0.0 and E0.imag == 0.0:
+        return SENTINEL, math.inf
+    lo = q - (N + 1) // 2 + 1
+    v = None
+    margin = math.inf
+    for Es, m in zip(E[1:], shifts[1:]):
+        r = Es * E0.conjugate()
+        theta = math.atan2(r.imag, r.real) / (2.0 * math.pi)
+        phi = (theta - ((m * lo) % N) / N) % 1.0
+        if v is None:
+            v = phi
+        else:
+            x = m * v - phi
+            k = math.floor(x + 0.5)
+            margin = min(margin, abs(abs(x - k) - 0.5))
+            v = (phi + k) / m
+    n_est = N * (v % 1.0)
+    rb = (b - lo) % P
+    best, d1, d2 = None, math.inf, math.inf
+    for lift in (-N, 0, N):
+        y = (n_est + lift - rb) / P
+        c = rb + P * math.floor(y + 0.5)
+        margin = min(margin, abs(abs(y - math.floor(y + 0.5)) - 0.5))
+        if 0 <= c < N:
+            dist = abs(c - (n_est + lift))
+            if dist < d1:
+                best, d1, d2 = c, dist, d1
+            elif dist < d2:
+                d2 = dist
+    if best is None:
+        return SENTINEL, margin
+    if d2 < math.inf:
+        margin = min(margin, (d2 - d1) / P)
+    return lo + best, margin
+
+
+def identify_clw(plan: Plan, j: int, t: int, Et: list[np.ndarray]) -> Identification:
+    """Reading R14 identification for bucket prime t of band j: clw_decode in every
+    bucket b < P_t, kept only if omega' lies in the passband [q - w, q + w) cap B
+    (line 10)."""
+    P = plan.primes[t]
+    q = plan.q[j]
+    cand = np.full(P, SENTINEL, dtype=np.int64)
+    gap = np.full(P, np.inf)
+    for b in range(P):
+        om, mg = clw_decode([E[b] for E in Et], plan.shifts[t], b, P, q, plan.N)
+        gap[b] = mg
+        if om != SENTINEL and q - plan.w <= om < q + plan.w and plan.B_lo <= om <= plan.B_hi:
+            cand[b] = om
     return Identification(cand=cand, gap=gap)
 
 
@@ -247,7 +322,11 @@ class DsftResult:
 def process_band(f: np.ndarray, plan: Plan, j: int) -> BandResult:
     """Algorithm 1 lines 4-12 for band j (0-based)."""
     Y = band_measurements(f, plan, j)
-    ids = [identify(plan, j, t, Y[t]) for t in range(plan.T)]
+    if plan.inner == "clw":  # reading R14; the estimate reads the unshifted grid (Y[t][0])
+        ids = [identify_clw(plan, j, t, Y[t]) for t in range(plan.T)]
+        Y = [[Y[t][0]] for t in range(plan.T)]
+    else:
+        ids = [identify(plan, j, t, Y[t]) for t in range(plan.T)]
     accepted = vote(plan, ids)
     oms, cs, zs, gaps = estimate(plan, j, Y, ids, accepted)
     # margin audit: argmax gaps in every bucket that can touch an accepted or

@@ -48,6 +48,7 @@ class OracleParams:
     band_budget: int = 0           # 0 = s (reading R11)
     seed: int = 0
     pool_rule: str = "smooth"      # reading R6: "full" = every prime of the range, "smooth" = 13-smooth P-1
+    inner: str = "gfft"            # inner SFT of line 9: "gfft" (readings R7-R10) or "clw" (reading R14)
 
 
 @dataclass
@@ -71,6 +72,8 @@ class Plan:
     vote_min: int = 3
     band_budget: int = 0
     seed: int = 0
+    inner: str = "gfft"
+    shifts: list[list[int]] = field(default_factory=list)  # CLW (R14): grid shifts m_sigma per prime
 
     @property
     def T(self) -> int:
@@ -132,6 +135,18 @@ def residue_moduli(P: int, N: int) -> list[int]:
     if best is None:
         raise ConfigError("no set of residue primes below the bucket prime reaches N")
     return list(best[2])
+
+
+def clw_shifts(P: int, N: int) -> list[int]:
+    """Reading R14: the grid shifts m_sigma (in steps 2 pi / N of f) of the CLW-style
+    inner SFT for bucket prime P: 0 (the unshifted grid), then 1, 2, 4, ..., 2^(L-1)
+    with L = ceil(log2(N / P)) + 1, the fewest dyadic scales after which the frequency
+    estimate is within P/4 of the truth whenever every phase error is below pi/2
+    (so the congruence omega = b (mod P) fixes it)."""
+    L = 1
+    while (1 << (L - 1)) * P < N:
+        L += 1
+    return [0] + [1 << l for l in range(L)]
 
 
 def derive_plan(N: int, s: int, params: OracleParams | None = None) -> Plan:
@@ -200,7 +215,16 @@ def derive_plan(N: int, s: int, params: OracleParams | None = None) -> Plan:
         primes = draw_distinct(pool, T, p.seed)
     if T < 1:
         raise ConfigError("need at least one bucket prime")
-    residues = [residue_moduli(P, N) for P in primes]
+    if p.inner == "gfft":
+        residues = [residue_moduli(P, N) for P in primes]
+        shifts = []
+    elif p.inner == "clw":
+        # Reading R14: one grid of length P_t (residue list [1]) sampled unshifted and
+        # shifted by m = 1, 2, 4, ..., 2^(L-1) steps of f, L = ceil(log2(N/P_t)) + 1
+        residues = [[1] for _ in primes]
+        shifts = [clw_shifts(P, N) for P in primes]
+    else:
+        raise ConfigError(f"unknown inner {p.inner!r}")
     # vote_min 0: "more than half" of the T primes
     vote_min = T // 2 + 1 if int(p.vote_min) == 0 else int(p.vote_min)
     if not (1 <= vote_min <= T):
@@ -209,4 +233,5 @@ def derive_plan(N: int, s: int, params: OracleParams | None = None) -> Plan:
 
     return Plan(N=N, s=s, preset=p.preset, kappa=kappa, beta=beta, c1=c1, tau=p.tau,
                 alpha=alpha, w=w, J=J, q=q, B_lo=B_lo, B_hi=B_hi, pool=pool, primes=primes,
-                residues=residues, vote_min=vote_min, band_budget=budget, seed=int(p.seed))
+                residues=residues, vote_min=vote_min, band_budget=budget, seed=int(p.seed),
+                inner=p.inner, shifts=shifts)

@@ -47,6 +47,16 @@ MUTANTS = [
     ("merge keeps zeros", "oracle/dsft.py", "if not (c.real == 0.0 and c.imag == 0.0)]", "]"),
     ("window kappa - 1", "oracle/dsft.py", "for u in range(-plan.kappa, plan.kappa + 1):",
      "for u in range(-plan.kappa + 1, plan.kappa):"),
+    # CLW-style inner SFT (reading R14)
+    ("clw: phase not offset by lo", "oracle/dsft.py", "phi = (theta - ((m * lo) % N) / N) % 1.0",
+     "phi = theta % 1.0"),
+    ("clw: floor in refinement", "oracle/dsft.py", "            k = math.floor(x + 0.5)",
+     "            k = math.floor(x)"),
+    ("clw: no circular lift", "oracle/dsft.py", "for lift in (-N, 0, N):", "for lift in (0,):"),
+    ("clw: shift sign", "oracle/dsft.py", "num = k * N + m * L - j * L", "num = k * N - m * L - j * L"),
+    ("clw: estimate on shifted grid", "oracle/dsft.py", "Y = [[Y[t][0]] for t in range(plan.T)]",
+     "Y = [[Y[t][1]] for t in range(plan.T)]"),
+    ("clw: one scale fewer", "oracle/params.py", "while (1 << (L - 1)) * P < N:", "while (1 << L) * P < N:"),
 ]
 
 
