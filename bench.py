@@ -357,6 +357,21 @@ def run_ours(a):
                               ">= 2(P-1)-1); smooth = primes with 13-smooth P-1 (DESIGN.md R6)"}
         plan2.close()
 
+    # ---- the CLW-style inner SFT (reading R14) on the same vector, same protocol
+    clw = None
+    if world == 1 and mode == "single":
+        plan3 = d.Plan(N, s, d.make_params(seed=a.seed, pool_rule=a.pool, inner="clw"))
+        for _ in range(a.warmup):
+            step(plan3, f, "single")
+        torch.cuda.synchronize()
+        fr3 = freqs[:s].cpu().numpy()
+        cms = timed_loop(max(10, a.steps // 2), md="single", p=plan3)
+        clw = {"inner": "clw", "value": 1.0 / (cms / 1e3), "unit": UNIT, "ms_per_step": cms,
+               "support_exact": sorted(fr3[fr3 != d.SENTINEL].tolist()) == pl.freqs.tolist(),
+               "shift_rows_per_prime": [plan3.info.n_shifts[t] for t in range(plan3.info.T)],
+               "note": "DMSFT-6 window with the phase-encoding inner SFT (CLW-DSFT family, PAPER.md:653)"}
+        plan3.close()
+
     # ---- kernel breakdown: a second pass with per-launch CUDA events on each launch's stream
     plan.dsft_plan_set_timing(True)
     kpass = max(10, min(a.steps, 50))
@@ -504,6 +519,7 @@ def run_ours(a):
         "support_exact": bool(support_exact),
         "band_sharded": band,
         "other_pool": other_pool,
+        "inner_clw": clw,
         "e2e": e2e,
         "cpu_baseline": cpu,
         "clocks": clocks,

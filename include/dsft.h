@@ -67,6 +67,14 @@ enum { DSFT_ALPHA_CORRECTED = 0, DSFT_ALPHA_LITERAL = 1 };
  * factor above 13 (every length-P DFT is then a Rader convolution over a 13-smooth
  * FFT; the general primes of FULL use a Bluestein chirp-z convolution). */
 enum { DSFT_POOL_FULL = 0, DSFT_POOL_SMOOTH = 1 };
+/* Inner SFT of Algorithm 1 line 9 (Section 5):
+ *  GFFT  the DMSFT family's randomized GFFT reading (R7-R10): residue
+ *        grids P_t r_i, argmax + CRT identification, majority vote
+ *  CLW   the CLW-DSFT family's phase encoding (R14): the length-P_t grid
+ *        unshifted and shifted by 1, 2, 4, ..., 2^(L-1) steps of f, frequencies
+ *        decoded from the phase ratios of each bucket, majority vote; the paper runs
+ *        it with kappa = 12..20 (use dsft_params.kappa) */
+enum { DSFT_INNER_GFFT = 0, DSFT_INNER_CLW = 1 };
 /* dsft_params.flags (execution options; results are bitwise identical either way):
  *  NO_JIT       no plan-time NVRTC specialisation (runtime-parameter K2/K3 kernels)
  *  NO_CLUSTER   rows above one CTA's shared memory use the two-launch split K2
@@ -100,7 +108,8 @@ enum {
  *  band_budget   entries kept per band after line 9 (0 = s; reading R11)
  *  seed          SplitMix64 seed of the bucket-prime draw (reading R7)
  *  pool_rule     DSFT_POOL_FULL or DSFT_POOL_SMOOTH (reading R6)
- *  flags         DSFT_FLAG_* execution options (above)                     */
+ *  flags         DSFT_FLAG_* execution options (above)
+ *  inner         DSFT_INNER_GFFT (default) or DSFT_INNER_CLW (reading R14)   */
 typedef struct {
   int32_t preset;
   double r;
@@ -114,6 +123,7 @@ typedef struct {
   uint64_t seed;
   int32_t pool_rule;
   uint32_t flags;
+  int32_t inner;
 } dsft_params;
 
 /* Derived plan quantities, for oracle cross-checks (read-only copy). */
@@ -126,12 +136,13 @@ typedef struct {
   int32_t vote_min;
   int64_t band_budget;
   int64_t primes[DSFT_MAX_T];   /* P_t ascending                               */
-  int32_t n_residues[DSFT_MAX_T];
-  int32_t residues[DSFT_MAX_T][DSFT_MAX_K];
-  int32_t n_shifts[DSFT_MAX_T]; /* S_t = 1 + sum_i (r_{t,i} - 1)               */
+  int32_t n_residues[DSFT_MAX_T];  /* CLW: 1                                     */
+  int32_t residues[DSFT_MAX_T][DSFT_MAX_K];  /* CLW: residues[t][0] = 1          */
+  int32_t n_shifts[DSFT_MAX_T]; /* S_t = 1 + sum_i (r_{t,i} - 1); CLW: 1 + L_t    */
   int64_t nodes;                /* sum_t S_t P_t: distinct sample nodes        */
   int64_t grid_points;          /* sum_t sum_i P_t r_{t,i}                     */
   int64_t sum_primes;           /* sum_t P_t                                   */
+  int32_t inner;                /* DSFT_INNER_*                                */
 } dsft_plan_info;
 
 void dsft_params_default(dsft_params* p);
@@ -277,7 +288,8 @@ dsft_status dsft_execute_batched_sharded(dsft_plan* plan, dsft_comm* comm, const
  * dsft_debug_grid: run K1 (what = 0: filtered samples h_q(x_k), k < L) or
  * K1+K2 (what = 1: E[b] = (1/L) sum_k h_q(x_k) e^{-2 pi i k b/L}, b < L) of
  * band `band`, bucket prime t, residue i, grid L = P_t r_{t,i}, into
- * out_dev[L] in natural order.
+ * out_dev[L] in natural order.  CLW plans: i selects the grid shift sigma
+ * (0 <= i < n_shifts[t]; nodes x_k + 2 pi m_sigma / N, L = P_t).
  * dsft_debug_copy: after an execute, copy an internal buffer of vector 0:
  *   which = 0: candidates  int64 [J][sum_t P_t]   (omega' or INT64_MIN)
  *   which = 1: band counts int32 [J]

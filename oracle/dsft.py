@@ -206,18 +206,56 @@ def clw_decode(E: list[complex], shifts: list[int], b: int, P: int, q: int, N: i
 
 def identify_clw(plan: Plan, j: int, t: int, Et: list[np.ndarray]) -> Identification:
     """Reading R14 identification for bucket prime t of band j: clw_decode in every
-    bucket b < P_t, kept only if omega' lies in the passband [q - w, q + w) cap B
-    (line 10)."""
+    bucket b < P_t (here elementwise over the buckets with numpy, the same operations
+    in the same order; pinned to the scalar clw_decode by
+    tests/test_oracle_clw.py::test_identify_clw_matches_decode_per_bucket), kept only
+    if omega' lies in the passband [q - w, q + w) cap B (line 10)."""
     P = plan.primes[t]
     q = plan.q[j]
-    cand = np.full(P, SENTINEL, dtype=np.int64)
+    N = plan.N
+    shifts = plan.shifts[t]
+    b = np.arange(P, dtype=np.int64)
+    E0 = Et[0]
+    live = ~((E0.real == 0.0) & (E0.imag == 0.0))
+    lo = q - (N + 1) // 2 + 1
     gap = np.full(P, np.inf)
-    for b in range(P):
-        om, mg = clw_decode([E[b] for E in Et], plan.shifts[t], b, P, q, plan.N)
-        gap[b] = mg
-        if om != SENTINEL and q - plan.w <= om < q + plan.w and plan.B_lo <= om <= plan.B_hi:
-            cand[b] = om
-    return Identification(cand=cand, gap=gap)
+    v = None
+    for Es, m in zip(Et[1:], shifts[1:]):
+        re = Es.real * E0.real + Es.imag * E0.imag          # Es conj(E0), no contraction
+        im = Es.real * (-E0.imag) + Es.imag * E0.real
+        theta = np.arctan2(im, re) / (2.0 * math.pi)
+        phi = (theta - ((m * lo) % N) / N) % 1.0
+        if v is None:
+            v = phi
+        else:
+            x = m * v - phi
+            k = np.floor(x + 0.5)
+            gap = np.minimum(gap, np.abs(np.abs(x - k) - 0.5))
+            v = (phi + k) / m
+    n_est = N * (v % 1.0)
+    rb = (b - lo) % P
+    best = np.full(P, -1, dtype=np.int64)
+    d1 = np.full(P, np.inf)
+    d2 = np.full(P, np.inf)
+    for lift in (-N, 0, N):
+        y = (n_est + lift - rb) / P
+        fl = np.floor(y + 0.5)
+        gap = np.minimum(gap, np.abs(np.abs(y - fl) - 0.5))
+        c = rb + P * fl.astype(np.int64)
+        ok = (c >= 0) & (c < N)
+        dist = np.abs(c - (n_est + lift))
+        better = ok & (dist < d1)
+        second = ok & ~better & (dist < d2)
+        d2 = np.where(better, d1, np.where(second, dist, d2))
+        best = np.where(better, c, best)
+        d1 = np.where(better, dist, d1)
+    with np.errstate(invalid="ignore"):  # (inf - inf where no second candidate: not used)
+        gap = np.where(np.isfinite(d2), np.minimum(gap, (d2 - d1) / P), gap)
+    om = lo + best
+    ok = live & (best >= 0)
+    ok &= (om >= q - plan.w) & (om < q + plan.w) & (om >= plan.B_lo) & (om <= plan.B_hi)
+    gap = np.where(live, gap, np.inf)
+    return Identification(cand=np.where(ok, om, SENTINEL), gap=gap)
 
 
 def window_representative(R, M: int, q: int, N: int):

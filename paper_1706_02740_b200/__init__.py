@@ -25,6 +25,7 @@ DSFT_ERR_NCCL, DSFT_ERR_NOMEM, DSFT_ERR_INTERNAL, DSFT_ERR_UNSUPPORTED = 5, 6, 7
 PRESETS = {"dmsft6": 0, "dmsft4": 1, "thm4": 2}
 ALPHA_RULES = {"corrected": 0, "literal": 1}
 POOL_RULES = {"full": 0, "smooth": 1}
+INNERS = {"gfft": 0, "clw": 1}
 FLAG_NO_JIT, FLAG_NO_CLUSTER, FLAG_HOST_COPY, FLAG_HOST_MAPPED, FLAG_SERIAL, FLAG_NO_GRAPH = 1, 2, 4, 8, 16, 32
 SENTINEL = -(1 << 63)
 
@@ -39,7 +40,7 @@ class dsft_params(C.Structure):
     _fields_ = [("preset", C.c_int32), ("r", C.c_double), ("kappa", C.c_int32), ("tau", C.c_double),
                 ("alpha_rule", C.c_int32), ("bucket_factor", C.c_double), ("n_bucket_primes", C.c_int32),
                 ("vote_min", C.c_int32), ("band_budget", C.c_int64), ("seed", C.c_uint64),
-                ("pool_rule", C.c_int32), ("flags", C.c_uint32)]
+                ("pool_rule", C.c_int32), ("flags", C.c_uint32), ("inner", C.c_int32)]
 
 
 class dsft_plan_info(C.Structure):
@@ -49,7 +50,7 @@ class dsft_plan_info(C.Structure):
                 ("band_budget", C.c_int64), ("primes", C.c_int64 * DSFT_MAX_T),
                 ("n_residues", C.c_int32 * DSFT_MAX_T), ("residues", (C.c_int32 * DSFT_MAX_K) * DSFT_MAX_T),
                 ("n_shifts", C.c_int32 * DSFT_MAX_T), ("nodes", C.c_int64), ("grid_points", C.c_int64),
-                ("sum_primes", C.c_int64)]
+                ("sum_primes", C.c_int64), ("inner", C.c_int32)]
 
 
 _P = C.c_void_p
@@ -127,7 +128,7 @@ def _check(st: int) -> None:
 def make_params(preset: str = "dmsft6", r: float = 1.0, kappa: int = 0, tau: float = 1.0 / 3.0,
                 alpha_rule: str = "corrected", bucket_factor: float = 4.0, n_bucket_primes: int = 5,
                 vote_min: int = 3, band_budget: int = 0, seed: int = 0, pool_rule: str | None = None,
-                flags: int = 0) -> dsft_params:
+                flags: int = 0, inner: str = "gfft") -> dsft_params:
     """dsft_params from keyword values (pool_rule None = the library default)."""
     p = dsft_params()
     lib().dsft_params_default(C.byref(p))
@@ -139,6 +140,7 @@ def make_params(preset: str = "dmsft6", r: float = 1.0, kappa: int = 0, tau: flo
     if pool_rule is not None:
         p.pool_rule = POOL_RULES[pool_rule]
     p.flags = flags
+    p.inner = INNERS[inner]
     return p
 
 

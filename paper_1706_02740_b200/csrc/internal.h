@@ -52,6 +52,7 @@ struct Bucket {
   int shift_r[kMaxShifts] = {};
   int shift_n2[kMaxShifts] = {};
   int shift_base[DSFT_MAX_K] = {};  // sigma of (i, n2=1)
+  int64_t shift_off[kMaxShifts] = {};  // window offset of shift sigma in steps of f (CLW grid shifts; 0 for GFFT)
   int64_t off = 0;           // sum_{t'<t} P_t'
   int64_t crtM = 0;          // P * prod r
   int64_t crtE[DSFT_MAX_K + 1] = {};  // CRT coefficients for moduli (P, r_0, ...)
@@ -92,6 +93,7 @@ struct Bucket {
   int* shift_r_dev = nullptr;   // [S] K1 shift tables (copies of shift_r, shift_n2, 2 pi / (N P r))
   int* shift_n2_dev = nullptr;
   double* shift_scale_dev = nullptr;
+  const int64_t* shift_off_dev = nullptr;
   double2* bhat = nullptr;      // [R_last][M/R_last] FFT_M(b)/M, DIF output position blk*R_last + c stored
                                 // at c*(M/R_last) + blk; b_m = exp(-2 pi i g^-m / P)
   double2* tw = nullptr;        // [ntw] per DIF stage s (span n_s, m_s = n_s/R_s): exp(-2 pi i floor(k/in_s) / d_s),

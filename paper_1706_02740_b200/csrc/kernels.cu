@@ -51,6 +51,7 @@ struct K1Prime {
   const int* shift_r;    // [S] residue prime of shift sigma (1 for the P-subgrid)   (device tables)
   const int* shift_n2;   // [S] n2 of shift sigma
   const double* shift_scale;  // [S] 2 pi / (N L_sigma)
+  const int64_t* shift_off;   // [S] window offset in steps of f (CLW grid shifts, reading R14; 0 for GFFT)
 };
 
 struct K1Params {
@@ -105,7 +106,8 @@ __device__ __forceinline__ NodeGeo node_geo(const K1Prime& p, int64_t N, int sig
   // j' = round(kN / L): L is odd, so 2kN + L is never an exact multiple tie (R3).
   const int64_t jp = (2 * k * N + L) / (2 * L);
   const int64_t num0 = k * N - jp * L;  // (x - y_j') N L / (2 pi), exact
-  return NodeGeo{jp, (double)num0 * __ldg(p.shift_scale + sigma)};
+  // a grid shifted by m whole steps of f moves j' by m and leaves x - y_j' unchanged
+  return NodeGeo{jp + __ldg(p.shift_off + sigma), (double)num0 * __ldg(p.shift_scale + sigma)};
 }
 
 // Fast path (KAPPA in {4, 6}): each warp stages the 32 windows of its nodes in
@@ -133,7 +135,8 @@ __device__ __forceinline__ NodeGeo node_geo_fast(const K1Prime& p, int64_t N, in
     --jp;
     num0 += L;
   }
-  return NodeGeo{jp, (double)num0 * __ldg(p.shift_scale + sigma)};
+  // a grid shifted by m whole steps of f moves j' by m and leaves x - y_j' unchanged
+  return NodeGeo{jp + __ldg(p.shift_off + sigma), (double)num0 * __ldg(p.shift_scale + sigma)};
 }
 
 // Output slot of global band j in the listed bands, or -1
@@ -758,6 +761,107 @@ __global__ void __launch_bounds__(256) k3_identify_multi(const __grid_constant__
   k3_body<RMAX, 0>(p.pr[i], (int64_t)((int)blockIdx.x - p.cta_off[i]) * blockDim.x + threadIdx.x);
 }
 
+
+// ================================================== K3 CLW (phase decoding)
+// Reading R14 (the CLW-style inner SFT): thread per (band,
+// bucket).  E_sigma = X_sigma[b] / P of the grid shifted by m_sigma steps of f; for
+// an isolated omega' in bucket b, E_sigma = E_0 exp(2 pi i omega' m_sigma / N), so the
+// phase ratios refine v ~ (omega' - lo) / N coarse to fine and the bucket congruence
+// fixes the low digits (oracle.dsft.clw_decode: same operations in the same order,
+// roundings forced with __d*_rn so no contraction changes a decision).  Candidates
+// only: the vote is counted by K5s probing every prime's bucket.  One launch may
+// cover several bucket primes (CTAs [cta_off[i], cta_off[i+1]) take prime i).
+constexpr int kClwMaxS = 40;
+constexpr int kClwMaxT = 48;
+struct K3ClwPrime {
+  const double2* Z;
+  int64_t z_vec_stride;
+  int P, S;
+  int64_t off;             // slot offset of this prime in the band's candidate row
+  const uint16_t* binat;   // [P-1] bucket at array position (Rader order of K2's output)
+  int64_t shift[kClwMaxS]; // m_sigma
+};
+struct K3ClwParams {
+  int nprime, nb, Kmax, pad_;
+  int cta_off[kClwMaxT + 1];
+  int64_t N, qfirst, qstep, halfN_up, halfN_dn, w, B_lo, B_hi;
+  int64_t* cand_w;
+  double2* cand_v;
+  int64_t cw_vec_stride, sumP;
+  K3ClwPrime pr[kClwMaxT];
+};
+static_assert(sizeof(K3ClwParams) <= 32764, "K3ClwParams exceeds the kernel parameter limit");
+
+__device__ __forceinline__ double pymod1(double x) { return __dsub_rn(x, floor(x)); }  // Python's x % 1.0
+
+__global__ void __launch_bounds__(256) k3_clw(const __grid_constant__ K3ClwParams p) {
+  int i = 0;
+  while (i + 1 < p.nprime && (int)blockIdx.x >= p.cta_off[i + 1]) ++i;
+  const K3ClwPrime& pp = p.pr[i];
+  const int64_t P = pp.P;
+  const int64_t gid = (int64_t)((int)blockIdx.x - p.cta_off[i]) * blockDim.x + threadIdx.x;
+  if (gid >= (int64_t)p.nb * P) return;
+  const int v = blockIdx.y;
+  const int j = (int)(gid / P);
+  const int64_t pos = gid - (int64_t)j * P;
+  const int64_t b = pos == P - 1 ? 0 : (int64_t)__ldg(pp.binat + pos);
+  const double2* col = pp.Z + (int64_t)v * pp.z_vec_stride + (int64_t)j * pp.S * P + pos;
+  const double dP = (double)P;
+  const double2 x0 = ldcg2(col);
+  const double2 E0 = make_double2(__ddiv_rn(x0.x, dP), __ddiv_rn(x0.y, dP));
+  const int64_t q = p.qfirst + (int64_t)j * p.qstep;
+  const int64_t N = p.N;
+  const int64_t lo = q - p.halfN_up + 1;
+  int64_t om = kSentinel;
+  if (!(E0.x == 0.0 && E0.y == 0.0)) {
+    constexpr double kTwoPi = 6.283185307179586;
+    double vv = 0.0;
+    for (int sg = 1; sg < pp.S; ++sg) {
+      const double2 xs = ldcg2(col + (int64_t)sg * P);
+      const double2 Es = make_double2(__ddiv_rn(xs.x, dP), __ddiv_rn(xs.y, dP));
+      // r = Es conj(E0), rounded like Python's complex product (no contraction)
+      const double re = __dadd_rn(__dmul_rn(Es.x, E0.x), __dmul_rn(Es.y, E0.y));
+      const double im = __dadd_rn(__dmul_rn(Es.x, -E0.y), __dmul_rn(Es.y, E0.x));
+      const double theta = __ddiv_rn(atan2(im, re), kTwoPi);
+      const int64_t m = pp.shift[sg];
+      int64_t ml = (int64_t)(((__int128)m * (__int128)lo) % (__int128)N);
+      if (ml < 0) ml += N;
+      const double phi = pymod1(__dsub_rn(theta, __ddiv_rn((double)ml, (double)N)));
+      if (sg == 1) {
+        vv = phi;
+      } else {
+        const double x = __dsub_rn(__dmul_rn((double)m, vv), phi);
+        const double k = floor(__dadd_rn(x, 0.5));
+        vv = __ddiv_rn(__dadd_rn(phi, k), (double)m);
+      }
+    }
+    const double n_est = __dmul_rn((double)N, pymod1(vv));
+    int64_t rb = (b - lo) % P;
+    if (rb < 0) rb += P;
+    int64_t best = -1;
+    double d1 = INFINITY;
+    for (int li = -1; li <= 1; ++li) {
+      const double center = __dadd_rn(n_est, (double)(li * N));
+      const double y = __ddiv_rn(__dsub_rn(center, (double)rb), dP);
+      const int64_t c = rb + P * (int64_t)floor(__dadd_rn(y, 0.5));
+      if (c >= 0 && c < N) {
+        const double dist = fabs(__dsub_rn((double)c, center));
+        if (dist < d1) {
+          best = c;
+          d1 = dist;
+        }
+      }
+    }
+    if (best >= 0) {
+      const int64_t o = lo + best;
+      if (o >= q - p.w && o < q + p.w && o >= p.B_lo && o <= p.B_hi) om = o;  // line 10
+    }
+  }
+  const int64_t slot = (int64_t)v * p.cw_vec_stride + (int64_t)j * p.sumP + pp.off + b;
+  DSFT_CHECK(b >= 0 && b < P && pp.off + b < p.sumP);
+  p.cand_w[slot] = om;
+  if (om != kSentinel) p.cand_v[slot * p.Kmax] = E0;
+}
 
 // =========================================================== K5a medians
 // Reading R10: z = median Re + i median Im of (-1)^omega E_{t,i}[omega mod L]
@@ -1401,6 +1505,7 @@ struct DbgParams {
   int64_t P, r, L;
   int64_t rinvP, PinvR;  // r^-1 mod P, P^-1 mod r
   int S, sb, what, band;
+  int row0;              // row of the n2 = 0 subgrid (0; CLW: the shifted grid sigma)
   double2* out;
 };
 
@@ -1408,7 +1513,7 @@ __global__ void k_debug_grid(const __grid_constant__ DbgParams p) {
   const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= p.L) return;
   const double2* zb = p.Z + (int64_t)p.band * p.S * p.P;
-  auto sig = [&](int64_t n2) -> int64_t { return n2 == 0 ? 0 : (int64_t)p.sb + n2 - 1; };
+  auto sig = [&](int64_t n2) -> int64_t { return n2 == 0 ? (int64_t)p.row0 : (int64_t)p.sb + n2 - 1; };
   const int64_t Mr = p.P - 1;
   if (p.what == 0) {
     const int64_t n1 = ((k % p.P) * p.rinvP) % p.P;
@@ -1538,6 +1643,7 @@ cudaError_t launch_k1(const Plan& p, int nprime, const int* ts, double2* const* 
     q.shift_r = b.shift_r_dev;
     q.shift_n2 = b.shift_n2_dev;
     q.shift_scale = b.shift_scale_dev;
+    q.shift_off = b.shift_off_dev;
     k.cta_off[i + 1] = k.cta_off[i] + (int)cdiv((int64_t)q.nnode, cta);
   }
   const dim3 grid((unsigned)k.cta_off[nprime], nvec);
@@ -1724,9 +1830,50 @@ static K3Params k3_params(const Plan& p, int t, const double2* Z, int64_t zstrid
   return k;
 }
 
+// K3 of the CLW-style inner SFT (reading R14) for bucket primes ts[0..n)
+static cudaError_t launch_k3_clw(const Plan& p, int n, const int* ts, const double2* const* Zs, const int64_t* zst,
+                                 int nvec, void* ws, const int* bands, int nbands, cudaStream_t st) {
+  if (n > kClwMaxT) return cudaErrorInvalidValue;
+  const WsLayout L = ws_layout(p, p.ws_batch);
+  K3ClwParams k{};
+  k.nprime = n;
+  k.nb = nbands;
+  k.Kmax = p.Kmax;
+  k.N = p.N;
+  const int stride = nbands > 1 ? bands[1] - bands[0] : 1;
+  k.qfirst = band_q(p, bands[0]);
+  k.qstep = 2 * p.w * (int64_t)stride;
+  k.halfN_up = p.halfN_up;
+  k.halfN_dn = p.N / 2;
+  k.w = p.w;
+  k.B_lo = p.B_lo;
+  k.B_hi = p.B_hi;
+  k.cand_w = (int64_t*)((char*)ws + L.cand_w);
+  k.cand_v = (double2*)((char*)ws + L.cand_v);
+  k.cw_vec_stride = L.cw_vec;
+  k.sumP = p.sumP;
+  k.cta_off[0] = 0;
+  for (int i = 0; i < n; ++i) {
+    const Bucket& b = p.bk[ts[i]];
+    if (b.S > kClwMaxS) return cudaErrorInvalidValue;
+    K3ClwPrime& q = k.pr[i];
+    q.Z = Zs[i];
+    q.z_vec_stride = zst[i];
+    q.P = (int)b.P;
+    q.S = b.S;
+    q.off = b.off;
+    q.binat = b.binat;
+    for (int sg = 0; sg < b.S; ++sg) q.shift[sg] = b.shift_off[sg];
+    k.cta_off[i + 1] = k.cta_off[i] + (int)cdiv((int64_t)nbands * b.P, 256);
+  }
+  k3_clw<<<dim3((unsigned)k.cta_off[n], nvec), 256, 0, st>>>(k);
+  return cudaGetLastError();
+}
+
 // one-launch K3 of several bucket primes (candidates only; K5s probes the votes)
 cudaError_t launch_k3_multi(const Plan& p, int n, const int* ts, double2* const* Zs, const int64_t* zst, int nvec,
                             void* ws, const int* bands, int nbands, cudaStream_t st) {
+  if (p.params.inner == DSFT_INNER_CLW) return launch_k3_clw(p, n, ts, Zs, zst, nvec, ws, bands, nbands, st);
   if (n > kMultiMaxT) return cudaErrorInvalidValue;
   K3Multi m{};
   m.nprime = n;
@@ -1746,6 +1893,7 @@ cudaError_t launch_k3_multi(const Plan& p, int n, const int* ts, double2* const*
 
 cudaError_t launch_k3(const Plan& p, int t, const double2* Z, int64_t zstride, int nvec, void* ws, const int* bands,
                       int nbands, cudaStream_t st, const int* prev, int nprev, int j0, int nb_launch) {
+  if (p.params.inner == DSFT_INNER_CLW) return launch_k3_clw(p, 1, &t, &Z, &zstride, nvec, ws, bands, nbands, st);
   const Bucket& b = p.bk[t];
   const K3Params k = k3_params(p, t, Z, zstride, ws, bands, nbands, prev, nprev, j0, nb_launch);
   dim3 grid(cdiv((int64_t)k.nb * b.P, 256), nvec);
@@ -1911,13 +2059,16 @@ cudaError_t launch_debug_grid(const Plan& p, int t, const double2* Z, int i, int
   k.Z = Z;
   k.posn = b.posn;
   k.posb = b.posb;
+  const bool clw = p.params.inner == DSFT_INNER_CLW;  // i selects the grid shift sigma
+  const int r = clw ? 1 : b.r[i];
   k.P = b.P;
-  k.r = b.r[i];
-  k.L = b.P * b.r[i];
-  k.rinvP = modinv(b.r[i], b.P);
-  k.PinvR = modinv(b.P, b.r[i]);
+  k.r = r;
+  k.L = b.P * r;
+  k.rinvP = modinv(r, b.P);
+  k.PinvR = r > 1 ? modinv(b.P, r) : 0;
   k.S = b.S;
-  k.sb = b.shift_base[i];
+  k.sb = clw ? 1 : b.shift_base[i];
+  k.row0 = clw ? i : 0;
   k.what = what;
   k.band = band;
   k.out = out;

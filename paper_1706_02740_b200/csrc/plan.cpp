@@ -446,6 +446,8 @@ static dsft_status derive(int64_t N, int64_t s, const dsft_params& prm, Plan& P)
   // bucket-prime pool (reading R6)
   if (prm.pool_rule != DSFT_POOL_FULL && prm.pool_rule != DSFT_POOL_SMOOTH)
     return fail(DSFT_ERR_CONFIG, "unknown pool_rule");
+  if (prm.inner != DSFT_INNER_GFFT && prm.inner != DSFT_INNER_CLW) return fail(DSFT_ERR_CONFIG, "unknown inner");
+  const bool clw = prm.inner == DSFT_INNER_CLW;
   const int64_t lo = (int64_t)ceil(prm.bucket_factor * (double)s);
   const int64_t hi = 2 * lo;
   std::vector<int64_t> pool;
@@ -500,8 +502,12 @@ static dsft_status derive(int64_t N, int64_t s, const dsft_params& prm, Plan& P)
     b.P = primes[t];
     // residue primes (reading R8): the set of distinct odd primes below min(P, 32) with
     // P prod r >= N minimising sum (r - 1) (extra shift rows), ties -> fewer primes,
-    // then lexicographically smallest; at least one
-    {
+    // then lexicographically smallest; at least one.  CLW (reading R14): one grid of
+    // length P ("residue" 1), no CRT.
+    if (clw) {
+      b.K = 1;
+      b.r[0] = 1;
+    } else {
       std::vector<int64_t> cand;
       for (int64_t pr : odd)
         if (pr <= 31 && pr < b.P) cand.push_back(pr);
@@ -533,16 +539,32 @@ static dsft_status derive(int64_t N, int64_t s, const dsft_params& prm, Plan& P)
       for (int i = 0; i < b.K; ++i) b.r[i] = (int)best[i];
     }
     const int K = b.K;
-    // shifts: sigma 0 = P-subgrid (n2 = 0 of every residue grid), then (i, n2 >= 1)
+    // shifts: sigma 0 = P-subgrid (n2 = 0 of every residue grid), then (i, n2 >= 1);
+    // CLW: sigma 0 unshifted, sigma = l + 1 shifted by m = 2^l steps of f, l < L with
+    // L the fewest scales for which 2^(L-1) P >= N (reading R14)
     int S = 1;
     b.shift_r[0] = 1;
     b.shift_n2[0] = 0;
-    for (int i = 0; i < K; ++i) {
+    b.shift_off[0] = 0;
+    if (clw) {
+      b.shift_base[0] = 1;
+      int L = 1;
+      while (((int64_t)1 << (L - 1)) * b.P < N) ++L;
+      if (L + 1 > kMaxShifts) return fail(DSFT_ERR_UNSUPPORTED, "too many CLW scales");
+      for (int l = 0; l < L; ++l, ++S) {
+        b.shift_r[S] = 1;
+        b.shift_n2[S] = 0;
+        b.shift_off[S] = (int64_t)1 << l;
+      }
+      grid_points += b.P;
+    }
+    for (int i = 0; i < K && !clw; ++i) {
       b.shift_base[i] = S;
       for (int n2 = 1; n2 < b.r[i]; ++n2) {
         if (S >= kMaxShifts) return fail(DSFT_ERR_UNSUPPORTED, "too many shifts");
         b.shift_r[S] = b.r[i];
         b.shift_n2[S] = n2;
+        b.shift_off[S] = 0;
         ++S;
       }
       grid_points += b.P * b.r[i];
@@ -650,6 +672,7 @@ static dsft_status derive(int64_t N, int64_t s, const dsft_params& prm, Plan& P)
   I.nodes = nodes;
   I.grid_points = grid_points;
   I.sum_primes = P.sumP;
+  I.inner = prm.inner;
   return DSFT_OK;
 }
 
@@ -660,8 +683,8 @@ static dsft_status upload_tables(Plan& P) {
   std::vector<size_t> offs(P.T), goff(P.T), cpx(P.T), soff(P.T);
   for (int t = 0; t < P.T; ++t) {
     const Bucket& b = P.bk[t];
-    soff[t] = bytes;  // K1 shift tables: scale [S] double | r [S] int | n2 [S] int
-    bytes = align256(bytes + (size_t)b.S * 16);
+    soff[t] = bytes;  // K1 shift tables: scale [S] double | r [S] int | n2 [S] int | off [S] int64
+    bytes = align256(bytes + (size_t)b.S * 24);
     offs[t] = bytes;
     goff[t] = align256(bytes + (size_t)b.P * 4);
     cpx[t] = align256(goff[t] + (size_t)b.M * 4);
@@ -677,10 +700,12 @@ static dsft_status upload_tables(Plan& P) {
       double* sc = (double*)(host.data() + soff[t]);
       int* sr = (int*)(sc + b.S);
       int* sn = sr + b.S;
+      int64_t* so = (int64_t*)(sn + b.S);
       for (int sg = 0; sg < b.S; ++sg) {
         sc[sg] = 2.0 * M_PI / ((double)P.N * (double)(b.P * b.shift_r[sg]));
         sr[sg] = b.shift_r[sg];
         sn[sg] = b.shift_n2[sg];
+        so[sg] = b.shift_off[sg];
       }
     }
     uint16_t* posn = (uint16_t*)(host.data() + offs[t]);
@@ -766,6 +791,7 @@ static dsft_status upload_tables(Plan& P) {
     b.shift_scale_dev = (double*)(base + soff[t]);
     b.shift_r_dev = (int*)(b.shift_scale_dev + b.S);
     b.shift_n2_dev = b.shift_r_dev + b.S;
+    b.shift_off_dev = (const int64_t*)(b.shift_n2_dev + b.S);
     b.posn = (uint16_t*)(base + offs[t]);
     b.posb = b.posn + b.P;
     b.gpow = (uint16_t*)(base + goff[t]);
@@ -790,7 +816,7 @@ static void specialise_k2(Plan& P) {
   std::vector<std::thread> th;
   std::vector<std::string> why(P.T);
   std::vector<std::string> why3(P.T);
-  for (int t = 0; t < P.T; ++t)
+  for (int t = 0; t < P.T && P.params.inner == DSFT_INNER_GFFT; ++t)  // (CLW: phase-decoding K3, not specialised)
     th.emplace_back([&, t, dev] {
       cudaSetDevice(dev);
       Bucket& bb = P.bk[t];
@@ -863,6 +889,7 @@ void dsft_params_default(dsft_params* p) {
   p->seed = 0;
   p->pool_rule = DSFT_POOL_SMOOTH;
   p->flags = 0;
+  p->inner = DSFT_INNER_GFFT;
 }
 
 const char* dsft_status_string(dsft_status st) {
@@ -1228,7 +1255,9 @@ static dsft_status run_bands(Plan& p, const double2* f, int64_t ld, int nv, cons
     CU(cudaEventRecord(evJoin2, a2), "pipeline join");
     CU(cudaStreamWaitEvent(st, evJoin2, 0), "pipeline join wait");
   }
-  CU(timed(p, 3, st, [&] { return launch_k45(p, nv, p.ws, bands, nb, st, freqs, coeffs); }),
+  // CLW (reading R14): K3 wrote candidates only; K5s counts the votes by probing
+  const bool probe = p.params.inner == DSFT_INNER_CLW;
+  CU(timed(p, 3, st, [&] { return launch_k45(p, nv, p.ws, bands, nb, st, freqs, coeffs, probe); }),
      "K456 vote/estimate/merge launch");
   return DSFT_OK;
 }
@@ -1423,7 +1452,8 @@ dsft_status dsft_debug_grid(dsft_plan* pl, const dsft_c128* f_dev, int32_t band,
                             dsft_c128* out_dev, void* stream) {
   if (!pl || !f_dev || !out_dev) return fail(DSFT_ERR_ARG, "NULL argument");
   Plan& p = pl->p;
-  if (band < 0 || band >= p.J || t < 0 || t >= p.T || i < 0 || i >= p.bk[t].K || what < 0 || what > 1)
+  const int ni = p.params.inner == DSFT_INNER_CLW ? p.bk[t].S : p.bk[t].K;  // CLW: i = grid shift sigma
+  if (band < 0 || band >= p.J || t < 0 || t >= p.T || i < 0 || i >= ni || what < 0 || what > 1)
     return fail(DSFT_ERR_ARG, "band/t/i/what out of range");
   dsft_status stt = ensure_ws(p, 1);
   if (stt != DSFT_OK) return stt;

@@ -70,6 +70,20 @@ def test_pool_rule_matches_oracle(rule):
     assert d.default_pool_rule() == OracleParams().pool_rule == "smooth"
 
 
+@pytest.mark.parametrize("N,s,kw", [(4096, 8, {}), (2**26, 1000, {}), (2**22, 50, {"kappa": 12}), (97, 4, {}),
+                                    (2**31 + 11, 8, {})])
+def test_clw_plan_matches_oracle(N, s, kw):
+    """Reading R14 on both sides: the same primes and, per prime, one grid with the
+    shifts 0, 1, 2, ..., 2^(L-1) (n_shifts = 1 + L)."""
+    info = d.dsft_plan_derive_info(N, s, d.make_params(inner="clw", seed=3, **kw))
+    p = derive_plan(N, s, OracleParams(inner="clw", seed=3, **kw))
+    assert info.inner == 1 and list(info.primes[:info.T]) == p.primes
+    assert [info.n_shifts[t] for t in range(info.T)] == [len(sh) for sh in p.shifts]
+    assert all(info.n_residues[t] == 1 and info.residues[t][0] == 1 for t in range(info.T))
+    assert info.grid_points == sum(p.primes)
+    assert info.nodes == sum(P * len(sh) for P, sh in zip(p.primes, p.shifts))
+
+
 def test_shard_bands_partition():
     for J in (1, 7, 15, 43):
         for world in (1, 2, 3, 4, 8):

@@ -615,3 +615,69 @@ def test_small_plan_path_equals_pipeline(N, s, kw):
     assert_parity(a, dsft(pl.f, s, OracleParams(seed=2, **kw)), s)
     if N <= 2**22 and s <= 50:
         assert plan.launches_per_execute() <= 2 + plan.info.T + 3 < ser.launches_per_execute()
+
+
+# ------------------------------------------------------- CLW-style inner SFT (R14)
+@pytest.mark.parametrize("N,s,kw", [(4096, 8, {"kappa": 12}), (2**20, 300, {}), (2**21, 1000, {"kappa": 12})])
+def test_clw_stage_parity(N, s, kw):
+    """Reading R14: K1 on the shifted grids (window moved by m steps of f) against O2
+    with the shift, K1+K2 against O3, and the phase-decoded candidates bit-exact
+    wherever the oracle's decision margin exceeds 1e-9."""
+    kw = dict(inner="clw", seed=4, **kw)
+    op = derive_plan(N, s, OracleParams(**kw))
+    plan = d.Plan(N, s, d.make_params(**kw))
+    pl = planted(N, s, cfg=47, trial=1)
+    f = to_dev(pl.f)
+    band = op.J // 2
+    for t in (0, op.T - 1):
+        P = op.primes[t]
+        for sg in (0, 1, len(op.shifts[t]) - 1):
+            out = torch.empty(P, dtype=torch.complex128, device=DEV)
+            plan.dsft_debug_grid(f, band, t, sg, 0, out)
+            h_ref = filtered_samples(pl.f, op, op.q[band], P, op.shifts[t][sg])
+            assert np.max(np.abs(out.cpu().numpy() - h_ref)) <= 1e-13 * max(1.0, np.max(np.abs(h_ref)))
+            plan.dsft_debug_grid(f, band, t, sg, 1, out)
+            Y_ref = alias_dft(h_ref)
+            assert np.max(np.abs(out.cpu().numpy() - Y_ref)) <= 1e-13 * max(1.0, np.max(np.abs(Y_ref)))
+    from oracle.dsft import identify_clw
+    plan(f)
+    torch.cuda.synchronize()
+    cand = torch.empty(op.J * sum(op.primes), dtype=torch.int64, device=DEV)
+    plan.dsft_debug_copy(0, cand)
+    cand = cand.cpu().numpy().reshape(op.J, -1)
+    checked = 0
+    for j in (0, band, op.J - 1):
+        Y = band_measurements(pl.f, op, j)
+        off = 0
+        for t in range(op.T):
+            ids = identify_clw(op, j, t, Y[t])
+            P = op.primes[t]
+            ok = ids.gap > 1e-9
+            assert np.array_equal(cand[j, off:off + P][ok], ids.cand[ok])
+            checked += int(ok.sum())
+            off += P
+    assert checked > 0.5 * 3 * sum(op.primes)
+
+
+CLW_E2E = [(4096, 8, 0, None, {"kappa": 12}), (2**16, 50, 1, None, {}), (2**22, 50, 2, None, {"kappa": 12}),
+           (6000011, 100, 3, 40.0, {"kappa": 12}), (2**20, 2000, 1, None, {}), (97, 4, 0, None, {"kappa": 12}),
+           (2**16, 50, 5, None, {"kappa": 12, "pool_rule": "full"})]
+
+
+@pytest.mark.parametrize("N,s,trial,snr,kw", CLW_E2E)
+def test_clw_end_to_end(N, s, trial, snr, kw):
+    pl = planted(N, s, cfg=48, trial=trial, snr_db=snr)
+    ref = dsft(pl.f, s, OracleParams(inner="clw", seed=trial, **kw))
+    plan = d.Plan(N, s, d.make_params(inner="clw", seed=trial, **kw))
+    assert_parity(run_gpu(plan, pl.f), ref, s)
+
+
+def test_clw_headline_size():
+    """BASELINE config 2 (N = 2^26, s = 1000) with the CLW-style inner SFT, DMSFT-6
+    window: exact support and oracle parity (16 shifted grids per prime)."""
+    N, s = 2**26, 1000
+    pl = planted(N, s, cfg=2, trial=0)
+    ref = dsft(pl.f, s, OracleParams(inner="clw", seed=0))
+    plan = d.Plan(N, s, d.make_params(inner="clw", seed=0))
+    assert_parity(run_gpu(plan, pl.f), ref, s)
+    assert sorted(ref.freqs.tolist()) == pl.freqs.tolist()
