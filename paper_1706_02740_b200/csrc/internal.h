@@ -41,6 +41,7 @@ constexpr int kZBufs = DSFT_ZBUFS;        // Z buffers the bucket-prime pipeline
 constexpr int kMaxRadix = 16;    // largest in-register FFT stage radix in K2
 constexpr int kMultiMaxT = 12;   // bucket primes of one-launch K2 / K3 (small plans; kernel-parameter limit)
 constexpr int64_t kTailMergeMaxS = 256;  // the fused small-plan tail merges in its last CTA up to this s
+constexpr int64_t kTailFusedMaxS = 16;   // small plans use the fused tail up to this s (measured, kernels.cu)
 constexpr double kK1OneLaunchBytes = 48.0e6;  // all primes' Z below this: one K1 launch (plan.cpp choose_order)
 
 // Per-bucket-prime tables (host copy + device pointers into plan->dev_tables).
@@ -202,7 +203,7 @@ cudaError_t launch_k3(const Plan& p, int t, const double2* Z, int64_t zstride, i
 // K4..K6 in one cooperative launch; freqs == nullptr: no merge (sharded path merges
 // after the allgather with launch_k6_blocks)
 cudaError_t launch_k45(const Plan& p, int nvec, void* ws, const int* band_list, int nbands, cudaStream_t st,
-                       int64_t* freqs, double2* coeffs, bool probe = false);
+                       int64_t* freqs, double2* coeffs, bool probe = false, bool small = false);
 // small plans (plan.cpp run_bands, grouped K1): every bucket prime in one K2 launch
 // (k2_multi_ok: all on the runtime <64,8> rows) and one K3 launch (candidates only;
 // the vote is counted by K5s, launch_k45(probe = true))

@@ -642,7 +642,7 @@ struct K2Multi {
 };
 static_assert(sizeof(K2Multi) <= 32764, "K2Multi exceeds the kernel parameter limit");
 
-__global__ void __launch_bounds__(32 * kK2RowsPerCta) k2_prime_dft_multi(const __grid_constant__ K2Multi p) {
+__global__ void __launch_bounds__(32 * kK2RowsPerCta, 4) k2_prime_dft_multi(const __grid_constant__ K2Multi p) {
   extern __shared__ double2 sm[];
   __shared__ double2 sX0[kK2RowsPerCta];
   const int w = threadIdx.x >> 5;
@@ -1627,6 +1627,11 @@ cudaError_t launch_k1(const Plan& p, int nprime, const int* ts, double2* const* 
     for (size_t e = 0; e < (size_t)p.J * p.kappa * 2; ++e) k.tab[e] = p.k1tab[e];
   }
   const int cta = fast ? kK1FastThreads : kK1GenThreads;
+  // (measured round 2: a software-pipelined variant -- each warp walking 4 groups of
+  // 32 nodes, the next group's windows copied by cp.async into a second shared buffer
+  // while the current one is mixed -- ran 2516 vs 2822 transforms/s at BASELINE
+  // config 2: fewer CTAs hide less latency than the overlap inside a warp gains)
+  const int per_cta = cta;  // nodes per CTA
   k.cta_off[0] = 0;
   for (int i = 0; i < nprime; ++i) {
     const Bucket& b = p.bk[ts[i]];
@@ -1644,7 +1649,7 @@ cudaError_t launch_k1(const Plan& p, int nprime, const int* ts, double2* const* 
     q.shift_n2 = b.shift_n2_dev;
     q.shift_scale = b.shift_scale_dev;
     q.shift_off = b.shift_off_dev;
-    k.cta_off[i + 1] = k.cta_off[i] + (int)cdiv((int64_t)q.nnode, cta);
+    k.cta_off[i + 1] = k.cta_off[i] + (int)cdiv((int64_t)q.nnode, per_cta);
   }
   const dim3 grid((unsigned)k.cta_off[nprime], nvec);
   if (fast && p.kappa == 6 && !big) k1_gather_mix_fast<6, int><<<grid, kK1FastThreads, 0, st>>>(k);
@@ -1946,7 +1951,7 @@ static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 g, dim3 b, size_t sme
 }
 
 cudaError_t launch_k45(const Plan& p, int nvec, void* ws, const int* bands, int nbands, cudaStream_t st,
-                       int64_t* freqs, double2* coeffs, bool probe) {
+                       int64_t* freqs, double2* coeffs, bool probe, bool small) {
   const WsLayout L = ws_layout(p, p.ws_batch);
   K5Params f{};
   f.vmask = (const uint64_t*)((char*)ws + L.vmask);
@@ -1999,7 +2004,14 @@ cudaError_t launch_k45(const Plan& p, int nvec, void* ws, const int* bands, int 
   k.band_nz = (int32_t*)((char*)ws + L.band_nz);
 
   cudaError_t e;
-  if (probe) {  // small plans: the fused per-band tail (+ merge by the last band CTA for small s)
+  // the fused per-band tail for the small-plan path (probe: K3 wrote candidates only);
+  // (measured round 2: the fused tail for the pipelined plans too -- K5s + k5_tail_small
+  // + K6 -- ran 2668 vs 2822 transforms/s at BASELINE config 2, 5883 vs 6686 at
+  // N = 2^24, s = 256; the four-kernel PDL tail stays there)
+  // (measured round 2 in the small-plan path: fused tail 0.043 / 0.080 / 0.098 ms at
+  // c0 / c1 / c3 against 0.045 / 0.074 / 0.090 ms for the four-kernel tail: fused only
+  // for the smallest budgets)
+  if (probe && small && p.s <= kTailFusedMaxS) {
     K5TailParams q{};
     q.f = f;
     q.merge = freqs && nbands == p.J && p.s <= kTailMergeMaxS;

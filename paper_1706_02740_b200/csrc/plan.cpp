@@ -838,6 +838,9 @@ static void specialise_k2(Plan& P) {
         return;
       }
       bb.jit_threads = nt;
+      // (measured round 2: loading each row with one bulk copy (cp.async.bulk + mbarrier)
+      // instead of stage 0's L2 loads: 2815 vs 2822 transforms/s at BASELINE config 2 --
+      // the row is L2-resident and the load is not what bounds K2; not kept)
       bb.k2_jit = jit_k2(nt, minb, bb.fac, bb.nfac, (size_t)bb.M * 16, &why[t], false,
                          bb.twf | (bb.pad ? 0x80000000u : 0u));  // bit 31: zero-padded rows
     });
@@ -1163,7 +1166,7 @@ static dsft_status run_bands_small(Plan& p, const double2* f, int64_t ld, int nv
   }
   CU(timed(p, 2, st, [&] { return launch_k3_multi(p, p.T, ts, Zs, zst, nv, p.ws, bands, nb, st); }),
      "K3 identify launch");
-  CU(timed(p, 3, st, [&] { return launch_k45(p, nv, p.ws, bands, nb, st, freqs, coeffs, true); }),
+  CU(timed(p, 3, st, [&] { return launch_k45(p, nv, p.ws, bands, nb, st, freqs, coeffs, true, true); }),
      "K456 vote/estimate/merge launch");
   return DSFT_OK;
 }
@@ -1215,6 +1218,9 @@ static dsft_status run_bands(Plan& p, const double2* f, int64_t ld, int nv, cons
     gfirst[g + 1] = gfirst[g] + (grouped ? p.T : 1);
     for (int k = gfirst[g]; k < gfirst[g + 1]; ++k) gof[k] = g;
   }
+  // (measured round 2: the first prime's K1 and K2 in two halves of its shift rows, so
+  // K2 starts on the first half while K1 finishes the second: 2806 vs 2822
+  // transforms/s at BASELINE config 2, 480 vs 476 at s = 4000 -- not kept)
   auto k1 = [&](int g) -> dsft_status {
     const int k0 = gfirst[g], n = gfirst[g + 1] - gfirst[g];
     if (!grouped && k0 >= kZBufs) CU(cudaStreamWaitEvent(a1, evK3[k0 - kZBufs], 0), "K1 waits K3");
@@ -1435,11 +1441,11 @@ int64_t dsft_plan_collect_timeline(dsft_plan* pl, double* rows, int64_t n) {
 
 int64_t dsft_plan_launches_per_execute(const dsft_plan* pl) {
   if (!pl) return 0;
-  if (small_plan(pl->p))  // K1, K2 (one or per prime), K3, fused tail (+ K6 above kTailMergeMaxS)
+  if (small_plan(pl->p))  // K1, K2 (one or per prime), K3, K5s + fused tail (s <= 16) or the 4-kernel tail
   {
     int64_t k2n = 0;  // K2 launches: one multi-prime launch, or per prime (split rows: K2a + K2b)
     for (int t = 0; t < pl->p.T; ++t) k2n += (pl->p.bk[t].split && !(pl->p.bk[t].cl && pl->p.bk[t].k2_jit)) ? 2 : 1;
-    return 2 + (k2_multi_ok(pl->p) ? 1 : k2n) + (pl->p.s <= kTailMergeMaxS ? 2 : 3);
+    return 2 + (k2_multi_ok(pl->p) ? 1 : k2n) + (pl->p.s <= kTailFusedMaxS ? 2 : 4);
   }
   int64_t n = 4;  // K5 scan, K5 medians, K5 select, K6 merge
   for (int t = 0; t < pl->p.T; ++t)  // K1, K2 (split rows: K2a + K2b), K3

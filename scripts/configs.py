@@ -328,9 +328,46 @@ def c4(quick):
             "oracle_parity": par, "synth_s": synth_s}
 
 
+def variants(quick):
+    """The inner-SFT and pool options on BASELINE config 2 (N = 2^26, s = 1000) and the
+    noise sweep of the CLW-style inner SFT at N = 2^22, s = 50 (kappa = 12, PAPER.md:653;
+    the paper reports CLW-DSFT losing exact support below 40 dB)."""
+    out = []
+    N, s = 2 ** 26, 1000
+    pl = planted(N, s, cfg=2, trial=0)
+    f = torch.from_numpy(pl.f).to(DEV)
+    for name, kw in (("gfft/smooth", {}), ("gfft/full", {"pool_rule": "full"}), ("clw/smooth", {"inner": "clw"}),
+                     ("clw/smooth/kappa12", {"inner": "clw", "kappa": 12}), ("thm4", {"preset": "thm4"})):
+        plan = d.Plan(N, s, d.make_params(seed=0, **kw))
+        g = run(plan, f)
+        fr = torch.empty(s, dtype=torch.int64, device=DEV)
+        co = torch.empty(s, dtype=torch.complex128, device=DEV)
+        ms = timed(lambda: plan.dsft_execute(f, fr, co), 5 if quick else 20)
+        row = {"variant": name, "N": N, "s": s, "ms_per_transform": ms, "transforms_per_s": 1e3 / ms,
+               **accuracy(g, pl.freqs, pl.fhat, s)}
+        out.append(row)
+        print("  variants", row, flush=True)
+        plan.close()
+    del f
+    N, s = 2 ** 22, 50
+    trials = 3 if quick else 10
+    plan = d.Plan(N, s, d.make_params(seed=0, inner="clw", kappa=12))
+    sweep = []
+    for snr in (0.0, 10.0, 20.0, 40.0, 60.0, 80.0):
+        l1, exact = [], 0
+        for t in range(trials):
+            pl = planted(N, s, cfg=6, trial=t, snr_db=snr)
+            a = accuracy(run(plan, torch.from_numpy(pl.f).to(DEV)), pl.freqs, pl.fhat, s)
+            l1.append(a["avg_l1"])
+            exact += a["support_exact"]
+        sweep.append({"snr_db": snr, "avg_l1_mean": float(np.mean(l1)), "support_exact": exact, "trials": trials})
+        print("  clw noise22", sweep[-1], flush=True)
+    return {"rows": out, "clw_noise22": sweep}
+
+
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--only", default="c0,c1,c2,c3,c4,det,thm4,nsweep,noise22,dense")
+    ap.add_argument("--only", default="c0,c1,c2,c3,c4,det,thm4,nsweep,noise22,dense,variants")
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "configs.json"))
     ap.add_argument("--quick", action="store_true")
     a = ap.parse_args()

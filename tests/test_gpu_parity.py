@@ -614,7 +614,7 @@ def test_small_plan_path_equals_pipeline(N, s, kw):
     assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
     assert_parity(a, dsft(pl.f, s, OracleParams(seed=2, **kw)), s)
     if N <= 2**22 and s <= 50:
-        assert plan.launches_per_execute() <= 2 + plan.info.T + 3 < ser.launches_per_execute()
+        assert plan.launches_per_execute() <= 2 + plan.info.T + 4 < ser.launches_per_execute()
 
 
 # ------------------------------------------------------- CLW-style inner SFT (R14)
