@@ -58,7 +58,8 @@ __device__ __forceinline__ double2 ldcg2(const double2* p) {  // L2 only (data w
 // L2 eviction-priority policy (createpolicy) for Z, the per-prime working set
 // K1 -> K2 -> K3 keeps in L2 (evict_last); f windows bypass L1 allocation.
 // (An evict_first policy on f was measured to lose the L2 hits between
-// neighbouring windows: +30% DRAM reads, profiles/r1c.)
+// neighbouring windows: +30% DRAM reads, profiles/r1c; round 2 in the four-stream
+// pipeline: 2806 vs 2822 transforms/s at BASELINE config 2.)
 __device__ __forceinline__ uint64_t l2_evict_first() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));

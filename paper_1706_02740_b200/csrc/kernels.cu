@@ -2027,6 +2027,9 @@ cudaError_t launch_k45(const Plan& p, int nvec, void* ws, const int* bands, int 
     return launch_k6_blocks(k.band_w, k.band_c, k.band_m, k.band_nz, p.J, p.info.band_budget, L.band_vec, L.bn_vec,
                             p.s, nvec, freqs, coeffs, st);
   }
+  // (measured round 2: the four tail kernels as the grid-synchronised phases of one
+  // cooperative kernel, one CTA per SM: 2743 vs 2823 transforms/s at BASELINE config
+  // 2, 0.0755 vs 0.0737 ms at c1 -- the PDL chain below stays)
   k5s_scan<<<dim3(cdiv((int64_t)nbands * p.sumP, 256), nvec), 256, 0, st>>>(f);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   if ((e = launch_pdl(k5a_medians, dim3(2 * 148, nvec), dim3(256), 0, st, f)) != cudaSuccess) return e;

@@ -841,6 +841,8 @@ static void specialise_k2(Plan& P) {
       // (measured round 2: loading each row with one bulk copy (cp.async.bulk + mbarrier)
       // instead of stage 0's L2 loads: 2815 vs 2822 transforms/s at BASELINE config 2 --
       // the row is L2-resident and the load is not what bounds K2; not kept)
+      // (measured round 2: a 96-register cap so that two K2 CTAs leave room for a K1
+      // CTA on the SM: 2822 vs 2823 transforms/s -- no change, not kept)
       bb.k2_jit = jit_k2(nt, minb, bb.fac, bb.nfac, (size_t)bb.M * 16, &why[t], false,
                          bb.twf | (bb.pad ? 0x80000000u : 0u));  // bit 31: zero-padded rows
     });

@@ -9,9 +9,10 @@ import paper_1706_02740_b200 as d
 from dsft_synth import planted
 
 N, s = int(sys.argv[1]) if len(sys.argv) > 1 else 2 ** 26, int(sys.argv[2]) if len(sys.argv) > 2 else 1000
+flags = int(sys.argv[3]) if len(sys.argv) > 3 else 0
 pl = planted(N, s, cfg=2, trial=0)
 f = torch.from_numpy(pl.f).cuda()
-plan = d.Plan(N, s, d.make_params(seed=0))
+plan = d.Plan(N, s, d.make_params(seed=0, flags=flags))
 fr = torch.empty(s, dtype=torch.int64, device="cuda")
 co = torch.empty(s, dtype=torch.complex128, device="cuda")
 st = torch.cuda.current_stream()
