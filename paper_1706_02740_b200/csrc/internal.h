@@ -39,9 +39,9 @@ constexpr int64_t kMaxWave = 4096;  // vectors processed concurrently by one bat
 #endif
 constexpr int kZBufs = DSFT_ZBUFS;        // Z buffers the bucket-prime pipeline rotates through (3: measured worse, L2)
 constexpr int kMaxRadix = 16;    // largest in-register FFT stage radix in K2
+constexpr int kK2TinyRow = 128;  // K2 rows up to this FFT length stay on the runtime kernel (plan.cpp specialise_k2)
 constexpr int kMultiMaxT = 12;   // bucket primes of one-launch K2 / K3 (small plans; kernel-parameter limit)
-constexpr int64_t kTailMergeMaxS = 256;  // the fused small-plan tail merges in its last CTA up to this s
-constexpr int64_t kTailFusedMaxS = 16;   // small plans use the fused tail up to this s (measured, kernels.cu)
+constexpr int64_t kTailFusedMaxS = 16;   // small plans use the two-launch fused tail up to this s (measured, kernels.cu)
 constexpr double kK1OneLaunchBytes = 48.0e6;  // all primes' Z below this: one K1 launch (plan.cpp choose_order)
 
 // Per-bucket-prime tables (host copy + device pointers into plan->dev_tables).
@@ -199,7 +199,7 @@ cudaError_t launch_k2(const Plan& p, int t, double2* Z, int64_t zstride, int nve
 // bands [j0, j0 + nb_launch) of the band list (<= 0: all)
 cudaError_t launch_k3(const Plan& p, int t, const double2* Z, int64_t zstride, int nvec, void* ws,
                       const int* band_list, int nbands, cudaStream_t st, const int* prev, int nprev, int j0 = 0,
-                      int nb_launch = 0);
+                      int nb_launch = 0, bool defer = false);
 // K4..K6 in one cooperative launch; freqs == nullptr: no merge (sharded path merges
 // after the allgather with launch_k6_blocks)
 cudaError_t launch_k45(const Plan& p, int nvec, void* ws, const int* band_list, int nbands, cudaStream_t st,

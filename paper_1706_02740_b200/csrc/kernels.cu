@@ -1892,15 +1892,18 @@ cudaError_t launch_k3_multi(const Plan& p, int n, const int* ts, double2* const*
   if (p.Rmax <= 7) k3_identify_multi<7><<<grid, 256, 0, st>>>(m);
   else if (p.Rmax <= 13) k3_identify_multi<13><<<grid, 256, 0, st>>>(m);
   else if (p.Rmax <= 17) k3_identify_multi<17><<<grid, 256, 0, st>>>(m);
+  else if (p.Rmax <= 19) k3_identify_multi<19><<<grid, 256, 0, st>>>(m);  // (c1: 228 -> fewer registers)
+  else if (p.Rmax <= 23) k3_identify_multi<23><<<grid, 256, 0, st>>>(m);
   else k3_identify_multi<31><<<grid, 256, 0, st>>>(m);
   return cudaGetLastError();
 }
 
 cudaError_t launch_k3(const Plan& p, int t, const double2* Z, int64_t zstride, int nvec, void* ws, const int* bands,
-                      int nbands, cudaStream_t st, const int* prev, int nprev, int j0, int nb_launch) {
+                      int nbands, cudaStream_t st, const int* prev, int nprev, int j0, int nb_launch, bool defer) {
   if (p.params.inner == DSFT_INNER_CLW) return launch_k3_clw(p, 1, &t, &Z, &zstride, nvec, ws, bands, nbands, st);
   const Bucket& b = p.bk[t];
-  const K3Params k = k3_params(p, t, Z, zstride, ws, bands, nbands, prev, nprev, j0, nb_launch);
+  K3Params k = k3_params(p, t, Z, zstride, ws, bands, nbands, prev, nprev, j0, nb_launch);
+  k.defer_vote = defer ? 1 : 0;
   dim3 grid(cdiv((int64_t)k.nb * b.P, 256), nvec);
   // the plan's NVRTC kernel with this prime's residue tuple as constants (2.0 %
   // faster at c2 s = 1000 than the runtime-residue kernel below)
@@ -2004,26 +2007,26 @@ cudaError_t launch_k45(const Plan& p, int nvec, void* ws, const int* bands, int 
   k.band_nz = (int32_t*)((char*)ws + L.band_nz);
 
   cudaError_t e;
-  // the fused per-band tail for the small-plan path (probe: K3 wrote candidates only);
-  // (measured round 2: the fused tail for the pipelined plans too -- K5s + k5_tail_small
-  // + K6 -- ran 2668 vs 2822 transforms/s at BASELINE config 2, 5883 vs 6686 at
-  // N = 2^24, s = 256; the four-kernel PDL tail stays there)
-  // (measured round 2 in the small-plan path: fused tail 0.043 / 0.080 / 0.098 ms at
-  // c0 / c1 / c3 against 0.045 / 0.074 / 0.090 ms for the four-kernel tail: fused only
-  // for the smallest budgets)
-  if (probe && small && p.s <= kTailFusedMaxS) {
+  if (small && p.s <= kTailFusedMaxS) {
+    // small plans with small s: K5s (the vote) and one CTA per band for the medians,
+    // the band select and -- in the vector's last CTA, after a __threadfence ticket --
+    // the merge: two launches.  (Measured round 2: c0 0.043 ms against 0.047 for K5s
+    // + medians in K5s + K5b with the merge, 0.053 for the four-kernel tail; at c1 /
+    // c3 / c2 s = 50 the four-kernel tail is faster.  Also measured and dropped: this
+    // fused tail for the pipelined plans (2668 vs 2822 transforms/s at BASELINE config 2),
+    // the cooperative one-kernel tail (below).)
     K5TailParams q{};
     q.f = f;
-    q.merge = freqs && nbands == p.J && p.s <= kTailMergeMaxS;
+    q.merge = freqs && nbands == p.J;
     if (q.merge)
       q.m = k6_params(k.band_w, k.band_c, k.band_m, k.band_nz, p.J, p.info.band_budget, L.band_vec, L.bn_vec, p.s,
                       freqs, coeffs);
     k5s_scan<<<dim3(cdiv((int64_t)nbands * p.sumP, 256), nvec), 256, 0, st>>>(f);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     if ((e = launch_pdl(k5_tail_small, dim3(nbands, nvec), dim3(kK5Threads), kRankTile * 64, st, q)) != cudaSuccess ||
-        !freqs || q.merge)
+        q.merge)
       return e;
-    if (nbands != p.J) return cudaErrorInvalidValue;
+    if (!freqs) return cudaSuccess;  // sharded: merged after the allgather
     return launch_k6_blocks(k.band_w, k.band_c, k.band_m, k.band_nz, p.J, p.info.band_budget, L.band_vec, L.bn_vec,
                             p.s, nvec, freqs, coeffs, st);
   }

@@ -331,10 +331,11 @@ bool choose_k2_layout(Bucket& b, std::vector<int>& rad, bool no_cluster) {
     return false;
   }
   if (!choose_radices(M, rad)) return false;
-  // small rows (M <= 1200) run the runtime-radix kernel, which multiplies by the
-  // all-ones tables of twiddle-free stages: one dimension there (c2 s = 50: 6975
-  // vs 7115 transforms/s with Good-Thomas dimensions)
-  if (M > 1200 && !b.pad) choose_k2_dims(b, rad);  // padded rows: natural order (zero tail)
+  // Good-Thomas dimensions for every row but the zero-padded ones (natural order, zero
+  // tail).  The runtime-radix kernel (the no-NVRTC fallback) multiplies by the all-ones
+  // tables of the twiddle-free stages -- bitwise the specialised kernel's result, ~2 %
+  // slower (round 1, c2 s = 50) -- so both paths share one layout
+  if (!b.pad) choose_k2_dims(b, rad);
   if ((int)rad.size() > kMaxFac) return false;
   if (M <= 1200) b.fft_variant = 0, b.fft_threads = 64;
   else if ((size_t)2 * ((size_t)M * 16 + 2048) <= 228 * 1024) b.fft_variant = 1, b.fft_threads = 256;
@@ -824,13 +825,20 @@ static void specialise_k2(Plan& P) {
     });
   for (int t = 0; t < P.T; ++t) {
     Bucket& b = P.bk[t];
-    if ((b.split && !b.cl) || b.fft_variant == 0) continue;
+    // (the small <64,8> rows are specialised too -- measured round 2, small-plan path
+    // with the per-prime K2 launches on four streams: c1 0.0717 -> 0.0594 ms, c3 0.0872
+    // -> 0.0755 ms, c2 s = 50 0.0899 -> 0.0768 ms, c0 unchanged)
+    if (b.split && !b.cl) continue;
+    // tiny rows (M <= 128, e.g. c0's P < 64) stay on the runtime kernel: all primes then
+    // run as one warp-per-row launch (k2_prime_dft_multi), which beat five specialised
+    // launches at c0 (0.043 vs 0.048 ms, round 2)
+    if (b.fft_variant == 0 && b.M <= kK2TinyRow) continue;
     th.emplace_back([&, t, dev] {
       cudaSetDevice(dev);
       Bucket& bb = P.bk[t];
       // (measured round 2: three CTAs per SM at an 80-register cap where three rows fit
       // shared memory -- no spills -- ran 2706 vs 2823 transforms/s at BASELINE config 2)
-      int nt = bb.fft_threads, minb = bb.fft_variant == 1 ? 2 : 1;
+      int nt = bb.fft_threads, minb = bb.fft_variant == 1 ? 2 : bb.fft_variant == 0 ? 8 : 1;
 
       if (bb.cl) {  // cluster kernel: blocks of M / C elements, 256 threads, 2 CTAs per SM
         bb.jit_threads = 256;
@@ -1162,10 +1170,27 @@ static dsft_status run_bands_small(Plan& p, const double2* f, int64_t ld, int nv
   if (k2_multi_ok(p)) {
     CU(timed(p, 1, st, [&] { return launch_k2_multi(p, p.T, ts, Zs, zst, nv, p.ws, nb, st); }), "K2 launch");
   } else {
-    for (int k = 0; k < p.T; ++k)
-      CU(timed(p, 1, st, [&] { return launch_k2(p, ts[k], Zs[k], zst[k], nv, p.ws, bands, nb, st); }),
+    // one K2 per bucket prime, spread over the plan's four streams (parallel graph
+    // branches), joined before K3
+    cudaStream_t ss[4] = {st, p.aux, p.aux2, p.aux3};
+    for (int t = 0; t < p.T; ++t)  // split-mode rows share one scratch region (Zs): one K2 at a time
+      if (p.bk[t].split && !(p.bk[t].cl && p.bk[t].k2_jit)) ss[1] = ss[2] = ss[3] = st;
+    cudaEvent_t evf = p.pipe_ev[3 * p.T], evj[3] = {p.pipe_ev[3 * p.T + 1], p.pipe_ev[3 * p.T + 2],
+                                                      p.pipe_ev[3 * p.T + 3]};
+    CU(cudaEventRecord(evf, st), "K2 fork");
+    for (int i = 1; i < 4; ++i) CU(cudaStreamWaitEvent(ss[i], evf, 0), "K2 fork wait");
+    for (int k = 0; k < p.T; ++k) {
+      cudaStream_t sk = ss[k % 4];
+      CU(timed(p, 1, sk, [&] { return launch_k2(p, ts[k], Zs[k], zst[k], nv, p.ws, bands, nb, sk); }),
          "K2 prime_dft launch");
+    }
+    for (int i = 1; i < 4; ++i) {
+      CU(cudaEventRecord(evj[i - 1], ss[i]), "K2 join");
+      CU(cudaStreamWaitEvent(st, evj[i - 1], 0), "K2 join wait");
+    }
   }
+  // K3 over every prime in one launch, candidates only (measured round 2: the plan-time
+  // per-prime K3 kernels on the four streams instead: c1 0.057 -> 0.072 ms)
   CU(timed(p, 2, st, [&] { return launch_k3_multi(p, p.T, ts, Zs, zst, nv, p.ws, bands, nb, st); }),
      "K3 identify launch");
   CU(timed(p, 3, st, [&] { return launch_k45(p, nv, p.ws, bands, nb, st, freqs, coeffs, true, true); }),
