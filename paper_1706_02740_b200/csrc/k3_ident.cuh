@@ -157,6 +157,8 @@ __device__ __forceinline__ void k3_body(const K3Params& p, int64_t gid) {
   if (!p.defer_vote) p.vmask[slot] = mk;  // this prime's slots: written only here, OR-ed only by later K3s
 }
 
+// (measured round 2: the plan-time K3 at three CTAs per SM (85 registers) ran 2636 vs
+// 2823 transforms/s at BASELINE config 2; two stay)
 template <int RMAX, int PC, int... Rs>
 __global__ void __launch_bounds__(256, sizeof...(Rs) > 0 ? 2 : 1) k3_identify(const __grid_constant__ K3Params p) {
   k3_body<RMAX, PC, Rs...>(p, (int64_t)blockIdx.x * blockDim.x + threadIdx.x);

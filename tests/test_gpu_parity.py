@@ -432,12 +432,18 @@ class LazyPlanted:
     def __init__(self, N, freqs, c):
         self.N, self.freqs, self.c = N, np.asarray(freqs, dtype=np.int64), np.asarray(c)
         self.shape = (N,)
+        self._memo = {}  # the same window index arrays recur for every band
 
     def __getitem__(self, idx):
         idx = np.asarray(idx, dtype=np.int64)
+        key = (idx.shape, hash(idx.tobytes()))
+        hit = self._memo.get(key)
+        if hit is not None and np.array_equal(hit[0], idx):
+            return hit[1]
         out = np.zeros(idx.shape, dtype=np.complex128)
         for om, cc in zip(self.freqs, self.c):
             out += cc * np.exp(2j * math.pi * ((om * idx) % self.N) / self.N)
+        self._memo[key] = (idx.copy(), out)
         return out
 
 
@@ -680,3 +686,48 @@ def test_clw_headline_size():
     plan = d.Plan(N, s, d.make_params(inner="clw", seed=0))
     assert_parity(run_gpu(plan, pl.f), ref, s)
     assert sorted(ref.freqs.tolist()) == pl.freqs.tolist()
+
+
+def test_thm4_headline_parity():
+    """The guaranteed preset at BASELINE config 2's size (N = 2^26, s = 1000: kappa = 26,
+    J = 43, the generic-kappa K1 over 43 bands in two chunks): oracle parity."""
+    N, s = 2**26, 1000
+    pl = planted(N, s, cfg=2, trial=0)
+    kw = dict(preset="thm4", seed=0)
+    ref = dsft(pl.f, s, OracleParams(**kw))
+    plan = d.Plan(N, s, d.make_params(**kw))
+    assert plan.info.kappa == 26 and plan.info.J == 43
+    assert_parity(run_gpu(plan, pl.f), ref, s)
+    assert sorted(ref.freqs.tolist()) == pl.freqs.tolist()
+
+
+@pytest.mark.parametrize("e", [28, 30])
+def test_runtime_sweep_large_N_parity(e):
+    """The runtime-vs-N protocol's largest points (s = 50, N = 2^28 and
+    2^30, 4 and 16 GiB of complex128), synthesised on the device; the oracle reads the
+    same signal lazily at the entries its windows touch: exact support and parity."""
+    N, s = 2**e, 50
+    free, _ = torch.cuda.mem_get_info()
+    if free < N * 16 + (4 << 30):
+        pytest.skip("not enough free device memory")
+    rng = np.random.default_rng(e)
+    freqs = np.sort(rng.choice(N, s, replace=False).astype(np.int64) - (N + 1) // 2 + 1)
+    c = np.exp(2j * math.pi * rng.random(s))
+    f = torch.zeros(N, dtype=torch.complex128, device=DEV)
+    chunk = 1 << 27
+    for a in range(0, N, chunk):
+        j = torch.arange(a, min(N, a + chunk), dtype=torch.int64, device=DEV)
+        for om, cc in zip(freqs.tolist(), c.tolist()):
+            f[a:a + j.numel()] += cc * torch.exp(1j * (((om * j) % N).to(torch.float64) * (2 * math.pi / N)))
+        del j
+    plan = d.Plan(N, s, d.make_params(seed=1))
+    fr = torch.empty(s, dtype=torch.int64, device=DEV)
+    co = torch.empty(s, dtype=torch.complex128, device=DEV)
+    plan.dsft_execute(f, fr, co)
+    torch.cuda.synchronize()
+    gpu = (fr.cpu().numpy(), co.cpu().numpy())
+    assert sorted(gpu[0].tolist()) == freqs.tolist()
+    ref = dsft(LazyPlanted(N, freqs, c), s, plan=derive_plan(N, s, OracleParams(seed=1)))
+    assert_parity(gpu, ref, s)
+    del f
+    torch.cuda.empty_cache()
