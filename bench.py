@@ -506,6 +506,7 @@ def run_ours(a):
                      "timing_pass": f"{kpass} steps with per-launch CUDA events ({kms:.4f} ms/step)"},
         "roofline_gather": {"kernel": "k1_gather_mix", "bound": "hbm", "achieved": achieved, "peak": peak_gbs,
                             "unit": "GB/s", "frac": achieved / peak_gbs, "traffic": k1_traffic,
+                            "frac_of_nominal_8tbs": achieved / 8000.0,
                             "traffic_source": k1_tsrc,
                             "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if peaks else "fallback 6.65 TB/s",
                             "algorithmic_bytes_per_launch": k1_launch_bytes, "avg_launch_ms": k1_avg_ms,
