@@ -235,6 +235,17 @@ class Plan:
     def residues(self) -> list[list[int]]:
         return [list(self.info.residues[t][:self.info.n_residues[t]]) for t in range(self.info.T)]
 
+    def dsft_plan_workspace_bytes(self, batch: int = 1) -> int:
+        return int(lib().dsft_plan_workspace_bytes(self._h, batch))
+
+    def dsft_plan_set_workspace(self, buf):
+        """Borrow a caller-owned device buffer (e.g. a torch uint8 tensor, 256-B aligned)
+        as the plan's workspace; the plan never frees it (keep `buf` alive)."""
+        if buf.device.type != "cuda" or not buf.is_contiguous():
+            raise DsftError(DSFT_ERR_ARG, "workspace: need a contiguous CUDA tensor")
+        _check(lib().dsft_plan_set_workspace(self._h, buf.data_ptr(), buf.numel() * buf.element_size()))
+        self._ws = buf
+
     def launches_per_execute(self) -> int:
         return int(lib().dsft_plan_launches_per_execute(self._h))
 

@@ -731,3 +731,40 @@ def test_runtime_sweep_large_N_parity(e):
     assert_parity(gpu, ref, s)
     del f
     torch.cuda.empty_cache()
+
+
+def test_borrowed_workspace_and_concurrent_plans():
+    """dsft_plan_set_workspace: a torch-owned workspace (the plan borrows it) gives the
+    owned-workspace result bitwise, also after a graph was captured on the owned one;
+    two plans executing concurrently on two streams (one in-flight execute per plan,
+    include/dsft.h) give their sequential results."""
+    N, s = 2**20, 300
+    pl = planted(N, s, cfg=49, trial=0)
+    f = to_dev(pl.f)
+    a = d.Plan(N, s)
+    ref = run_gpu(a, pl.f)
+    nbytes = a.dsft_plan_workspace_bytes(1)
+    ws = torch.empty(nbytes + 256, dtype=torch.uint8, device=DEV)
+    off = (-ws.data_ptr()) % 256
+    a.dsft_plan_set_workspace(ws[off:off + nbytes])
+    got = run_gpu(a, pl.f)
+    assert np.array_equal(got[0], ref[0]) and np.array_equal(got[1], ref[1])
+    with pytest.raises(d.DsftError):
+        a.dsft_plan_set_workspace(ws[1:1 + nbytes])  # misaligned
+    pl2 = planted(2**22, 50, cfg=49, trial=1)
+    b = d.Plan(2**22, 50)
+    ref2 = run_gpu(b, pl2.f)
+    f2 = to_dev(pl2.f)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    outs = []
+    for _ in range(3):
+        fa, ca = torch.empty(s, dtype=torch.int64, device=DEV), torch.empty(s, dtype=torch.complex128, device=DEV)
+        fb, cb = torch.empty(50, dtype=torch.int64, device=DEV), torch.empty(50, dtype=torch.complex128, device=DEV)
+        torch.cuda.synchronize()
+        a.dsft_execute(f, fa, ca, s1)
+        b.dsft_execute(f2, fb, cb, s2)
+        torch.cuda.synchronize()
+        outs.append((fa.cpu().numpy(), ca.cpu().numpy(), fb.cpu().numpy(), cb.cpu().numpy()))
+    for fa, ca, fb, cb in outs:
+        assert np.array_equal(fa, ref[0]) and np.array_equal(ca, ref[1])
+        assert np.array_equal(fb, ref2[0]) and np.array_equal(cb, ref2[1])
