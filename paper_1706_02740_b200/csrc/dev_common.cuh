@@ -89,6 +89,15 @@ __device__ __forceinline__ void st_keep(double2* ptr, double2 v, uint64_t pol) {
 // Forward DFT (W = e^{-2 pi i / R}) of R values in registers.
 template <int R>
 __device__ __forceinline__ void dft_odd(double2 (&x)[R]) {
+  if constexpr (R == 3) {  // X1,2 = x0 - (x1 + x2)/2 -+ i sin(2 pi/3) (x1 - x2): 12 FP64 instructions
+    const double s1 = RadixTab<3>::s(1), c1 = RadixTab<3>::c(1);
+    const double2 A = cadd(x[1], x[2]), D = csub(x[1], x[2]);
+    const double2 sa = make_double2(fma(A.x, c1, x[0].x), fma(A.y, c1, x[0].y));
+    x[0] = cadd(x[0], A);
+    x[1] = make_double2(fma(D.y, s1, sa.x), fma(D.x, -s1, sa.y));
+    x[2] = make_double2(fma(D.y, -s1, sa.x), fma(D.x, s1, sa.y));
+    return;
+  }
   constexpr int H = (R - 1) / 2;
   double2 A[H], D[H];
 #pragma unroll

@@ -851,6 +851,17 @@ static void specialise_k2(Plan& P) {
       // the row is L2-resident and the load is not what bounds K2; not kept)
       // (measured round 2: a 96-register cap so that two K2 CTAs leave room for a K1
       // CTA on the SM: 2822 vs 2823 transforms/s -- no change, not kept)
+      // (measured round 2, session 2, BASELINE config 2, K2 per launch in serial mode and
+      // the pipelined step; none kept -- scripts/kern_times.py, scripts/ab.py):
+      //  * CTA sizes 288/320/352/384 x 2 and 96/128/160/192 x 3 per SM: 128 x 3 -15 %,
+      //    288 -17 %, 320 -2 %, 384 +-0 (no spills at any size);
+      //  * warp-group sub-FFTs (after the first WS stages the row is independent blocks;
+      //    groups of G warps own block ranges and synchronise with __syncwarp / named
+      //    barriers instead of __syncthreads; bitwise the same row): WS = 1-3, G = 1-2:
+      //    -0.6 % to -15 % (barrier stalls move to other stalls);
+      //  * persistent CTAs (one per SM) that bulk-copy row i+1 into a second buffer while
+      //    transforming row i: -8 % to -14 % at 256-768 threads;
+      //  * prefetching bhat into L1 ahead of the turn: -1 %.
       bb.k2_jit = jit_k2(nt, minb, bb.fac, bb.nfac, (size_t)bb.M * 16, &why[t], false,
                          bb.twf | (bb.pad ? 0x80000000u : 0u));  // bit 31: zero-padded rows
     });

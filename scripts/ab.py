@@ -53,7 +53,12 @@ def main():
     plans = []
     for spec in a.variants:
         name, kw = parse_kw(spec)
+        env = {k: str(v) for k, v in kw.items() if k.startswith("DSFT_")}  # plan-time experiment knobs
+        kw = {k: v for k, v in kw.items() if not k.startswith("DSFT_")}
+        os.environ.update(env)
         p = d.Plan(a.N, a.s, d.make_params(**kw))
+        for k in env:
+            del os.environ[k]
         for _ in range(3):
             p.dsft_execute(f, fr, co)
         torch.cuda.synchronize()
