@@ -453,6 +453,14 @@ def run_ours(a):
     k1_avg_ms = k1_ms / max(k1_n, 1)
     achieved = (k1_launch_bytes / 1e9) / (k1_avg_ms / 1e3)
     k1_traffic, k1_tsrc = stored_traffic("k1")
+    # K1 is also FP64 work: SURVEY 8(d) counts (2 kappa + 1)(8 J + 3) flops per node (band
+    # mix + Gaussian taps); at J = 15 its intensity sits near the FP64 ridge, so the
+    # binding roof of K1 is the larger of the two times (SURVEY 8(d) "Targets")
+    k1_flops = (2 * info.kappa + 1) * (8 * nb_local + 3) * info.nodes
+    k1_launch_flops = k1_flops / k1_launches
+    k1_tflops = (k1_launch_flops / 1e12) / (k1_avg_ms / 1e3)
+    k1_roof_ms = max(k1_launch_bytes / (peak_gbs * 1e9), k1_launch_flops / (FP64_PEAK_TFLOPS * 1e12)) * 1e3
+    step_flops = k1_flops + k2_flops  # the two FP64 bodies of the path (K3-K6: O(T K) per candidate)
     total_kernel_ms = sum(v[0] for v in kt.values())
     kernels = {k: {"ms_per_step": v[0] / kpass, "busy_ms_per_step": busy[k] / kpass,
                    "launches_per_step": v[1] / kpass,
@@ -513,7 +521,18 @@ def run_ours(a):
                             "launches_per_step": k1_launches,
                             "algorithmic": "16 B x distinct f entries under the 2kappa+1 windows of the launch's nodes",
                             "note": "launch duration measured inside the pipeline (K1 shares the SMs with K2/K3)",
-                            "z_samples_bytes_per_launch": z_bytes / k1_launches},
+                            "z_samples_bytes_per_launch": z_bytes / k1_launches,
+                            "fp64": {"achieved": k1_tflops, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                                     "frac": k1_tflops / FP64_PEAK_TFLOPS,
+                                     "algorithmic_flops_per_launch": k1_launch_flops,
+                                     "algorithmic": "SURVEY 8(d): (2 kappa + 1)(8 J + 3) per node"},
+                            "binding_roof": ("fp64" if k1_launch_flops / FP64_PEAK_TFLOPS / 1e3 >
+                                             k1_launch_bytes / peak_gbs else "hbm"),
+                            "frac_of_binding_roof": k1_roof_ms / k1_avg_ms},
+        "step_roofline": {"algorithmic_flops": step_flops, "floor_ms": step_flops / (FP64_PEAK_TFLOPS * 1e12) * 1e3,
+                          "frac": step_flops / (FP64_PEAK_TFLOPS * 1e12) * 1e3 / ms,
+                          "note": "K1 band mix + K2 aliasing DFTs (SURVEY 8(d) algorithmic counts) at the FP64 "
+                                  "peak, against ms_per_step"},
         "kernels": kernels,
         "k2_specialized": plan.dsft_plan_k2_specialized()[0],
         "filtered_samples_per_s": units * info.J * info.nodes / (ms / 1e3),

@@ -117,11 +117,22 @@ __device__ __forceinline__ void k3_body(const K3Params& p, int64_t gid) {
     R += (int64_t)b * p.crtE[i + 1];
     yv[i] = y;
   }
-  R %= p.crtM;
+  // the CRT modulus M_t = P_t prod r_i: a compile-time constant in the plan-time
+  // kernels (the two 64-bit remainders become multiply-high sequences)
+  constexpr int64_t CM = (PC > 0 && sizeof...(Rs) > 0) ? (int64_t)PC * ((int64_t)Rs * ... * (int64_t)1) : 0;
+  DSFT_CHECK(CM == 0 || CM == p.crtM);
   const int64_t q = p.qfirst + (int64_t)j * p.qstep;
   const int64_t lo = q - p.halfN_up + 1;  // smallest element of q + B
-  int64_t d = (R - lo) % p.crtM;
-  if (d < 0) d += p.crtM;
+  int64_t d;
+  if constexpr (CM > 0) {
+    R %= CM;
+    d = (R - lo) % CM;
+    if (d < 0) d += CM;
+  } else {
+    R %= p.crtM;
+    d = (R - lo) % p.crtM;
+    if (d < 0) d += p.crtM;
+  }
   const int64_t om = lo + d;
   const bool ok = (om <= q + p.halfN_dn) && (om >= q - p.w) && (om < q + p.w) && (om >= p.B_lo) && (om <= p.B_hi);
   const int64_t slot = (int64_t)v * p.cw_vec_stride + (int64_t)j * p.sumP + p.off + a;

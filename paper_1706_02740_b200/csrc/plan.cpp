@@ -865,7 +865,9 @@ static void specialise_k2(Plan& P) {
       //  * exact twiddles W_d^{kl c} from per-stage tables indexed by the dimension-local
       //    index (a few hundred entries, L1-resident, mostly warp-broadcast loads) instead
       //    of the power recurrence: -12 % FP64 instructions but K2 +9 % (P = 4051: 33 ->
-      //    48 us; each cmul now waits on a load), 2854 -> 2743 transforms/s.
+      //    48 us; each cmul now waits on a load), 2854 -> 2743 transforms/s;
+      //  * the odd CTAs of the first wave started 4 us late (so the wave's row loads and
+      //    FFT passes are not in lockstep across the GPU): 2839 -> 2823.
       bb.k2_jit = jit_k2(nt, minb, bb.fac, bb.nfac, (size_t)bb.M * 16, &why[t], false,
                          bb.twf | (bb.pad ? 0x80000000u : 0u));  // bit 31: zero-padded rows
     });
