@@ -75,6 +75,17 @@ __device__ __forceinline__ uint64_t l2_evict_last() {
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
+// load with an L2 eviction-priority policy (K3's last read of Z: evict_first frees the
+// dead Z lines that K1/K2 wrote with evict_last -- measured round 2: 2855 -> 2889
+// transforms/s at BASELINE config 2, +0.8 % at s = 2000 and 500; a discard.global.L2 of
+// the lines wholly inside each warp's span on top of it: no further change, and K1's
+// window loads at evict_first: no change); non-volatile: loads of the same address may
+// be merged (the data is not written during the kernel)
+__device__ __forceinline__ double2 ld_hint(const double2* ptr, uint64_t pol) {
+  double2 v;
+  asm("ld.global.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(v.x), "=d"(v.y) : "l"(ptr), "l"(pol));
+  return v;
+}
 __device__ __forceinline__ double2 ld_stream(const double2* ptr) {
   double2 v;
   asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(ptr));

@@ -49,9 +49,10 @@ template <int R>
 __device__ __forceinline__ void residue_argmax(const double2* __restrict__ col, int64_t P, int sb, double invL,
                                                int& best, double2& yv) {
   double2 x[R];
-  x[0] = col[0];
+  const uint64_t pol = l2_evict_first();  // the last read of Z (K1/K2 wrote it evict_last)
+  x[0] = ld_hint(col, pol);
 #pragma unroll
-  for (int n = 1; n < R; ++n) x[n] = col[(int64_t)(sb + n - 1) * P];
+  for (int n = 1; n < R; ++n) x[n] = ld_hint(col + (int64_t)(sb + n - 1) * P, pol);
   dft<R>(x);
   best = 0;
   double bm = cabs2_rn(x[0]);
