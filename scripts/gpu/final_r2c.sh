@@ -8,7 +8,7 @@ timeout 2400 python -m pytest tests -m gpu -q > gpurun_out/pytest_$TAG.log 2>&1;
 # ncu capture of K1/K2/K3 first, so the bench below reports measured traffic for these sources
 python scripts/run_one.py 67108864 1000 2 flags=32 > gpurun_out/plain1_$TAG.log 2>&1 && \
 timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"k1_gather|k2_ct|k3_ident" -s 0 -c 15 -o gpurun_out/prof_$TAG python scripts/run_one.py 67108864 1000 2 flags=32 > gpurun_out/ncu_full_$TAG.log 2>&1; echo "full rc=$?"
-python scripts/ncu_traffic.py gpurun_out/prof_$TAG.ncu-rep --capture "ncu --set full --clock-control none --import-source on -k regex:'k1_gather|k2_ct|k3_ident' -s 0 -c 15 python scripts/run_one.py 67108864 1000 2 flags=32 (BASELINE config 2, session-2 final sources, cold caches per kernel replay)"; echo "traffic rc=$?"
+python scripts/ncu_traffic.py gpurun_out/prof_$TAG.ncu-rep --capture "ncu --set full --clock-control none --import-source on -k regex:'k1_gather|k2_ct|k3_ident' -s 0 -c 15 python scripts/run_one.py 67108864 1000 2 flags=32 (BASELINE config 2, round-2 final sources, cold caches per kernel replay)"; echo "traffic rc=$?"
 cp profiles/traffic.json gpurun_out/traffic_$TAG.json
 timeout 900 python bench.py > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.err; echo "bench rc=$?"
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref_$TAG.json 2> gpurun_out/bench_ref_$TAG.err; echo "ref rc=$?"
