@@ -88,7 +88,10 @@ __device__ __forceinline__ double2 ld_hint(const double2* ptr, uint64_t pol) {
 }
 __device__ __forceinline__ double2 ld_stream(const double2* ptr) {
   double2 v;
-  asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(ptr));
+  // L2::64B: the window (208 B at a 16-B offset) is fetched from DRAM in 64-B pieces
+  // instead of the default 128-B lines -- less over-fetch (measured round 2 at BASELINE
+  // config 2: 64B 2922, default 2889, 128B 2889, 256B 2854 transforms/s)
+  asm volatile("ld.global.nc.L1::no_allocate.L2::64B.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(ptr));
   return v;
 }
 __device__ __forceinline__ void st_keep(double2* ptr, double2 v, uint64_t pol) {
