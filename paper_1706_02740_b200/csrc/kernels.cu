@@ -246,40 +246,25 @@ __device__ __forceinline__ void k1_mix_node(const K1Params& p, const K1Prime& pp
   }
 }
 
-// one block of kK1FastThreads nodes (local block index lb of the prime); PF: first issue
-// L2 prefetches of the windows of block lb + 1 (the CTA's next block), so its window
-// loads hit L2 while this block's DRAM round trip and band mix run
-template <int KAPPA, typename IdxT, bool PF>
-__device__ __forceinline__ void k1_fast_block(const K1Params& p, const K1Prime& pp, int lb,
-                                              double2 (&s_win)[kK1FastThreads / 32][32][2 * KAPPA + 1]) {
+template <int KAPPA, typename IdxT>
+__global__ void __launch_bounds__(kK1FastThreads) k1_gather_mix_fast(const __grid_constant__ K1Params p) {
   constexpr int W = 2 * KAPPA + 1;
+  __shared__ double2 s_win[kK1FastThreads / 32][32][W];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int lb;
+  const K1Prime& pp = p.pr[k1_prime(p, lb)];
   const int nodes = pp.node0 + pp.nnode;
-  const int v = blockIdx.y;
-  const IdxT N = (IdxT)p.N;
-  const double2* fv = p.f + (int64_t)v * p.ld;
-  if constexpr (PF) {
-    const int gid2 = pp.node0 + (lb + 1) * kK1FastThreads + threadIdx.x;
-    if (gid2 < nodes) {
-      const int sg2 = gid2 / pp.P, q2 = gid2 - sg2 * pp.P;
-      const NodeGeo g2 = node_geo_fast(pp, p.N, sg2, rader_node(pp, q2));
-      const IdxT s2 = (IdxT)g2.jp - KAPPA;
-      if (s2 >= 0 && s2 + W <= N) {
-        const char* a0 = (const char*)(fv + s2);
-        const char* a1 = (const char*)(fv + s2 + W) - 1;
-        for (const char* a = (const char*)((uintptr_t)a0 & ~(uintptr_t)63); a <= a1; a += 64)
-          asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
-      }
-    }
-  }
   const int gid = pp.node0 + lb * kK1FastThreads + threadIdx.x;
   const bool active = gid < nodes;
+  const int v = blockIdx.y;
   const int sigma = active ? gid / pp.P : 0;
   const int q = active ? gid - sigma * pp.P : 0;
   const NodeGeo g = active ? node_geo_fast(pp, p.N, sigma, rader_node(pp, q)) : NodeGeo{0, 0.0};
+  const IdxT N = (IdxT)p.N;
   // window start j' - kappa, or -1 - start for windows that wrap mod N
   IdxT st = (IdxT)g.jp - KAPPA;
   if (st < 0 || st + W > N) st = -1 - ((st % N) + N) % N;
+  const double2* fv = p.f + (int64_t)v * p.ld;
   {
     const int h = lane >> 4, u = lane & 15;
     const bool lane_on = u < W;
@@ -301,27 +286,13 @@ __device__ __forceinline__ void k1_fast_block(const K1Params& p, const K1Prime& 
         buf[i] = ld_stream(fv + idx);
       }
     }
-    __syncwarp();  // the previous block's windows are consumed
 #pragma unroll
     for (int i = 0; i < 16; ++i)
       if (lane_on) s_win[warp][2 * i + h][u] = buf[i];
   }
   __syncwarp();
-  if (active) k1_mix_node<KAPPA>(p, pp, v, sigma, q, g.d0, &s_win[warp][lane][0]);
-}
-
-// NB node blocks per CTA (NB = 2: the second block's windows prefetched into L2 first)
-template <int KAPPA, typename IdxT, int NB>
-__global__ void __launch_bounds__(kK1FastThreads) k1_gather_mix_fast(const __grid_constant__ K1Params p) {
-  __shared__ double2 s_win[kK1FastThreads / 32][32][2 * KAPPA + 1];
-  int lb;
-  const K1Prime& pp = p.pr[k1_prime(p, lb)];
-  if constexpr (NB == 1) {
-    k1_fast_block<KAPPA, IdxT, false>(p, pp, lb, s_win);
-  } else {
-    k1_fast_block<KAPPA, IdxT, true>(p, pp, 2 * lb, s_win);
-    k1_fast_block<KAPPA, IdxT, false>(p, pp, 2 * lb + 1, s_win);
-  }
+  if (!active) return;
+  k1_mix_node<KAPPA>(p, pp, v, sigma, q, g.d0, &s_win[warp][lane][0]);
 }
 
 // Any kappa (THM4: kappa = O(r log N) taps; kappa overrides): one
@@ -1659,9 +1630,10 @@ cudaError_t launch_k1(const Plan& p, int nprime, const int* ts, double2* const* 
   // (measured round 2: a software-pipelined variant -- each warp walking 4 groups of
   // 32 nodes, the next group's windows copied by cp.async into a second shared buffer
   // while the current one is mixed -- ran 2516 vs 2822 transforms/s at BASELINE
-  // config 2: fewer CTAs hide less latency than the overlap inside a warp gains)
-  const int nbk = (fast && getenv("DSFT_X_K1NB")) ? atoi(getenv("DSFT_X_K1NB")) : 1;  // EXPERIMENT
-  const int per_cta = cta * (fast ? nbk : 1);  // nodes per CTA
+  // config 2: fewer CTAs hide less latency than the overlap inside a warp gains; and
+  // two node blocks per CTA with the second block's windows prefetched into L2
+  // (prefetch.global.L2) first: K1 142 -> 197 us per transform, 2922 -> 2584)
+  const int per_cta = cta;  // nodes per CTA
   k.cta_off[0] = 0;
   for (int i = 0; i < nprime; ++i) {
     const Bucket& b = p.bk[ts[i]];
@@ -1682,11 +1654,10 @@ cudaError_t launch_k1(const Plan& p, int nprime, const int* ts, double2* const* 
     k.cta_off[i + 1] = k.cta_off[i] + (int)cdiv((int64_t)q.nnode, per_cta);
   }
   const dim3 grid((unsigned)k.cta_off[nprime], nvec);
-  if (fast && nbk == 2 && p.kappa == 6 && !big) k1_gather_mix_fast<6, int, 2><<<grid, kK1FastThreads, 0, st>>>(k);
-  else if (fast && p.kappa == 6 && !big) k1_gather_mix_fast<6, int, 1><<<grid, kK1FastThreads, 0, st>>>(k);
-  else if (fast && p.kappa == 6) k1_gather_mix_fast<6, int64_t, 1><<<grid, kK1FastThreads, 0, st>>>(k);
-  else if (fast && p.kappa == 4 && !big) k1_gather_mix_fast<4, int, 1><<<grid, kK1FastThreads, 0, st>>>(k);
-  else if (fast && p.kappa == 4) k1_gather_mix_fast<4, int64_t, 1><<<grid, kK1FastThreads, 0, st>>>(k);
+  if (fast && p.kappa == 6 && !big) k1_gather_mix_fast<6, int><<<grid, kK1FastThreads, 0, st>>>(k);
+  else if (fast && p.kappa == 6) k1_gather_mix_fast<6, int64_t><<<grid, kK1FastThreads, 0, st>>>(k);
+  else if (fast && p.kappa == 4 && !big) k1_gather_mix_fast<4, int><<<grid, kK1FastThreads, 0, st>>>(k);
+  else if (fast && p.kappa == 4) k1_gather_mix_fast<4, int64_t><<<grid, kK1FastThreads, 0, st>>>(k);
   else {
     // band chunk: the smallest instantiation holding ceil(nb / ceil(nb / 32)) bands
     // (43 bands run as two chunks of <= 24 instead of 32 + 11)
