@@ -65,7 +65,8 @@ enum { DSFT_ALPHA_CORRECTED = 0, DSFT_ALPHA_LITERAL = 1 };
  * (the Monte Carlo variant reads a random subset of the
  * deterministic measurements); SMOOTH = only the primes P whose P - 1 has no prime
  * factor above 13 (every length-P DFT is then a Rader convolution over a 13-smooth
- * FFT; the general primes of FULL use a Bluestein chirp-z convolution). */
+ * FFT; the general primes of FULL run the same Rader convolution zero-padded to a
+ * 13-smooth FFT length M >= 2 (P - 1) - 1, R6). */
 enum { DSFT_POOL_FULL = 0, DSFT_POOL_SMOOTH = 1 };
 /* Inner SFT of Algorithm 1 line 9 (Section 5):
  *  GFFT  the DMSFT family's randomized GFFT reading (R7-R10): residue
