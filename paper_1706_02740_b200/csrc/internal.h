@@ -86,6 +86,7 @@ struct Bucket {
   int dim_m[kMaxFac] = {};
   int dim_s0[kMaxFac + 1] = {};
   unsigned twf = 0;
+  unsigned kmj = 0;              // bit S: middle stage S in k-major butterfly order (k2_bank_orders)
   // device pointers
   uint16_t* posn = nullptr;     // [P] array position of node n (posn[0] unused; parity hooks)
   uint16_t* posb = nullptr;     // [P] array position of bin a (posb[0] unused; parity hooks)

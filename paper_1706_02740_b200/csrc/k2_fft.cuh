@@ -32,9 +32,27 @@ __device__ __forceinline__ int k2_row(const K2Params& p, int b) {
   return (p.band0 + bl) * p.S + p.sig0 + (b - bl * p.nsig);
 }
 
+// butterfly beta of a stage of span N, radix R -> (block, k).  k-minor (KMJ = false):
+// consecutive threads take consecutive k (stride-1 runs of m = N / R elements);
+// k-major (KMJ = true): consecutive threads take consecutive blocks at one k (stride N).
+// Which order a stage uses changes only its shared-memory bank pattern, never the
+// arithmetic (plan.cpp k2_bank_orders picks it per stage by counting wavefronts).
+template <int M, int N, int R, bool KMJ>
+__device__ __forceinline__ void bf_index(int beta, int& blk, int& k) {
+  if constexpr (KMJ) {
+    constexpr int nblk = M / N;
+    k = beta / nblk;
+    blk = beta - k * nblk;
+  } else {
+    constexpr int m = N / R;
+    blk = beta / m;
+    k = beta - blk * m;
+  }
+}
+
 // TW = false: a stage that ends its Good-Thomas dimension (twiddles all 1, skipped);
-// PADV: zero-padded row (global reads at index >= mv return 0)
-template <int NT, int M, int N, int R, bool GSRC, bool TW = true, bool PADV = false>
+// PADV: zero-padded row (global reads at index >= mv return 0); KMJ: butterfly order
+template <int NT, int M, int N, int R, bool GSRC, bool TW = true, bool PADV = false, bool KMJ = false>
 __device__ __forceinline__ void dif_ct(const double2* __restrict__ src, double2* s, const double2* __restrict__ tw,
                                        int mv = M) {
   constexpr int m = N / R, nbf = M / R, iters = (nbf + NT - 1) / NT;
@@ -42,8 +60,8 @@ __device__ __forceinline__ void dif_ct(const double2* __restrict__ src, double2*
   for (int it = 0; it < iters; ++it) {
     const int beta = threadIdx.x + it * NT;
     if ((nbf % NT == 0) || beta < nbf) {
-      const int blk = beta / m;
-      const int k = beta - blk * m;
+      int blk, k;
+      bf_index<M, N, R, KMJ>(beta, blk, k);
       const int base = blk * N + k;
       double2 v[R];
 #pragma unroll
@@ -74,7 +92,7 @@ __device__ __forceinline__ void dif_ct(const double2* __restrict__ src, double2*
   }
 }
 
-template <int NT, int M, int N, int R, bool GDST, bool TW = true, bool PADV = false>
+template <int NT, int M, int N, int R, bool GDST, bool TW = true, bool PADV = false, bool KMJ = false>
 __device__ __forceinline__ void dit_ct(double2* s, double2* __restrict__ dst, const double2* __restrict__ tw, double2 x0,
                                        int mv = M) {
   constexpr int m = N / R, nbf = M / R, iters = (nbf + NT - 1) / NT;
@@ -83,8 +101,8 @@ __device__ __forceinline__ void dit_ct(double2* s, double2* __restrict__ dst, co
   for (int it = 0; it < iters; ++it) {
     const int beta = threadIdx.x + it * NT;
     if ((nbf % NT == 0) || beta < nbf) {
-      const int blk = beta / m;
-      const int k = beta - blk * m;
+      int blk, k;
+      bf_index<M, N, R, KMJ>(beta, blk, k);
       const int base = blk * N + k;
       double2 v[R];
 #pragma unroll
@@ -174,11 +192,14 @@ struct RadixList {
   }
 };
 
-// TWF: bit S set = stage S ends its Good-Thomas dimension (no twiddles)
+// TWF: bit S set = stage S ends its Good-Thomas dimension (no twiddles); bit 24 + S
+// (S <= 6): middle stage S runs its butterflies in k-major order (bf_index)
+__host__ __device__ constexpr bool k2_kmj(unsigned twf, int s) { return s >= 1 && s <= 6 && ((twf >> (24 + s)) & 1u); }
+
 template <int NT, class L, int S, unsigned TWF = 0u>
 __device__ __forceinline__ void dif_mid(double2* sm, const K2Params& p) {
   if constexpr (S <= L::F - 2) {
-    dif_ct<NT, L::M, L::span(S), L::R[S], false, !((TWF >> S) & 1u)>(sm, sm, p.tw + p.toff[S]);
+    dif_ct<NT, L::M, L::span(S), L::R[S], false, !((TWF >> S) & 1u), false, k2_kmj(TWF, S)>(sm, sm, p.tw + p.toff[S]);
     __syncthreads();
     dif_mid<NT, L, S + 1, TWF>(sm, p);
   }
@@ -187,14 +208,16 @@ __device__ __forceinline__ void dif_mid(double2* sm, const K2Params& p) {
 template <int NT, class L, int S, unsigned TWF = 0u>
 __device__ __forceinline__ void dit_mid(double2* sm, const K2Params& p, double2 x0) {
   if constexpr (S >= 1) {
-    dit_ct<NT, L::M, L::span(S), L::R[S], false, !((TWF >> S) & 1u)>(sm, sm, p.tw + p.toff[S], x0);
+    dit_ct<NT, L::M, L::span(S), L::R[S], false, !((TWF >> S) & 1u), false, k2_kmj(TWF, S)>(sm, sm, p.tw + p.toff[S],
+                                                                                              x0);
     __syncthreads();
     dit_mid<NT, L, S - 1, TWF>(sm, p, x0);
   }
 }
 
 // NT threads, MINB CTAs per SM (register cap 65536 / (NT MINB)), radices Rs...;
-// TWF: twiddle-free stages (bit i: stage i ends its Good-Thomas dimension); bit 31:
+// TWF: twiddle-free stages (bit i: stage i ends its Good-Thomas dimension); bits
+// 25-30: k-major butterfly order of middle stages 1-6 (k2_kmj); bit 31:
 // zero-padded row (general bucket prime: FFT length M >= 2 (P - 1) - 1, the P - 1
 // valid samples first, x0 at row[P - 1])
 template <int NT, int MINB, unsigned TWF, int... Rs>

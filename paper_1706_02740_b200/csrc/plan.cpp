@@ -279,6 +279,48 @@ static void choose_k2_dims(Bucket& b, std::vector<int>& rad) {
   b.twf &= ~(1u << (rad.size() - 1));  // the turn stage has no twiddle table
 }
 
+// Shared-memory wavefronts of one middle stage of k2_ct (span N, radix R, NT threads,
+// one value per butterfly r; every r has the same bank pattern): 16-B accesses are
+// served per quarter warp (8 lanes), and a quarter costs as many wavefronts as the most
+// distinct 16-B words it puts on one of the 8 bank groups (word mod 8).  This model
+// reproduces ncu's l1tex__data_bank_conflicts_pipe_lsu_mem_shared share of every
+// BASELINE config 2 K2 launch to within 1.5 points (profiles/r2e_ncu_full.md: 2.8 %,
+// 28.2 %, 22.8 %, 3.6 %, 4.4 %).
+static long k2_stage_wavefronts(int M, int N, int R, int NT, bool kmajor) {
+  const int m = N / R, nbf = M / R, nblk = M / N;
+  long wf = 0;
+  for (int w0 = 0; w0 < nbf; w0 += 32)
+    for (int q = 0; q < 4; ++q) {
+      int cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      for (int l = 8 * q; l < 8 * q + 8 && w0 + l < nbf; ++l) {
+        const int beta = w0 + l;
+        const int blk = kmajor ? beta % nblk : beta / m, k = kmajor ? beta / nblk : beta % m;
+        ++cnt[(blk * N + k) & 7];  // 8 lanes: distinct butterflies touch distinct words
+      }
+      wf += *std::max_element(cnt, cnt + 8);
+    }
+  (void)NT;  // warps are 32 consecutive betas whatever the CTA size
+  return wf;
+}
+
+// Butterfly order of each middle stage (1 .. min(F - 2, 6)) of a single-CTA row: k-major
+// where it needs fewer wavefronts (bitwise the same row either way).  BASELINE config
+// 2: P = 4057 [8 | 13, 13 | 3] and P = 4357 [4 | 11, 11 | 9] lose their bank conflicts
+// (stage 2 of span 39 / 99: 2.0x / 1.8x the conflict-free wavefronts).
+static unsigned k2_bank_orders(const Bucket& b) {
+  if (b.cl || b.split || b.nfac < 3) return 0;
+  unsigned kmj = 0;
+  int span = b.M;
+  for (int S = 0; S + 1 < b.nfac; ++S) {
+    if (S >= 1 && S <= 6 &&
+        k2_stage_wavefronts(b.M, span, b.fac[S], b.fft_threads, true) <
+            k2_stage_wavefronts(b.M, span, b.fac[S], b.fft_threads, false))
+      kmj |= 1u << S;
+    span /= b.fac[S];
+  }
+  return kmj;
+}
+
 // K2 layout (DESIGN.md §6 K2): radices of choose_radices, CTA-wide stages.
 // Instantiation by shared-memory fit: <64,8> small rows, <256,2> two rows per
 // SM (8 warps, 128 registers: 4 warps per SM sub-partition), <512,1> one row per
@@ -616,6 +658,7 @@ static dsft_status derive(int64_t N, int64_t s, const dsft_params& prm, Plan& P)
     if (!choose_k2_layout(b, rad, (prm.flags & DSFT_FLAG_NO_CLUSTER) != 0)) return fail(DSFT_ERR_UNSUPPORTED, "too many K2 FFT stages");
     b.nfac = (int)rad.size();
     for (int i = 0; i < b.nfac; ++i) b.fac[i] = rad[i];
+    b.kmj = k2_bank_orders(b);
     if (b.ndim == 1) {
       b.dim_m[0] = b.M;
       b.dim_s0[0] = 0;
@@ -869,7 +912,8 @@ static void specialise_k2(Plan& P) {
       //  * the odd CTAs of the first wave started 4 us late (so the wave's row loads and
       //    FFT passes are not in lockstep across the GPU): 2839 -> 2823.
       bb.k2_jit = jit_k2(nt, minb, bb.fac, bb.nfac, (size_t)bb.M * 16, &why[t], false,
-                         bb.twf | (bb.pad ? 0x80000000u : 0u));  // bit 31: zero-padded rows
+                         bb.twf | (bb.kmj << 24) | (bb.pad ? 0x80000000u : 0u));  // bits 25-30: k-major
+                                                                               // stages; 31: zero-padded rows
     });
   }
   for (auto& x : th) x.join();
