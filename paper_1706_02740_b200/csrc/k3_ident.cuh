@@ -45,12 +45,13 @@ struct K3Params {
   int defer_vote;         // 1: candidates only; K5s counts the votes by probing (one-launch K3)
 };
 
+// x0: the unshifted row's bin (sigma = 0), shared by every residue grid
 template <int R>
-__device__ __forceinline__ void residue_argmax(const double2* __restrict__ col, int64_t P, int sb, double invL,
-                                               int& best, double2& yv) {
+__device__ __forceinline__ void residue_argmax(const double2* __restrict__ col, double2 x0, int64_t P, int sb,
+                                               double invL, int& best, double2& yv) {
   double2 x[R];
   const uint64_t pol = l2_evict_first();  // the last read of Z (K1/K2 wrote it evict_last)
-  x[0] = ld_hint(col, pol);
+  x[0] = x0;
 #pragma unroll
   for (int n = 1; n < R; ++n) x[n] = ld_hint(col + (int64_t)(sb + n - 1) * P, pol);
   dft<R>(x);
@@ -72,11 +73,11 @@ __device__ __forceinline__ void residue_argmax(const double2* __restrict__ col, 
 }
 
 template <int R>
-__device__ __forceinline__ void k3_res(const K3Params& p, int64_t P, const double2* col, int i, int64_t& Rc,
-                                       double2* yv) {
+__device__ __forceinline__ void k3_res(const K3Params& p, int64_t P, const double2* col, double2 x0, int i,
+                                       int64_t& Rc, double2* yv) {
   int b = 0;
   double2 y = make_double2(0.0, 0.0);
-  residue_argmax<R>(col, P, p.shift_base[i], p.invL[i], b, y);
+  residue_argmax<R>(col, x0, P, p.shift_base[i], p.invL[i], b, y);
   Rc += (int64_t)b * p.crtE[i + 1];
   yv[i] = y;
 }
@@ -97,9 +98,10 @@ __device__ __forceinline__ void k3_body(const K3Params& p, int64_t gid) {
   const double2* col = p.Z + (int64_t)v * p.z_vec_stride + (int64_t)j * p.S * P + pos;
   int64_t R = a * p.crtE[0];
   double2 yv[kK3MaxK];
+  const double2 x0 = ld_hint(col, l2_evict_first());  // read once for all residue grids
   if constexpr (sizeof...(Rs) > 0) {
     int i = 0;
-    ((k3_res<Rs>(p, P, col, i, R, yv), ++i), ...);
+    ((k3_res<Rs>(p, P, col, x0, i, R, yv), ++i), ...);
   } else
   for (int i = 0; i < p.K; ++i) {
     int b = 0;
@@ -108,7 +110,7 @@ __device__ __forceinline__ void k3_body(const K3Params& p, int64_t gid) {
     switch (p.r[i]) {
 #define DSFT_RES(RR) \
   case RR:           \
-    if constexpr (RR <= RMAX) residue_argmax<RR>(col, P, sb, p.invL[i], b, y); \
+    if constexpr (RR <= RMAX) residue_argmax<RR>(col, x0, P, sb, p.invL[i], b, y); \
     break;
       DSFT_RES(3) DSFT_RES(5) DSFT_RES(7) DSFT_RES(11) DSFT_RES(13) DSFT_RES(17) DSFT_RES(19) DSFT_RES(23)
       DSFT_RES(29) DSFT_RES(31)
@@ -155,13 +157,19 @@ __device__ __forceinline__ void k3_body(const K3Params& p, int64_t gid) {
     // here).  The accepted set and the masks do not depend on the order.
     if (p.defer_vote) return;  // one-launch K3: K5s counts the votes by probing
     const int64_t bb = (int64_t)v * p.cw_vec_stride + (int64_t)j * p.sumP;
+    // probe the earlier primes' buckets of om four at a time (independent loads: one L2
+    // round trip per four primes), then take the first producer in processing order
     int t0 = p.t;
-    for (int k = 0; k < p.nprev; ++k) {
-      const int t2 = p.prev[k];
-      if (__ldcg(p.cand_w + bb + p.offt[t2] + pmod(om, p.Pt[t2])) == om) {
-        t0 = t2;
-        break;
+    for (int k0 = 0; k0 < p.nprev && t0 == p.t; k0 += 4) {
+      int64_t pw[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int t2 = p.prev[k0 + u < p.nprev ? k0 + u : k0];
+        pw[u] = k0 + u < p.nprev ? __ldcg(p.cand_w + bb + p.offt[t2] + pmod(om, p.Pt[t2])) : kK3Sentinel;
       }
+#pragma unroll
+      for (int u = 3; u >= 0; --u)
+        if (pw[u] == om) t0 = p.prev[k0 + u];  // descending: the first match wins
     }
     if (t0 == p.t) mk = 1ull << p.t;
     else atomicOr((unsigned long long*)(p.vmask + bb + p.offt[t0] + pmod(om, p.Pt[t0])), 1ull << p.t);
