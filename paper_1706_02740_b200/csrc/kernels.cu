@@ -246,6 +246,9 @@ __device__ __forceinline__ void k1_mix_node(const K1Params& p, const K1Prime& pp
   }
 }
 
+// (measured round 2, session 3: six CTAs per SM via __launch_bounds__(128, 6) -- 80
+// registers, 36 B of spill stores -- so that a prime's 1235 CTAs need 1.4 waves instead
+// of 1.7: K1 144.5 -> 154.6 us per transform serial, 2978 -> 2881 transforms/s; not kept)
 template <int KAPPA, typename IdxT>
 __global__ void __launch_bounds__(kK1FastThreads) k1_gather_mix_fast(const __grid_constant__ K1Params p) {
   constexpr int W = 2 * KAPPA + 1;
