@@ -381,6 +381,10 @@ bool choose_k2_layout(Bucket& b, std::vector<int>& rad, bool no_cluster) {
   if ((int)rad.size() > kMaxFac) return false;
   if (M <= 1200) b.fft_variant = 0, b.fft_threads = 64;
   else if ((size_t)2 * ((size_t)M * 16 + 2048) <= 228 * 1024) b.fft_variant = 1, b.fft_threads = 256;
+  // (round 2, session 3: 544 threads for P = 7561 [8 | 15, 9 | 7] would cut the turn's
+  // butterfly rounds from three to two, but 17 warps put five on one SM sub-partition,
+  // whose 16 K registers then allow 96 per thread (the kernel needs 114): the launch
+  // fails; CTA sizes stay multiples of 128)
   else b.fft_variant = 2, b.fft_threads = 512;
   b.fft_group = 1;
   return true;
