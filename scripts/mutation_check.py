@@ -19,7 +19,8 @@ import tempfile
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
-# (name, file, old, new) -- each `old` must occur exactly once
+# (name, file, old, new) -- an `old` that occurs n > 1 times (the same line in vote() and in
+# the CLW-style vote) gives n mutants, one per occurrence ("name #k")
 MUTANTS = [
     ("vote >= 1", "oracle/dsft.py", "len(voters(plan, ids, om)) >= plan.vote_min)",
      "len(voters(plan, ids, om)) >= 1)"),
@@ -68,13 +69,21 @@ def main() -> int:
     with tempfile.TemporaryDirectory() as tmp:
         dst = os.path.join(tmp, "repo")
         shutil.copytree(ROOT, dst, ignore=shutil.ignore_patterns(".git", "gpurun_out", "profiles", "*.so", "build*"))
+        expanded = []
         for name, rel, old, new in MUTANTS:
+            orig = open(os.path.join(ROOT, rel)).read()
+            n = orig.count(old)
+            assert n >= 1, (name, n)
+            pos = -1
+            for k in range(n):
+                pos = orig.index(old, pos + 1)
+                mutated = orig[:pos] + new + orig[pos + len(old):]
+                expanded.append((name if n == 1 else f"{name} #{k + 1}", rel, orig, mutated))
+        for name, rel, orig, mutated in expanded:
             if a.k and a.k not in name:
                 continue
             path = os.path.join(dst, rel)
-            orig = open(os.path.join(ROOT, rel)).read()
-            assert orig.count(old) == 1, (name, orig.count(old))
-            open(path, "w").write(orig.replace(old, new))
+            open(path, "w").write(mutated)
             r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "not gpu", "tests",
                                 "--ignore=tests/test_abi.py", "--ignore=tests/test_dist_gloo.py"],
                                cwd=dst, capture_output=True, text=True)
