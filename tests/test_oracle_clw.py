@@ -143,18 +143,21 @@ def test_clw_band_edges():
     assert sorted(res.freqs[:n].tolist()) == freqs and np.all(np.abs(res.coeffs[n:]) < 1e-6)
 
 
-def test_identify_clw_matches_decode_per_bucket():
-    """identify_clw = clw_decode in every bucket followed by the passband and B (line 10)."""
+@pytest.mark.parametrize("j,t", [(4, 1), (0, 0), (7, 3), (14, 4)])
+def test_identify_clw_matches_decode_per_bucket(j, t):
+    """identify_clw = clw_decode in every bucket followed by the passband and B (line 10);
+    the decision margins agree too (they cover the buckets whose circular estimate sits at
+    the ends of q + B, where only the lifts by -N / +N find the nearest representative:
+    those candidates fall outside the passband, so only the margin shows the lift)."""
     N, s = 4096, 8
     plan = derive_plan(N, s, OracleParams(inner="clw", seed=2))
     pl = planted(N, s, cfg=64, trial=1)
-    j = 4
     q = plan.q[j]
-    t = 1
     P = plan.primes[t]
     Et = [alias_dft(filtered_samples(pl.f, plan, q, P, m)) for m in plan.shifts[t]]
     ids = identify_clw(plan, j, t, Et)
     for b in range(P):
-        om, _ = clw_decode([E[b] for E in Et], plan.shifts[t], b, P, q, N)
+        om, margin = clw_decode([E[b] for E in Et], plan.shifts[t], b, P, q, N)
         keep = om != SENTINEL and q - plan.w <= om < q + plan.w and plan.B_lo <= om <= plan.B_hi
         assert ids.cand[b] == (om if keep else SENTINEL)
+        assert abs(ids.gap[b] - margin) <= 1e-9 or ids.gap[b] == margin  # (inf == inf: empty bucket)
