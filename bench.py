@@ -188,6 +188,23 @@ def window_entries(info, N: int) -> list[int]:
     return out
 
 
+def workload_config(N, s, units, mode, world, pool, J, T, primes, nodes):
+    """The `config` object of the JSON line.  Both arms print the same one (the
+    reference arm derives J, T, primes and nodes from the oracle's own plan; the ABI
+    test pins the two derivations to each other), so the driver's same-config check
+    compares like with like; the entries that describe the GPU arm's timing say so."""
+    return {"workload": f"BASELINE config 2: N=2^{int(math.log2(N))} complex128, s={s}, noiseless, "
+                        "dmsft6 (kappa=6, tau=1/3, c_b=4, T=5, v_min=3)",
+            "global_batch": units, "mode": mode,
+            "parallelism": {"single": "one vector per step, one process (GPU arm: 1 GPU)",
+                            "batched-sharded": f"{world} vectors, 1 per GPU, results allgathered (NCCL) every step",
+                            "band-sharded": f"1 vector, J bands over {world} GPUs, band blocks allgathered (NCCL)"}[mode],
+            "pool": pool,
+            "l2": "GPU arm: flushed (256 MiB write) between steps, outside the timed events; f is 1 GiB",
+            "J": int(J), "T": int(T), "primes": [int(x) for x in primes], "nodes": int(nodes)}
+
+
+
 # ------------------------------------------------------------------ reference
 def run_reference(a):
     """--impl reference: the oracle (numpy, CPU) as it stands, on this host."""
@@ -203,6 +220,10 @@ def run_reference(a):
     pl = planted(N, s, cfg=2, trial=0)
     pool = a.pool or "smooth"
     plan = derive_plan(N, s, OracleParams(seed=a.seed, pool_rule=pool))
+    if plan.inner == "clw":
+        ref_nodes = sum(P * len(sh) for P, sh in zip(plan.primes, plan.shifts))
+    else:
+        ref_nodes = sum(P * (1 + sum(r - 1 for r in rs)) for P, rs in zip(plan.primes, plan.residues))
     times = []
     for k in range(a.warmup + a.steps):
         j = k % plan.J
@@ -217,9 +238,7 @@ def run_reference(a):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": band_s * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"BASELINE config 2: N=2^{int(math.log2(N))} complex128, s={s}, noiseless, "
-                               "dmsft6 (kappa=6, tau=1/3, c_b=4, T=5, v_min=3)",
-                   "global_batch": 1, "parallelism": "single host process", "pool": pool},
+        "config": workload_config(N, s, 1, "single", 1, pool, plan.J, plan.T, plan.primes, ref_nodes),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "host_cores": os.cpu_count(), "kind": "oracle",
                          "sample": f"each step = one of the J={plan.J} bands of Algorithm 1 (oracle.process_band); "
                                    "value = 1/(J * mean band time)"},
@@ -488,15 +507,7 @@ def run_ours(a):
         "ms_per_step": ms, "higher_is_better": True, "scaling": "strong" if mode == "band-sharded" else "weak",
         "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (dsft_synth: s unit-magnitude random-phase tones on B, seeded)",
-        "config": {"workload": f"BASELINE config 2: N=2^{int(math.log2(N))} complex128, s={s}, noiseless, "
-                               "dmsft6 (kappa=6, tau=1/3, c_b=4, T=5, v_min=3)",
-                   "global_batch": units, "mode": mode,
-                   "parallelism": {"single": "1 GPU", "batched-sharded": f"{world} vectors, 1 per GPU, results "
-                                   "allgathered (NCCL) every step", "band-sharded": f"1 vector, J bands over "
-                                   f"{world} GPUs, band blocks allgathered (NCCL)"}[mode],
-                   "pool": pool,
-                   "l2": "flushed (256 MiB write) between steps, outside the timed events; f is 1 GiB",
-                   "J": info.J, "T": info.T, "primes": list(info.primes[:info.T]), "nodes": info.nodes},
+        "config": workload_config(N, s, units, mode, world, pool, info.J, info.T, info.primes[:info.T], info.nodes),
         "gpu_launches": launches,
         "roofline": {"kernel": "k2_prime_dft", "bound": "alu", "achieved": k2_achieved, "peak": FP64_PEAK_TFLOPS,
                      "unit": "TFLOP/s", "frac": k2_achieved / FP64_PEAK_TFLOPS, "traffic": k2_traffic,
